@@ -1,0 +1,71 @@
+"""The five BASELINE.json workloads and scaled-down
+variants of the same operator families used for element-wise parity tests.
+
+``build(name)`` returns ``(A: CSR, b: ndarray, interval: (a, b) or None)``.
+The interval is the operator's closed-form spectral interval (problem data; the
+3D Laplacian formula is PAPER.md:419), passed to the Chebyshev construction.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from . import operators as ops
+from .vectors import gaussian_vector
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    family: str                  # "laplacian" | "convdiff" | "wilson"
+    params: dict = field(default_factory=dict)
+    func: str = "invsqrt"        # "invsqrt" | "sqrt"   (sqrt = A^{-1/2}(Ab))
+    degs: tuple = (4,)           # degree of q (deg = d-1 in the paper's notation, reading Q1)
+    krylov: str = "lanczos"      # "lanczos" | "cgs2"
+    poly: str = "chebyshev"      # "chebyshev" | "ritz"
+    tol: float = 1e-8
+    m_max: int = 60
+    b_seed: int = 0
+
+    @property
+    def complex_(self) -> bool:
+        return self.family == "wilson"
+
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "C1": Config("C1", "laplacian", dict(N=32, dim=2), "invsqrt", (4,), "lanczos", "chebyshev", 1e-10, 60, 101),
+    "C2": Config("C2", "convdiff", dict(N=256, dim=2, beta=(20.0, 20.0)), "sqrt", (5, 10, 20), "cgs2",
+                 "chebyshev", 1e-8, 120, 102),
+    "C3": Config("C3", "laplacian", dict(N=200, dim=3), "invsqrt", (10, 20, 40), "lanczos", "chebyshev",
+                 1e-8, 80, 103),
+    "C4": Config("C4", "convdiff", dict(N=256, dim=3, beta=(10.0, 10.0, 10.0)), "sqrt", (20,), "cgs2",
+                 "chebyshev", 1e-8, 60, 104),
+    "C5": Config("C5", "wilson", dict(L=16, m0=-1.0, link_seed=205), "invsqrt", (16,), "cgs2", "ritz",
+                 1e-8, 30, 105),
+    # scaled-down members of the same families (oracle finishes in seconds)
+    "C3s": Config("C3s", "laplacian", dict(N=30, dim=3), "invsqrt", (10, 20), "lanczos", "chebyshev",
+                  1e-8, 80, 203),
+    "C4s": Config("C4s", "convdiff", dict(N=32, dim=3, beta=(10.0, 10.0, 10.0)), "sqrt", (20, 5), "cgs2",
+                  "chebyshev", 1e-8, 60, 204),
+    "C5s": Config("C5s", "wilson", dict(L=4, m0=-1.0, link_seed=305), "invsqrt", (16, 4), "cgs2", "ritz",
+                  1e-8, 30, 205),
+}
+
+
+def operator(cfg: Config):
+    p = cfg.params
+    if cfg.family == "laplacian":
+        return ops.laplacian(p["N"], p["dim"]), ops.laplacian_interval(p["N"], p["dim"])
+    if cfg.family == "convdiff":
+        return (ops.convdiff(p["N"], p["dim"], p["beta"]),
+                ops.convdiff_interval(p["N"], p["dim"], p["beta"]))
+    if cfg.family == "wilson":
+        return ops.wilson_dirac(p["L"], p["m0"], seed=p["link_seed"]), None
+    raise ValueError(cfg.family)
+
+
+def build(name_or_cfg):
+    cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
+    A, interval = operator(cfg)
+    b = gaussian_vector(A.n, cfg.b_seed, cfg.complex_)
+    return A, b, interval

@@ -1,0 +1,156 @@
+"""Pins for oracle/chebyshev.py and oracle/newton.py against the paper's printed
+numbers (§3.2 worked example), closed forms and textbook special cases."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from inputs import operators as ops
+from oracle import chebyshev, newton, reference
+from oracle.spmv import Operator
+
+from .conftest import GOLDEN
+
+
+def test_sec32_worked_example():
+    """κ(A) ≈ 1054, ε = 0.1263, κ_pre ≤ 1.7345, κ_pre = 1.5153."""
+    g = json.load(open(os.path.join(GOLDEN, "sec3_2_example.json")))
+    N = g["grid_N"]
+    a, b = ops.laplacian_interval(N, 2)
+    assert abs(b / a - g["kappa_A"]) < 1.0                           # "≈ 1054" (1053.48)
+    q = chebyshev.coefficients(a, b, g["d"] - 1)
+    z = np.linspace(a, b, 400001)
+    eps = np.max(np.abs(1.0 - np.sqrt(z) * chebyshev.evaluate(q, z)))
+    assert abs(eps - g["epsilon"]) < g["tol_epsilon"]
+    bound = (1 + 2 * eps + eps**2) / (1 - 2 * eps - eps**2)          # Prop 3.2
+    assert abs(bound - g["kappa_pre_bound"]) < g["tol_kappa_pre_bound"]
+    k = np.arange(1, N + 1)
+    mu = 2 - 2 * np.cos(k * np.pi / (N + 1))
+    lam = (mu[:, None] + mu[None, :]).ravel()                        # closed-form spec(A)
+    pre = lam * chebyshev.evaluate(q, lam) ** 2                      # spec(A q(A)^2)
+    assert abs(pre.max() / pre.min() - g["kappa_pre"]) < g["tol_kappa_pre"]
+    # Prop 3.2's interval contains the preconditioned spectrum
+    assert pre.min() >= 1 - 2 * eps - eps**2 - 1e-12 and pre.max() <= 1 + 2 * eps + eps**2 + 1e-12
+
+
+def test_chebyshev_closed_form_evaluation():
+    """q(z) = Σ c_i cos(i arccos t): the closed form of T_i on [-1, 1]."""
+    q = chebyshev.coefficients(0.3, 17.0, 25)
+    z = np.linspace(0.3, 17.0, 1001)
+    t = np.clip((2 * z - 0.3 - 17.0) / (17.0 - 0.3), -1, 1)
+    ref = sum(q.c[i] * np.cos(i * np.arccos(t)) for i in range(26))
+    assert np.abs(chebyshev.evaluate(q, z) - ref).max() < 1e-13
+
+
+def test_chebyshev_interpolates_at_nodes():
+    """The d-point rule makes q interpolate z^{-1/2} at the first-kind nodes (F1)."""
+    a, b, deg = 0.05, 9.0, 12
+    q = chebyshev.coefficients(a, b, deg)
+    d = deg + 1
+    th = np.pi * (np.arange(d) + 0.5) / d
+    zl = (a + b) / 2 + (b - a) / 2 * np.cos(th)
+    assert np.abs(chebyshev.evaluate(q, zl) - zl**-0.5).max() < 1e-12 * np.max(zl**-0.5)
+    # and matches numpy's independent interpolant construction
+    from numpy.polynomial import chebyshev as npc
+    c_np = npc.chebinterpolate(lambda t: ((a + b) / 2 + (b - a) / 2 * t) ** -0.5, deg)
+    assert np.abs(c_np - q.c).max() < 1e-13
+
+
+def test_chebyshev_degree0_and_certificate():
+    q = chebyshev.coefficients(1.0, 1.0 + 1e-12, 0)
+    assert q.c[0] == pytest.approx(1.0, rel=1e-11)
+    a, b = ops.laplacian_interval(50, 2)
+    assert chebyshev.certify(chebyshev.coefficients(a, b, 31)) > 0
+    pts = chebyshev.certificate_points(2.0, 5.0)
+    assert len(pts) == 1001 and pts[0] == 2.0 and pts[-1] == 5.0
+
+
+def test_chebyshev_apply_vs_dst_closed_form():
+    """O3 chain: q(A)b = S q(Λ) S b for the Dirichlet Laplacian (R1 eigenbasis)."""
+    import scipy.fft as sfft
+    N = 20
+    A = ops.laplacian(N, 2)
+    a, b = ops.laplacian_interval(N, 2)
+    q = chebyshev.coefficients(a, b, 9)
+    v = np.random.default_rng(4).standard_normal(N * N)
+    op = Operator(A.to_scipy())
+    got = chebyshev.apply(q, op, v)
+    assert op.mvms == 9                                               # deg mvms
+    k = np.arange(1, N + 1)
+    mu = 2 - 2 * np.cos(k * np.pi / (N + 1))
+    lam = mu[:, None] + mu[None, :]
+    t = np.clip((2 * lam - a - b) / (b - a), -1, 1)
+    qlam = sum(q.c[i] * np.cos(i * np.arccos(t)) for i in range(10))
+    ref = sfft.idstn(sfft.dstn(v.reshape(N, N), type=1, norm="ortho") * qlam, type=1,
+                     norm="ortho").ravel()
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < 1e-13
+
+
+def test_newton_two_nodes_spec_example():
+    """nodes {1,4} ⇒ q(z) = 7/6 - z/6; S:335-336 q(diag(1,4))(1,1) = (1, 1/2)."""
+    q = newton.from_nodes([1.0, 4.0])
+    z = np.array([0.0, 1.0, 4.0, 10.0])
+    assert np.allclose(newton.evaluate(q, z), 7 / 6 - z / 6, atol=1e-15)
+    import scipy.sparse as sp
+    op = Operator(sp.csr_matrix(np.diag([1.0, 4.0]).astype(np.complex128)))
+    out = newton.apply(q, op, np.array([1.0, 1.0]))
+    assert np.allclose(out, [1.0, 0.5], atol=1e-15)
+
+
+def test_newton_interpolation_property_lagrange():
+    """q(θ_i) = θ_i^{-1/2} and agreement with the Lagrange form everywhere."""
+    rng = np.random.default_rng(9)
+    th = 3.0 + 2.0 * (rng.random(12) * np.exp(2j * np.pi * rng.random(12)))
+    q = newton.from_nodes(th)
+    assert np.abs(newton.evaluate(q, q.nodes) - q.nodes**-0.5).max() < 1e-10
+    z = 3.0 + 1.5 * np.exp(1j * np.linspace(0, 2 * np.pi, 50))
+    lag = np.zeros_like(z)
+    for i, ti in enumerate(th):
+        li = np.ones_like(z)
+        for j, tj in enumerate(th):
+            if j != i:
+                li = li * (z - tj) / (ti - tj)
+        lag = lag + ti**-0.5 * li
+    assert np.abs(newton.evaluate(q, z) - lag).max() < 1e-9
+
+
+def test_leja_order_properties():
+    th = np.array([1.0, 2.0, 3.0, 4.0 + 0j, 2.5 + 1j])
+    order = newton.leja_order(th)
+    assert order[0] == 4.0
+    # second point maximises distance to the first
+    assert order[1] == 1.0
+    assert sorted(map(complex, order), key=lambda c: (c.real, c.imag)) == \
+        sorted(map(complex, th), key=lambda c: (c.real, c.imag))
+
+
+def test_newton_apply_matches_dense_polynomial():
+    """Newton apply vs dense evaluation Σ dd_j Π (A - θ_i) v."""
+    rng = np.random.default_rng(1)
+    n = 30
+    M = rng.standard_normal((n, n)) / np.sqrt(n) + 3 * np.eye(n)
+    import scipy.sparse as sp
+    op = Operator(sp.csr_matrix(M.astype(np.complex128)))
+    q = newton.from_nodes(np.linalg.eigvals(M[:8, :8]) + 0.0)
+    v = rng.standard_normal(n) + 0j
+    P = np.zeros((n, n), dtype=complex)
+    prod = np.eye(n, dtype=complex)
+    for j in range(q.deg + 1):
+        P += q.dd[j] * prod
+        prod = prod @ (M - q.nodes[j] * np.eye(n))
+    assert np.linalg.norm(newton.apply(q, op, v) - P @ v) < 1e-11 * np.linalg.norm(P @ v)
+
+
+def test_ritz_values_are_eigs_of_hessenberg_and_branch_check():
+    rng = np.random.default_rng(2)
+    n = 40
+    M = np.diag(np.linspace(1, 10, n)) + 0.1 * rng.standard_normal((n, n))
+    import scipy.sparse as sp
+    op = Operator(sp.csr_matrix(M))
+    H, ips = newton.arnoldi_plain(op, rng.standard_normal(n), n)
+    th = np.sort_complex(newton.ritz_values(H[:n, :n]))
+    ev = np.sort_complex(np.linalg.eigvals(M).astype(complex))
+    assert np.abs(th - ev).max() < 1e-8                               # full space: Ritz = eig
+    with pytest.raises(newton.BranchError):
+        newton.ritz_values(np.diag([1.0, -2.0]))
