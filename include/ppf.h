@@ -1,0 +1,250 @@
+/*
+ * ppf.h -- polynomially preconditioned f(A)b, C ABI of the B200 hot path.
+ *
+ * Method: Frommer, Ramirez-Hidalgo, Schweitzer, Tsolakis, "Polynomial
+ * preconditioning for the action of the matrix square root and inverse square
+ * root" (arXiv 2401.06684).  Citations "P:n" are lines of that paper's
+ * PAPER.md; "Qn" are the readings listed in DESIGN.md §3.
+ *
+ *   Algorithm 1: c = q(A)s, v_1 = c/||c||; for j = 1..m:
+ *     u = A v_j, y = q(A)u, w = q(A)y (three stages);
+ *     orthogonalise w against v_1..v_j (H_m upper Hessenberg);
+ *     h_{j+1,j} = ||w||, v_{j+1} = w/h_{j+1,j};
+ *   f_m = V_m (H_m^{-1/2} e_1 ||c||)
+ *   with s = b for f(z) = z^{-1/2} and s = A b for f(z) = z^{1/2}.
+ *
+ * Conventions shared by every entry point
+ *   - Every function returns ppf_status; no C++ exception crosses the ABI.
+ *     PPF_OK = 0.  On any other status ppf_last_error() (thread-local) holds a
+ *     one-line description.  Output arguments are untouched on failure.
+ *   - Scalars are double (PPF_R64) or interleaved (re, im) double pairs
+ *     (PPF_C128, C99 double _Complex layout).
+ *   - Index arrays are 0-based int64.  A matrix is given as this rank's
+ *     contiguous row slab [row0, row0 + n_local) of a global n_global x n_global
+ *     matrix in CSR form with GLOBAL column indices sorted within each row.
+ *   - "device" pointers are CUDA device memory owned by the caller (PyTorch
+ *     allocations), 256-byte aligned, valid for the duration of the call and of
+ *     the stream work it enqueues.  The library never calls cudaMalloc or
+ *     cudaFree; size-query functions say how much the caller must provide.
+ *     "host" pointers are ordinary host memory, only read/written during the
+ *     call (the library copies what it needs).
+ *   - Vectors passed to ppf_run are this rank's slab (n_local entries).
+ *   - Work is enqueued on the context's CUDA stream.  A context is not
+ *     thread-safe: use one per host thread.
+ */
+#ifndef PPF_H_
+#define PPF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPF_ABI_VERSION 1
+
+typedef enum {
+  PPF_OK = 0,
+  PPF_EINVAL = 1,          /* invalid argument (see ppf_last_error) */
+  PPF_ECUDA = 2,           /* CUDA runtime error */
+  PPF_ENCCL = 3,           /* NCCL error */
+  PPF_EWORKSPACE = 4,      /* caller-provided buffer too small */
+  PPF_EBRANCH = 5,         /* a node / eigenvalue of H_m lies on (-inf, 0], or the
+                              positivity certificate of q failed */
+  PPF_EDENSE = 6,          /* host dense eigen/Schur iteration did not converge */
+  PPF_ESTATE = 7           /* object used in the wrong state / mismatched objects */
+} ppf_status;
+
+typedef enum { PPF_R64 = 0, PPF_C128 = 1 } ppf_dtype;
+typedef enum { PPF_INVSQRT = 0, PPF_SQRT = 1 } ppf_func;            /* SQRT = A^{-1/2}(A b) */
+typedef enum { PPF_LANCZOS = 0, PPF_ARNOLDI_CGS2 = 1 } ppf_krylov;  /* reading Q8 */
+typedef enum { PPF_STOP_FIXED_M = 0, PPF_STOP_EST = 1, PPF_STOP_TRUE_ERR = 2 } ppf_stop;
+typedef enum { PPF_CONVERGED = 0, PPF_MAX_ITER = 1, PPF_BREAKDOWN = 2 } ppf_term;
+typedef enum { PPF_POLY_CHEBYSHEV = 0, PPF_POLY_NEWTON = 1 } ppf_poly_kind;
+typedef enum { PPF_FMT_SELL = 0, PPF_FMT_CSR = 1 } ppf_format;
+
+typedef struct ppf_ctx ppf_ctx;
+typedef struct ppf_plan ppf_plan;
+typedef struct ppf_mat ppf_mat;
+typedef struct ppf_poly ppf_poly;
+
+const char* ppf_status_string(int status);
+const char* ppf_last_error(void);
+int ppf_abi_version(void);
+
+/* ----------------------------------------------------------------------------
+ * Context: one per GPU / rank.
+ * ppf_nccl_unique_id: writes 128 bytes (an ncclUniqueId) to host `out128`; call
+ *   on rank 0 and broadcast the bytes (e.g. torch.distributed) to the others.
+ * ppf_ctx_create: device = CUDA ordinal; cuda_stream = cudaStream_t to enqueue
+ *   on (NULL = the legacy default stream).  nranks > 1 requires id128 (the
+ *   broadcast unique id) and initialises an NCCL communicator; nranks == 1
+ *   ignores id128.
+ * ------------------------------------------------------------------------- */
+ppf_status ppf_nccl_unique_id(void* out128);
+ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128,
+                          void* cuda_stream, ppf_ctx** out);
+void ppf_ctx_destroy(ppf_ctx* ctx);
+
+/* ----------------------------------------------------------------------------
+ * Operator A (layer L0).  Host-only planning, then upload.
+ *
+ * ppf_plan_create: host-side conversion of this rank's CSR slab into the
+ *   device layout.  row_bounds[nranks+1] gives every rank's first row
+ *   (row_bounds[0] = 0, row_bounds[nranks] = n_global, nondecreasing); this
+ *   rank owns [row_bounds[rank], row_bounds[rank+1]).  row_ptr[n_local+1]
+ *   (row_ptr[0] = 0, nondecreasing), col[nnz] (global, sorted per row, in
+ *   [0, n_global)), val[nnz] (dtype scalars).  format: PPF_FMT_SELL uses
+ *   SELL-C-sigma with slice height `sell_C` (32 or 64 for R64, 32 for C128) and
+ *   row-sorting window `sell_sigma` (1 = no sorting, else a multiple of
+ *   sell_C); PPF_FMT_CSR ignores both.  Columns owned by this rank go to the
+ *   diagonal block, others to the off-diagonal (halo) block.  Needs no GPU.
+ * ppf_plan_device_bytes: bytes of device memory ppf_mat_create needs.
+ * ppf_plan_halo_count / ppf_plan_halo_recv: the global indices this rank must
+ *   receive from rank `peer` before each SpMV (sorted, unique).
+ * ppf_plan_set_halo_send: the local row indices this rank sends to `peer`
+ *   (what `peer` reported as its recv list for us, minus row_bounds[rank]);
+ *   the caller exchanges the lists (e.g. torch.distributed) -- host logic only.
+ * ppf_mat_create: uploads the plan into device_buf (>= ppf_plan_device_bytes)
+ *   on the context stream; the plan may be destroyed afterwards.
+ * ppf_spmv: y = A x on this rank's slab (x, y device, n_local entries),
+ *   including the halo exchange; for tests and benchmarks.
+ * ------------------------------------------------------------------------- */
+ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int rank,
+                           const int64_t* row_bounds, const int64_t* row_ptr,
+                           const int64_t* col, const void* val, ppf_format format,
+                           int sell_C, int sell_sigma, ppf_plan** out);
+ppf_status ppf_plan_device_bytes(const ppf_plan* plan, size_t* bytes);
+ppf_status ppf_plan_info(const ppf_plan* plan, int64_t* n_local, int64_t* nnz,
+                         int64_t* stored_entries, int64_t* halo_total);
+ppf_status ppf_plan_halo_count(const ppf_plan* plan, int peer, int64_t* count);
+ppf_status ppf_plan_halo_recv(const ppf_plan* plan, int peer, int64_t* global_idx);
+ppf_status ppf_plan_set_halo_send(ppf_plan* plan, int peer, int64_t count,
+                                  const int64_t* local_rows);
+void ppf_plan_destroy(ppf_plan* plan);
+
+ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* plan, void* device_buf,
+                          size_t bytes, ppf_mat** out);
+ppf_status ppf_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
+void ppf_mat_destroy(ppf_mat* A);
+
+/* ----------------------------------------------------------------------------
+ * Preconditioning polynomial q ~ z^{-1/2} (layer L1), a host object.
+ *
+ * ppf_poly_chebyshev (reading Q2): the degree-`deg` Chebyshev
+ *   interpolant of z^{-1/2} at the deg+1 first-kind points of [a, b]
+ *   (= the coefficient integrals of P:329 by (deg+1)-point Gauss-Chebyshev
+ *   quadrature).  Certificate: q > 0 at z_k = a + (b-a)k/1000, k = 0..1000,
+ *   else PPF_EBRANCH.  Requires 0 < a < b, 0 <= deg <= 256.
+ * ppf_poly_ritz_newton: runs deg+1 Arnoldi steps with A started
+ *   from `start` (device, n_local entries; "started with the vector b"),
+ *   takes the Ritz values (eigenvalues of H_{deg+1}), rejects any on
+ *   (-inf, 0] (PPF_EBRANCH), Leja-orders them (max modulus first, then
+ *   greedy max sum log|theta - chosen|, ties to the smaller index after sorting
+ *   by (Re, Im)) and forms the divided differences of z^{-1/2}.  `work` is
+ *   device scratch of at least ppf_ritz_workspace_bytes.  Always complex.
+ * ppf_poly_import: kind CHEBYSHEV: ab = {a, b}, coef = deg+1 doubles, nodes
+ *   ignored.  kind NEWTON: coef = deg+1 complex divided differences, nodes =
+ *   deg+1 complex Leja-ordered nodes, ab ignored.  No certificate is applied.
+ * ppf_poly_export: the same layout (caller buffers of deg+1 entries; query deg
+ *   first with coef = nodes = NULL).
+ * ppf_poly_eval: q at `npts` complex points (host, interleaved) -> host out.
+ * ------------------------------------------------------------------------- */
+ppf_status ppf_poly_chebyshev(double a, double b, int deg, ppf_poly** out);
+ppf_status ppf_ritz_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, int deg, size_t* bytes);
+ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
+                                void* work, size_t work_bytes, ppf_poly** out);
+ppf_status ppf_poly_import(int kind, int deg, const double* ab, const void* coef,
+                           const void* nodes, ppf_poly** out);
+ppf_status ppf_poly_export(const ppf_poly* q, int* kind, int* deg, double* ab,
+                           void* coef, void* nodes);
+ppf_status ppf_poly_eval(const ppf_poly* q, int npts, const double* z, double* out);
+/* y = q(A) x on the device (x, y device, n_local entries, distinct), the fused
+ * SpMV chain of the hot path (Clenshaw P:332 / Newton-Horner P:354): exactly
+ * deg SpMV launches.  `work` is device scratch of ppf_poly_apply_bytes. */
+ppf_status ppf_poly_apply_bytes(ppf_ctx* ctx, const ppf_mat* A, size_t* bytes);
+ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const void* x, void* y,
+                          void* work, size_t work_bytes);
+void ppf_poly_destroy(ppf_poly* q);
+
+/* ----------------------------------------------------------------------------
+ * The run (layers L2-L5): Algorithm 1, f(H_m) on the host, x = V_m y_m.
+ *
+ * opts.func / krylov: see enums.  m_max >= 1 (<= 255).  stop:
+ *   FIXED_M   run exactly m_max steps (unless breakdown);
+ *   EST       stop at the first checkpoint m with the paper's estimate
+ *             ||f_m - f_{m-k}|| / ||f_m|| = ||[y_{m-k};0] - y_m|| / ||y_m|| <= tol
+ *             (P:174), k = check_every;
+ *   TRUE_ERR  stop at the first checkpoint with ||f_m - x_ref|| / ||x_ref|| <= tol
+ *             (x_ref device, n_local entries; for calibrating m*, reading Q11).
+ * breakdown_rtol: h_{j+1,j} <= breakdown_rtol * ||c|| ends the run with
+ *   term = BREAKDOWN (reading Q9; 0 selects 1e-14).
+ * record_history: keep per-checkpoint (m, est, err, mvms) for ppf_history.
+ * Non-convergence and breakdown are not errors (status OK, term says why).
+ *
+ * ppf_workspace_bytes: device scratch `work` needed by ppf_run for these
+ *   (A, q, opts); it holds V (m_max+1 columns), 5 n-vectors and reduction
+ *   scratch.
+ * ppf_run: b, x device (n_local entries).  Enqueues everything on the context
+ *   stream and returns once x has been enqueued; the report is valid on return.
+ * ppf_run_host: the same with b_host / x_host host buffers; the H2D copy of b
+ *   and the D2H copy of x go through the library (pinned staging) and the call
+ *   returns with x_host filled.
+ * ppf_history: per-checkpoint records of the last run (count <= cap).
+ * ppf_hessenberg: the last run's (m+1) x m matrix H (column-major, leading
+ *   dimension ld >= m+1, dtype scalars) and ||c||.  Query m with H = NULL.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int func;            /* ppf_func */
+  int krylov;          /* ppf_krylov */
+  int m_max;
+  int stop;            /* ppf_stop */
+  double tol;
+  int check_every;     /* k >= 1 */
+  const void* x_ref;   /* device, TRUE_ERR only */
+  double breakdown_rtol;
+  int record_history;
+} ppf_opts;
+
+typedef struct {
+  int iterations;              /* m of the returned f_m */
+  int term;                    /* ppf_term */
+  long long mvms;              /* products with A (P:455 unit), incl. c = q(A)s, A b */
+  long long inner_products;     /* norms included, ||c|| not */
+  double est;                  /* last estimate (NaN if none) */
+  double err;                  /* last true error (NaN unless TRUE_ERR) */
+  double beta0;                /* ||c|| */
+  double seconds_total;        /* host wall time of the call */
+  double seconds_host_dense;   /* host time in f(H_m) evaluations */
+  long long kernel_launches;   /* kernels this call launched */
+} ppf_report;
+
+ppf_status ppf_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, const ppf_poly* q,
+                               const ppf_opts* opts, size_t* bytes);
+ppf_status ppf_run(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts* opts,
+                   const void* b, void* x, void* work, size_t work_bytes, ppf_report* rep);
+ppf_status ppf_run_host(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts* opts,
+                        const void* b_host, void* x_host, void* work, size_t work_bytes,
+                        ppf_report* rep);
+ppf_status ppf_history(ppf_ctx* ctx, int cap, int* count, int* m, double* est, double* err,
+                       long long* mvms);
+ppf_status ppf_hessenberg(ppf_ctx* ctx, int ld, void* H, int* m, double* beta0);
+
+/* ----------------------------------------------------------------------------
+ * Host dense kernel (layer L4, K10), exposed for tests:
+ * y = beta0 * H^{-1/2} e_1 for an m x m matrix H (column-major, leading
+ * dimension ld, dtype scalars), principal branch.  hermitian != 0: H is taken
+ * as symmetric tridiagonal (diagonal and first subdiagonal read) and solved by
+ * a tridiagonal eigendecomposition; else complex Schur -> triangular square
+ * root -> triangular solve.  PPF_EBRANCH if an eigenvalue is on
+ * (-inf, 0].  y: m dtype scalars (host).
+ * ------------------------------------------------------------------------- */
+ppf_status ppf_dense_invsqrt_e1(ppf_dtype dtype, int m, const void* H, int ld, double beta0,
+                                int hermitian, void* y);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PPF_H_ */

@@ -1,0 +1,582 @@
+// C ABI entry points (include/ppf.h): errors, context, operator planning and
+// upload, polynomial objects, the host dense kernel.  ppf_run lives in run.cpp.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+
+#include "ppf_internal.h"
+
+namespace ppf {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+[[noreturn]] void fail(ppf_status st, const std::string& msg) { throw Error{st, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(PPF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace ppf
+
+using namespace ppf;
+
+#define PPF_API_BEGIN try {
+#define PPF_API_END                      \
+  return PPF_OK;                         \
+  }                                      \
+  catch (const ppf::Error& e) {          \
+    ppf::set_last_error(e.msg);          \
+    return e.st;                         \
+  }                                      \
+  catch (const std::bad_alloc&) {        \
+    ppf::set_last_error("out of host memory"); \
+    return PPF_EINVAL;                   \
+  }                                      \
+  catch (...) {                          \
+    ppf::set_last_error("unknown C++ exception"); \
+    return PPF_EINVAL;                   \
+  }
+
+extern "C" {
+
+const char* ppf_status_string(int st) {
+  switch (st) {
+    case PPF_OK: return "PPF_OK";
+    case PPF_EINVAL: return "PPF_EINVAL";
+    case PPF_ECUDA: return "PPF_ECUDA";
+    case PPF_ENCCL: return "PPF_ENCCL";
+    case PPF_EWORKSPACE: return "PPF_EWORKSPACE";
+    case PPF_EBRANCH: return "PPF_EBRANCH";
+    case PPF_EDENSE: return "PPF_EDENSE";
+    case PPF_ESTATE: return "PPF_ESTATE";
+    default: return "PPF_UNKNOWN";
+  }
+}
+
+const char* ppf_last_error(void) { return g_last_error.c_str(); }
+int ppf_abi_version(void) { return PPF_ABI_VERSION; }
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+ppf_status ppf_nccl_unique_id(void* out128) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(out128, "out128 is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) fail(PPF_ENCCL, "ncclGetUniqueId failed");
+  std::memcpy(out128, &id, 128);
+  PPF_API_END
+}
+
+ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, void* stream,
+                          ppf_ctx** out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(out, "out is NULL");
+  PPF_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank/nranks");
+  PPF_REQUIRE(nranks == 1 || id128, "nranks > 1 needs the NCCL unique id");
+  PPF_CUDA(cudaSetDevice(device));
+  auto* c = new ppf_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->stream = static_cast<cudaStream_t>(stream);
+  c->nccl_comm = nullptr;
+  c->last_m = 0;
+  c->last_beta0 = 0.0;
+  c->last_dtype = PPF_R64;
+  c->launches = 0;
+  try {
+    PPF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    c->h_pinned_bytes = size_t(258) * 256 * 16 + 16384;
+    PPF_CUDA(cudaHostAlloc(&c->h_pinned, c->h_pinned_bytes, cudaHostAllocDefault));
+    PPF_CUDA(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, id128, 128);
+      ncclComm_t comm;
+      if (ncclCommInitRank(&comm, nranks, id, rank) != ncclSuccess)
+        fail(PPF_ENCCL, "ncclCommInitRank failed");
+      c->nccl_comm = comm;
+    }
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *out = c;
+  PPF_API_END
+}
+
+void ppf_ctx_destroy(ppf_ctx* c) {
+  if (!c) return;
+  if (c->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->ev) cudaEventDestroy(c->ev);
+  delete c;
+}
+
+// ---------------------------------------------------------------------------
+// Plan: host conversion CSR slab -> device layout (diag block SELL or CSR,
+// off-rank columns into a compact halo CSR).
+// ---------------------------------------------------------------------------
+ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int rank,
+                           const int64_t* row_bounds, const int64_t* row_ptr, const int64_t* col,
+                           const void* val, ppf_format format, int sell_C, int sell_sigma,
+                           ppf_plan** out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(out, "out is NULL");
+  PPF_REQUIRE(dtype == PPF_R64 || dtype == PPF_C128, "bad dtype");
+  PPF_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank/nranks");
+  PPF_REQUIRE(row_bounds && row_ptr, "NULL row_bounds/row_ptr");
+  PPF_REQUIRE(n_global >= 1 && n_global < (int64_t(1) << 31), "n_global out of range");
+  PPF_REQUIRE(row_bounds[0] == 0 && row_bounds[nranks] == n_global, "row_bounds must span [0, n)");
+  for (int r = 0; r < nranks; ++r)
+    PPF_REQUIRE(row_bounds[r] <= row_bounds[r + 1], "row_bounds not nondecreasing");
+  const int64_t row0 = row_bounds[rank], n_local = row_bounds[rank + 1] - row0;
+  PPF_REQUIRE(n_local >= 1, "empty row slab");
+  PPF_REQUIRE(row_ptr[0] == 0, "row_ptr[0] != 0");
+  for (int64_t i = 0; i < n_local; ++i)
+    PPF_REQUIRE(row_ptr[i + 1] >= row_ptr[i], "row_ptr not monotone");
+  const int64_t nnz = row_ptr[n_local];
+  PPF_REQUIRE(nnz == 0 || (col && val), "NULL col/val");
+  PPF_REQUIRE(nnz < (int64_t(1) << 40), "nnz too large");
+  for (int64_t i = 0; i < n_local; ++i)
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+      PPF_REQUIRE(col[k] >= 0 && col[k] < n_global, "column index out of range");
+      PPF_REQUIRE(k == row_ptr[i] || col[k] > col[k - 1], "columns not strictly sorted in a row");
+    }
+  PPF_REQUIRE(format == PPF_FMT_SELL || format == PPF_FMT_CSR, "bad format");
+  if (format == PPF_FMT_SELL) {
+    PPF_REQUIRE(sell_C == 32 || (sell_C == 64 && dtype == PPF_R64),
+                "sell_C must be 32 (or 64 for R64)");
+    PPF_REQUIRE(sell_sigma >= 1, "sell_sigma >= 1");
+    PPF_REQUIRE(sell_sigma == 1 || (sell_sigma % sell_C == 0 && sell_C == 32),
+                "sell_sigma must be 1 or a multiple of C (C = 32 when sorting)");
+  }
+  const int ND = dtype == PPF_R64 ? 1 : 2;
+  const double* v = static_cast<const double*>(val);
+
+  auto* p = new ppf_plan();
+  std::unique_ptr<ppf_plan> guard(p);
+  p->dtype = dtype;
+  p->n_global = n_global;
+  p->row0 = row0;
+  p->n_local = n_local;
+  p->nnz = nnz;
+  p->nranks = nranks;
+  p->rank = rank;
+  p->bounds.assign(row_bounds, row_bounds + nranks + 1);
+  p->fmt = format;
+  p->C = format == PPF_FMT_SELL ? sell_C : 1;
+  p->sigma = format == PPF_FMT_SELL ? sell_sigma : 1;
+  p->recv.assign(nranks, {});
+  p->send.assign(nranks, {});
+  const int64_t row1 = row0 + n_local;
+  auto owner = [&](int64_t g) {
+    return int(std::upper_bound(p->bounds.begin(), p->bounds.end(), g) - p->bounds.begin()) - 1;
+  };
+  // diagonal-block row lengths and halo needs
+  std::vector<int64_t> dlen(n_local, 0);
+  int64_t halo_nnz = 0;
+  for (int64_t i = 0; i < n_local; ++i)
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+      if (col[k] >= row0 && col[k] < row1)
+        ++dlen[i];
+      else {
+        ++halo_nnz;
+        p->recv[owner(col[k])].push_back(col[k]);
+      }
+    }
+  p->recv_off.assign(nranks + 1, 0);
+  for (int r = 0; r < nranks; ++r) {
+    auto& rv = p->recv[r];
+    std::sort(rv.begin(), rv.end());
+    rv.erase(std::unique(rv.begin(), rv.end()), rv.end());
+    p->recv_off[r + 1] = p->recv_off[r] + int64_t(rv.size());
+  }
+  // halo block
+  if (halo_nnz) {
+    auto& H = p->halo;
+    H.ptr.push_back(0);
+    for (int64_t i = 0; i < n_local; ++i) {
+      bool any = false;
+      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+        if (col[k] >= row0 && col[k] < row1) continue;
+        const int o = owner(col[k]);
+        const auto& rv = p->recv[o];
+        const int64_t pos = std::lower_bound(rv.begin(), rv.end(), col[k]) - rv.begin();
+        H.col.push_back(int32_t(p->recv_off[o] + pos));
+        for (int d = 0; d < ND; ++d) H.val.push_back(v[k * ND + d]);
+        any = true;
+      }
+      if (any) {
+        H.rows.push_back(int32_t(i));
+        H.ptr.push_back(int64_t(H.col.size()));
+      }
+    }
+  }
+  // diagonal block
+  auto& B = p->diag;
+  B.rows = n_local;
+  if (format == PPF_FMT_CSR) {
+    B.ptr.assign(n_local + 1, 0);
+    for (int64_t i = 0; i < n_local; ++i) B.ptr[i + 1] = B.ptr[i] + dlen[i];
+    B.col.resize(B.ptr[n_local]);
+    B.val.resize(size_t(B.ptr[n_local]) * ND);
+    for (int64_t i = 0; i < n_local; ++i) {
+      int64_t o = B.ptr[i];
+      for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
+        if (col[k] < row0 || col[k] >= row1) continue;
+        B.col[o] = int32_t(col[k] - row0);
+        for (int d = 0; d < ND; ++d) B.val[size_t(o) * ND + d] = v[k * ND + d];
+        ++o;
+      }
+    }
+  } else {
+    const int C = p->C;
+    std::vector<int32_t> perm(n_local);
+    for (int64_t i = 0; i < n_local; ++i) perm[i] = int32_t(i);
+    if (p->sigma > 1) {
+      for (int64_t w0 = 0; w0 < n_local; w0 += p->sigma) {
+        const int64_t w1 = std::min<int64_t>(n_local, w0 + p->sigma);
+        std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                         [&](int32_t a, int32_t b) { return dlen[a] > dlen[b]; });
+      }
+      B.perm = perm;
+    }
+    B.nslices = (n_local + C - 1) / C;
+    B.ptr.assign(B.nslices + 1, 0);
+    for (int64_t s = 0; s < B.nslices; ++s) {
+      int64_t w = 0;
+      for (int64_t pp = s * C; pp < std::min<int64_t>(n_local, (s + 1) * C); ++pp)
+        w = std::max(w, dlen[perm[pp]]);
+      B.ptr[s + 1] = B.ptr[s] + w * C;
+    }
+    const int64_t stored = B.ptr[B.nslices];
+    B.col.assign(stored, 0);
+    B.val.assign(size_t(stored) * ND, 0.0);
+    for (int64_t s = 0; s < B.nslices; ++s) {
+      const int64_t w = (B.ptr[s + 1] - B.ptr[s]) / C;
+      const int32_t pad_col = perm[s * C];
+      for (int lane = 0; lane < C; ++lane) {
+        const int64_t pp = s * C + lane;
+        int64_t k = 0;
+        if (pp < n_local) {
+          const int64_t i = perm[pp];
+          for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+            if (col[e] < row0 || col[e] >= row1) continue;
+            const int64_t idx = B.ptr[s] + k * C + lane;
+            B.col[idx] = int32_t(col[e] - row0);
+            for (int d = 0; d < ND; ++d) B.val[size_t(idx) * ND + d] = v[e * ND + d];
+            ++k;
+          }
+        }
+        for (; k < w; ++k) B.col[B.ptr[s] + k * C + lane] = pad_col;
+      }
+    }
+  }
+  p->sends_set = (nranks == 1);
+  *out = guard.release();
+  PPF_API_END
+}
+
+ppf_status ppf_plan_halo_count(const ppf_plan* p, int peer, int64_t* count) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p && count && peer >= 0 && peer < p->nranks, "bad arguments");
+  *count = int64_t(p->recv[peer].size());
+  PPF_API_END
+}
+
+ppf_status ppf_plan_halo_recv(const ppf_plan* p, int peer, int64_t* idx) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p && peer >= 0 && peer < p->nranks, "bad arguments");
+  PPF_REQUIRE(idx || p->recv[peer].empty(), "idx is NULL");
+  std::copy(p->recv[peer].begin(), p->recv[peer].end(), idx);
+  PPF_API_END
+}
+
+ppf_status ppf_plan_set_halo_send(ppf_plan* p, int peer, int64_t count, const int64_t* rows) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p && peer >= 0 && peer < p->nranks && count >= 0, "bad arguments");
+  PPF_REQUIRE(peer != p->rank || count == 0, "cannot send to self");
+  PPF_REQUIRE(count == 0 || rows, "rows is NULL");
+  for (int64_t i = 0; i < count; ++i)
+    PPF_REQUIRE(rows[i] >= 0 && rows[i] < p->n_local, "send row out of range");
+  p->send[peer].assign(rows, rows + count);
+  p->sends_set = true;
+  PPF_API_END
+}
+
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t ptr, col, val, perm, hrows, hptr, hcol, hval, recv, send, sidx, total;
+};
+
+static Layout layout_of(const ppf_plan* p) {
+  const size_t sc = p->dtype == PPF_R64 ? 8 : 16;
+  Layout L{};
+  size_t o = 0;
+  L.ptr = o;
+  o += al256(p->diag.ptr.size() * 8);
+  L.col = o;
+  o += al256(p->diag.col.size() * 4);
+  L.val = o;
+  o += al256(p->diag.col.size() * sc);
+  L.perm = o;
+  o += al256(p->diag.perm.size() * 4);
+  L.hrows = o;
+  o += al256(p->halo.rows.size() * 4);
+  L.hptr = o;
+  o += al256(p->halo.ptr.size() * 8);
+  L.hcol = o;
+  o += al256(p->halo.col.size() * 4);
+  L.hval = o;
+  o += al256(p->halo.col.size() * sc);
+  int64_t recv_total = p->recv_off.empty() ? 0 : p->recv_off.back();
+  int64_t send_total = 0;
+  for (auto& s : p->send) send_total += int64_t(s.size());
+  L.recv = o;
+  o += al256(size_t(recv_total) * sc);
+  L.send = o;
+  o += al256(size_t(send_total) * sc);
+  L.sidx = o;
+  o += al256(size_t(send_total) * 4);
+  L.total = o;
+  return L;
+}
+
+ppf_status ppf_plan_device_bytes(const ppf_plan* p, size_t* bytes) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p && bytes, "NULL argument");
+  *bytes = layout_of(p).total;
+  PPF_API_END
+}
+
+ppf_status ppf_plan_info(const ppf_plan* p, int64_t* n_local, int64_t* nnz, int64_t* stored,
+                         int64_t* halo_total) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p, "NULL plan");
+  if (n_local) *n_local = p->n_local;
+  if (nnz) *nnz = p->nnz;
+  if (stored) *stored = int64_t(p->diag.col.size()) + int64_t(p->halo.col.size());
+  if (halo_total) *halo_total = p->recv_off.empty() ? 0 : p->recv_off.back();
+  PPF_API_END
+}
+
+void ppf_plan_destroy(ppf_plan* p) { delete p; }
+
+ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t bytes,
+                          ppf_mat** out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(ctx && p && out, "NULL argument");
+  PPF_REQUIRE(p->nranks == ctx->nranks && p->rank == ctx->rank, "plan/context rank mismatch");
+  PPF_REQUIRE(p->sends_set, "halo send lists not set (ppf_plan_set_halo_send)");
+  const Layout L = layout_of(p);
+  PPF_REQUIRE(buf && bytes >= L.total, "device buffer too small");
+  PPF_REQUIRE((reinterpret_cast<uintptr_t>(buf) & 255) == 0, "device buffer not 256-B aligned");
+  const size_t sc = p->dtype == PPF_R64 ? 8 : 16;
+  char* b = static_cast<char*>(buf);
+  cudaStream_t st = ctx->stream;
+  auto up = [&](size_t off, const void* src, size_t n) {
+    if (n) PPF_CUDA(cudaMemcpyAsync(b + off, src, n, cudaMemcpyHostToDevice, st));
+  };
+  up(L.ptr, p->diag.ptr.data(), p->diag.ptr.size() * 8);
+  up(L.col, p->diag.col.data(), p->diag.col.size() * 4);
+  up(L.val, p->diag.val.data(), p->diag.col.size() * sc);
+  up(L.perm, p->diag.perm.data(), p->diag.perm.size() * 4);
+  up(L.hrows, p->halo.rows.data(), p->halo.rows.size() * 4);
+  up(L.hptr, p->halo.ptr.data(), p->halo.ptr.size() * 8);
+  up(L.hcol, p->halo.col.data(), p->halo.col.size() * 4);
+  up(L.hval, p->halo.val.data(), p->halo.col.size() * sc);
+  std::vector<int32_t> sidx;
+  auto* m = new ppf_mat();
+  m->send_count.assign(p->nranks, 0);
+  m->send_off.assign(p->nranks + 1, 0);
+  m->recv_count.assign(p->nranks, 0);
+  m->recv_off.assign(p->recv_off.begin(), p->recv_off.end());
+  for (int r = 0; r < p->nranks; ++r) {
+    m->recv_count[r] = int64_t(p->recv[r].size());
+    m->send_count[r] = int64_t(p->send[r].size());
+    m->send_off[r + 1] = m->send_off[r] + m->send_count[r];
+    for (int64_t x : p->send[r]) sidx.push_back(int32_t(x));
+  }
+  up(L.sidx, sidx.data(), sidx.size() * 4);
+  PPF_CUDA(cudaStreamSynchronize(st));
+  m->ctx = ctx;
+  m->dtype = p->dtype;
+  m->fmt = p->fmt;
+  m->n_global = p->n_global;
+  m->row0 = p->row0;
+  m->n_local = p->n_local;
+  m->nnz = p->nnz;
+  m->stored = int64_t(p->diag.col.size());
+  m->C = p->C;
+  m->sigma = p->sigma;
+  m->nranks = p->nranks;
+  m->rank = p->rank;
+  m->nslices = p->diag.nslices;
+  m->d_ptr = reinterpret_cast<const int64_t*>(b + L.ptr);
+  m->d_col = reinterpret_cast<const int32_t*>(b + L.col);
+  m->d_val = b + L.val;
+  m->d_perm = p->diag.perm.empty() ? nullptr : reinterpret_cast<const int32_t*>(b + L.perm);
+  {
+    const double avg = double(m->stored) / double(std::max<int64_t>(1, p->n_local));
+    int g = 2;
+    while (g < 32 && g < avg) g *= 2;
+    m->csr_group = g;
+  }
+  m->halo_rows = int64_t(p->halo.rows.size());
+  m->halo_nnz = int64_t(p->halo.col.size());
+  m->halo_total = p->recv_off.empty() ? 0 : p->recv_off.back();
+  m->send_total = int64_t(sidx.size());
+  m->d_halo_rows = reinterpret_cast<const int32_t*>(b + L.hrows);
+  m->d_halo_ptr = reinterpret_cast<const int64_t*>(b + L.hptr);
+  m->d_halo_col = reinterpret_cast<const int32_t*>(b + L.hcol);
+  m->d_halo_val = b + L.hval;
+  m->d_recv = b + L.recv;
+  m->d_send = b + L.send;
+  m->d_send_idx = reinterpret_cast<const int32_t*>(b + L.sidx);
+  *out = m;
+  PPF_API_END
+}
+
+void ppf_mat_destroy(ppf_mat* m) { delete m; }
+
+// ---------------------------------------------------------------------------
+// Polynomials
+// ---------------------------------------------------------------------------
+ppf_status ppf_poly_chebyshev(double a, double b, int deg, ppf_poly** out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(out, "out is NULL");
+  PPF_REQUIRE(std::isfinite(a) && std::isfinite(b) && 0.0 < a && a < b, "need 0 < a < b");
+  PPF_REQUIRE(deg >= 0 && deg <= 256, "deg out of range [0, 256]");
+  auto* q = new ppf_poly();
+  std::unique_ptr<ppf_poly> g(q);
+  q->kind = PPF_POLY_CHEBYSHEV;
+  q->deg = deg;
+  q->a = a;
+  q->b = b;
+  chebyshev_coefficients(a, b, deg, q->c);
+  // positivity certificate on z_k = a + (b-a)k/1000
+  double mn = HUGE_VAL;
+  for (int k = 0; k <= 1000; ++k) mn = std::min(mn, chebyshev_eval(*q, a + (b - a) * k / 1000.0));
+  if (!(mn > 0.0)) fail(PPF_EBRANCH, "Chebyshev q is not positive on [a, b]");
+  *out = g.release();
+  PPF_API_END
+}
+
+ppf_status ppf_poly_import(int kind, int deg, const double* ab, const void* coef,
+                           const void* nodes, ppf_poly** out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(out && coef, "NULL argument");
+  PPF_REQUIRE(deg >= 0 && deg <= 256, "deg out of range");
+  auto* q = new ppf_poly();
+  std::unique_ptr<ppf_poly> g(q);
+  q->kind = kind;
+  q->deg = deg;
+  if (kind == PPF_POLY_CHEBYSHEV) {
+    PPF_REQUIRE(ab && ab[0] < ab[1], "bad interval");
+    q->a = ab[0];
+    q->b = ab[1];
+    const double* c = static_cast<const double*>(coef);
+    q->c.assign(c, c + deg + 1);
+  } else if (kind == PPF_POLY_NEWTON) {
+    PPF_REQUIRE(nodes, "nodes is NULL");
+    const double* c = static_cast<const double*>(coef);
+    const double* nd = static_cast<const double*>(nodes);
+    for (int i = 0; i <= deg; ++i) {
+      q->dd.push_back(zc(c[2 * i], c[2 * i + 1]));
+      q->nodes.push_back(zc(nd[2 * i], nd[2 * i + 1]));
+    }
+  } else {
+    fail(PPF_EINVAL, "bad poly kind");
+  }
+  *out = g.release();
+  PPF_API_END
+}
+
+ppf_status ppf_poly_export(const ppf_poly* q, int* kind, int* deg, double* ab, void* coef,
+                           void* nodes) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(q, "NULL poly");
+  if (kind) *kind = q->kind;
+  if (deg) *deg = q->deg;
+  if (q->kind == PPF_POLY_CHEBYSHEV) {
+    if (ab) {
+      ab[0] = q->a;
+      ab[1] = q->b;
+    }
+    if (coef) std::copy(q->c.begin(), q->c.end(), static_cast<double*>(coef));
+  } else {
+    double* c = static_cast<double*>(coef);
+    double* nd = static_cast<double*>(nodes);
+    for (int i = 0; i <= q->deg; ++i) {
+      if (c) {
+        c[2 * i] = q->dd[i].real();
+        c[2 * i + 1] = q->dd[i].imag();
+      }
+      if (nd) {
+        nd[2 * i] = q->nodes[i].real();
+        nd[2 * i + 1] = q->nodes[i].imag();
+      }
+    }
+  }
+  PPF_API_END
+}
+
+ppf_status ppf_poly_eval(const ppf_poly* q, int npts, const double* z, double* out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(q && npts >= 0 && (npts == 0 || (z && out)), "bad arguments");
+  for (int i = 0; i < npts; ++i) {
+    const zc r = poly_eval(*q, zc(z[2 * i], z[2 * i + 1]));
+    out[2 * i] = r.real();
+    out[2 * i + 1] = r.imag();
+  }
+  PPF_API_END
+}
+
+void ppf_poly_destroy(ppf_poly* q) { delete q; }
+
+// ---------------------------------------------------------------------------
+// Host dense kernel
+// ---------------------------------------------------------------------------
+ppf_status ppf_dense_invsqrt_e1(ppf_dtype dtype, int m, const void* H, int ld, double beta0,
+                                int hermitian, void* y) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(H && y && m >= 1 && ld >= m, "bad arguments");
+  const int ND = dtype == PPF_R64 ? 1 : 2;
+  const double* h = static_cast<const double*>(H);
+  double* yo = static_cast<double*>(y);
+  if (hermitian) {
+    std::vector<double> d(m), e(m, 0.0), yy(m);
+    for (int i = 0; i < m; ++i) d[i] = h[(size_t(i) + size_t(i) * ld) * ND];
+    for (int i = 0; i + 1 < m; ++i) e[i] = h[(size_t(i + 1) + size_t(i) * ld) * ND];
+    tridiag_invsqrt_e1(m, d.data(), e.data(), beta0, yy.data());
+    for (int i = 0; i < m; ++i) {
+      yo[i * ND] = yy[i];
+      if (ND == 2) yo[i * ND + 1] = 0.0;
+    }
+  } else {
+    std::vector<zc> A(size_t(m) * m), yy;
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < m; ++i) {
+        const size_t o = (size_t(i) + size_t(j) * ld) * ND;
+        A[size_t(i) + size_t(j) * m] = zc(h[o], ND == 2 ? h[o + 1] : 0.0);
+      }
+    general_invsqrt_e1(m, A, beta0, yy);
+    for (int i = 0; i < m; ++i) {
+      yo[i * ND] = yy[i].real();
+      if (ND == 2) yo[i * ND + 1] = yy[i].imag();
+    }
+  }
+  PPF_API_END
+}
+
+}  // extern "C"

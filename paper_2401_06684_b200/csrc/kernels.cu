@@ -1,0 +1,737 @@
+// Device kernels of the hot path, sm_100a.
+//
+// Everything here is HBM-bandwidth bound (SURVEY §8(d) roofline: 0.17-0.5
+// flop/byte), so the kernels are organised around coalesced streams:
+//  * SpMV (K1) with the polynomial recurrences fused into the epilogue (K2
+//    Clenshaw, K3 Newton-Horner): one pass over A per degree, P:136/P:332/P:354.
+//    SELL-C-sigma (one row per lane, C = 32, or two rows per lane as 128-bit
+//    double2/int2 loads, C = 64) and a CSR kernel (G lanes per row).
+//  * CGS2 (K5/K6/K7): three fused tall-skinny sweeps over V, warps own columns,
+//    V values are held in registers between the update and the projection.
+//  * Lanczos (K8), combine x = V y (K9), norms.
+// Reductions are deterministic: per-block partials, then the last block to
+// arrive sums them in block order (fixed tree), independent of timing.
+#include <cuda_runtime.h>
+
+#include "ppf_internal.h"
+
+namespace ppf {
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <typename T> struct EpiT {
+  T s_ax, s_x, s_z, s_u;
+  const T* z;
+  const T* u;
+};
+
+template <typename T> EpiT<T> to_epi(const Epi& e) {
+  EpiT<T> r;
+  r.s_ax = s_from<T>(e.s_ax[0], e.s_ax[1]);
+  r.s_x = s_from<T>(e.s_x[0], e.s_x[1]);
+  r.s_z = s_from<T>(e.s_z[0], e.s_z[1]);
+  r.s_u = s_from<T>(e.s_u[0], e.s_u[1]);
+  r.z = static_cast<const T*>(e.z);
+  r.u = static_cast<const T*>(e.u);
+  return r;
+}
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+__device__ __forceinline__ cplx ldg(const cplx* p) {
+  double2 v = __ldg(reinterpret_cast<const double2*>(p));
+  return {v.x, v.y};
+}
+
+template <typename T>
+__device__ __forceinline__ T epilogue(const EpiT<T>& e, T ax, const T* __restrict__ x, int64_t row,
+                                      bool has_x) {
+  T r = s_mul(e.s_ax, ax);
+  if (has_x) r = s_fma(e.s_x, ldg(x + row), r);
+  if (e.z) r = s_fma(e.s_z, ldg(e.z + row), r);
+  if (e.u) r = s_fma(e.s_u, ldg(e.u + row), r);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// SELL-C-sigma SpMV + fused epilogue.  One warp per slice; R rows per lane.
+// ---------------------------------------------------------------------------
+template <typename T, bool PERM>
+__global__ void __launch_bounds__(256) sell1_kernel(int64_t nslices, int64_t n,
+                                                    const int64_t* __restrict__ sptr,
+                                                    const int32_t* __restrict__ col,
+                                                    const T* __restrict__ val,
+                                                    const T* __restrict__ x, T* __restrict__ out,
+                                                    EpiT<T> e, bool has_x,
+                                                    const int32_t* __restrict__ perm) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (slice >= nslices) return;
+  const int64_t base = sptr[slice];
+  const int w = int((sptr[slice + 1] - base) >> 5);
+  const int32_t* cp = col + base + lane;
+  const T* vp = val + base + lane;
+  T acc = s_zero<T>();
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int c = __ldg(cp + 32 * k);
+    const T v = ldg(vp + 32 * k);
+    acc = s_fma(v, ldg(x + c), acc);
+  }
+  const int64_t pos = slice * 32 + lane;
+  if (pos < n) {
+    const int64_t row = PERM ? int64_t(perm[pos]) : pos;
+    out[row] = epilogue(e, acc, x, row, has_x);
+  }
+}
+
+// two rows per lane, 128-bit loads of (val, val) and (col, col); C = 64, fp64
+__global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
+                                                    const int64_t* __restrict__ sptr,
+                                                    const int32_t* __restrict__ col,
+                                                    const double* __restrict__ val,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ out, EpiT<double> e,
+                                                    bool has_x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t slice = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (slice >= nslices) return;
+  const int64_t base = sptr[slice];
+  const int w = int((sptr[slice + 1] - base) >> 6);
+  const int2* cp = reinterpret_cast<const int2*>(col + base) + lane;
+  const double2* vp = reinterpret_cast<const double2*>(val + base) + lane;
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int2 c = __ldg(cp + 32 * k);
+    const double2 v = __ldg(vp + 32 * k);
+    a0 = fma(v.x, __ldg(x + c.x), a0);
+    a1 = fma(v.y, __ldg(x + c.y), a1);
+  }
+  const int64_t r0 = slice * 64 + 2 * lane;
+  if (r0 + 1 < n) {
+    double2 r;
+    r.x = e.s_ax * a0;
+    r.y = e.s_ax * a1;
+    if (has_x) {
+      const double2 xv = __ldg(reinterpret_cast<const double2*>(x + r0));
+      r.x = fma(e.s_x, xv.x, r.x);
+      r.y = fma(e.s_x, xv.y, r.y);
+    }
+    if (e.z) {
+      const double2 zv = __ldg(reinterpret_cast<const double2*>(e.z + r0));
+      r.x = fma(e.s_z, zv.x, r.x);
+      r.y = fma(e.s_z, zv.y, r.y);
+    }
+    if (e.u) {
+      const double2 uv = __ldg(reinterpret_cast<const double2*>(e.u + r0));
+      r.x = fma(e.s_u, uv.x, r.x);
+      r.y = fma(e.s_u, uv.y, r.y);
+    }
+    *reinterpret_cast<double2*>(out + r0) = r;
+  } else if (r0 < n) {
+    out[r0] = epilogue(e, a0, x, r0, has_x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMV + fused epilogue, G lanes per row.
+// ---------------------------------------------------------------------------
+template <typename T, int G>
+__global__ void __launch_bounds__(256) csr_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                                  const int32_t* __restrict__ col,
+                                                  const T* __restrict__ val,
+                                                  const T* __restrict__ x, T* __restrict__ out,
+                                                  EpiT<T> e, bool has_x) {
+  const int64_t gt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t row = gt / G;
+  const int lg = threadIdx.x % G;
+  const int lane = threadIdx.x & 31;
+  const unsigned mask = (G == 32) ? FULL : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  if (row >= n) return;  // whole group exits together
+  T acc = s_zero<T>();
+  const int64_t end = rp[row + 1];
+  for (int64_t k = rp[row] + lg; k < end; k += G) acc = s_fma(ldg(val + k), ldg(x + __ldg(col + k)), acc);
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    if constexpr (sizeof(T) == 8) {
+      acc = s_add(acc, __shfl_xor_sync(mask, acc, o));
+    } else {
+      cplx t;
+      t.re = __shfl_xor_sync(mask, reinterpret_cast<cplx&>(acc).re, o);
+      t.im = __shfl_xor_sync(mask, reinterpret_cast<cplx&>(acc).im, o);
+      acc = s_add(acc, reinterpret_cast<T&>(t));
+    }
+  }
+  if (lg == 0) out[row] = epilogue(e, acc, x, row, has_x);
+}
+
+// halo: out[rows[i]] += s_ax * sum val * recv[col]
+template <typename T>
+__global__ void halo_apply_kernel(int64_t nrows, const int32_t* __restrict__ rows,
+                                  const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                  const T* __restrict__ val, const T* __restrict__ recv,
+                                  T* __restrict__ out, T s_ax) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  T acc = s_zero<T>();
+  for (int64_t k = rp[i]; k < rp[i + 1]; ++k) acc = s_fma(ldg(val + k), ldg(recv + col[k]), acc);
+  const int64_t r = rows[i];
+  out[r] = s_fma(s_ax, acc, out[r]);
+}
+
+template <typename T>
+__global__ void halo_pack_kernel(int64_t cnt, const int32_t* __restrict__ idx,
+                                 const T* __restrict__ x, T* __restrict__ send) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < cnt) send[i] = ldg(x + idx[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Reduction helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+// Block-wide sum of `v` (all threads participate); result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* sm) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sm[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x < 32) {
+    r = (lane < int(blockDim.x >> 5)) ? sm[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+// After each block wrote its partials: returns true (block-uniform) in the last
+// block to arrive.  Partials written before the call are then visible to it.
+__device__ __forceinline__ bool last_block(unsigned* counter) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(counter, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last;
+}
+
+// In the last block: sum partials[b * stride + i] over b = 0..nb-1 for i in
+// [0, nv) (one warp per value, fixed order), calling f(i, sum) in lane 0.
+template <typename F>
+__device__ __forceinline__ void reduce_partials(const double* partials, int nb, int stride, int nv,
+                                                F f) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = w; i < nv; i += nw) {
+    double s = 0.0;
+    for (int b = lane; b < nb; b += 32) s += __ldcg(partials + int64_t(b) * stride + i);
+    s = warp_sum(s);
+    if (lane == 0) f(i, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// scale / norm / diffnorm / combine
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void scale_kernel(int64_t n, const T* __restrict__ src, T* __restrict__ dst,
+                             const double* __restrict__ alpha_dev, double alpha_host) {
+  const double a = alpha_dev ? *alpha_dev : alpha_host;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = s_scale(ldg(src + i), a);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) norm_kernel(int64_t n, const T* __restrict__ v,
+                                                   double* __restrict__ out, double* partials,
+                                                   unsigned* counter) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    s += s_abs2(ldg(v + i));
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  if (last_block(counter)) {
+    reduce_partials(partials, gridDim.x, 1, 1, [&](int, double t) {
+      const double nrm = sqrt(t);
+      out[0] = nrm;
+      out[1] = 1.0 / nrm;
+      *counter = 0;
+    });
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) diffnorm_kernel(int64_t n, const T* __restrict__ a,
+                                                       const T* __restrict__ b,
+                                                       double* __restrict__ out, double* partials,
+                                                       unsigned* counter) {
+  __shared__ double sm[32];
+  double s = 0.0, t = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const T bv = ldg(b + i);
+    s += s_abs2(s_sub(ldg(a + i), bv));
+    t += s_abs2(bv);
+  }
+  s = block_sum(s, sm);
+  t = block_sum(t, sm);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = s;
+    partials[2 * blockIdx.x + 1] = t;
+  }
+  if (last_block(counter)) {
+    reduce_partials(partials, gridDim.x, 2, 2, [&](int i, double v) { out[i] = sqrt(v); });
+    __syncthreads();
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) combine_kernel(int64_t n, const T* __restrict__ V,
+                                                      int64_t ldv, int ncols,
+                                                      const T* __restrict__ y, T* __restrict__ x) {
+  extern __shared__ double ysm_raw[];
+  T* ysm = reinterpret_cast<T*>(ysm_raw);
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) ysm[c] = y[c];
+  __syncthreads();
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    T acc = s_zero<T>();
+    for (int c = 0; c < ncols; ++c) acc = s_fma(ldg(V + c * ldv + i), ysm[c], acc);
+    x[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CGS2 sweeps.  Block = 8 warps; warp w owns columns c = w + 8 t (t < CPW);
+// lanes own rows (RPL rows per lane per chunk).  Grid-stride over row chunks.
+// ---------------------------------------------------------------------------
+constexpr int CGS_WARPS = 8;
+
+template <typename T, int CPW, int RPL, int MODE>
+__global__ void __launch_bounds__(256) cgs_kernel(int64_t n, const T* __restrict__ V, int64_t ldv,
+                                                  int ncols, T* __restrict__ w,
+                                                  const T* __restrict__ coef_in,
+                                                  T* __restrict__ coef_out, T* __restrict__ Hcol,
+                                                  T* __restrict__ Hsub, double* __restrict__ inv,
+                                                  double* partials, unsigned* counter) {
+  constexpr int ND = n_doubles<T>();
+  constexpr int ROWS = 32 * RPL;
+  __shared__ T red[CGS_WARPS][ROWS];
+  __shared__ T cin[CGS_WARPS * CPW];
+  __shared__ double smn[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (MODE != 0) {
+    for (int c = threadIdx.x; c < ncols; c += blockDim.x) cin[c] = coef_in[c];
+    __syncthreads();
+  }
+  T acc[CPW];
+#pragma unroll
+  for (int t = 0; t < CPW; ++t) acc[t] = s_zero<T>();
+  double nrm = 0.0;
+  const int64_t nchunks = (n + ROWS - 1) / ROWS;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t r0 = ch * ROWS + lane;
+    T vreg[CPW][RPL];
+    T wv[RPL];
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int64_t r = r0 + 32 * i;
+      wv[i] = (r < n) ? w[r] : s_zero<T>();
+    }
+#pragma unroll
+    for (int t = 0; t < CPW; ++t) {
+      const int c = warp + CGS_WARPS * t;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int64_t r = r0 + 32 * i;
+        vreg[t][i] = (c < ncols && r < n) ? ldg(V + int64_t(c) * ldv + r) : s_zero<T>();
+      }
+    }
+    if (MODE != 0) {
+      // phase 1: w' = w - V coef_in (warp partials over own columns, then smem)
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        T p = s_zero<T>();
+#pragma unroll
+        for (int t = 0; t < CPW; ++t) {
+          const int c = warp + CGS_WARPS * t;
+          if (c < ncols) p = s_fma(vreg[t][i], cin[c], p);
+        }
+        red[warp][lane + 32 * i] = p;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        T s = s_zero<T>();
+#pragma unroll
+        for (int q = 0; q < CGS_WARPS; ++q) s = s_add(s, red[q][lane + 32 * i]);
+        wv[i] = s_sub(wv[i], s);
+        const int64_t r = r0 + 32 * i;
+        if (warp == 0 && r < n) w[r] = wv[i];
+        if (MODE == 2 && warp == 0) nrm += s_abs2(wv[i]);
+      }
+      __syncthreads();
+    }
+    if (MODE != 2) {
+#pragma unroll
+      for (int t = 0; t < CPW; ++t)
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) acc[t] = s_cfma(vreg[t][i], wv[i], acc[t]);
+    }
+  }
+  // publish per-block partials
+  if (MODE != 2) {
+#pragma unroll
+    for (int t = 0; t < CPW; ++t) {
+      const int c = warp + CGS_WARPS * t;
+      double* a = reinterpret_cast<double*>(&acc[t]);
+#pragma unroll
+      for (int d = 0; d < ND; ++d) {
+        const double s = warp_sum(a[d]);
+        if (lane == 0 && c < ncols) partials[int64_t(blockIdx.x) * ncols * ND + c * ND + d] = s;
+      }
+    }
+  } else {
+    const double s = block_sum(nrm, smn);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  }
+  if (last_block(counter)) {
+    if (MODE != 2) {
+      reduce_partials(partials, gridDim.x, ncols * ND, ncols * ND, [&](int i, double s) {
+        double* co = reinterpret_cast<double*>(coef_out);
+        co[i] = s;
+        if (MODE == 1) {
+          const double* ci = reinterpret_cast<const double*>(coef_in);
+          reinterpret_cast<double*>(Hcol)[i] = ci[i] + s;
+        }
+      });
+    } else {
+      reduce_partials(partials, gridDim.x, 1, 1, [&](int, double s) {
+        const double nr = sqrt(s);
+        double* hs = reinterpret_cast<double*>(Hsub);
+        hs[0] = nr;
+        if (ND == 2) hs[1] = 0.0;
+        inv[0] = 1.0 / nr;
+      });
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+// Lanczos (K8).  phase 1: w -= beta_prev*vprev; alpha = v^H w.
+//                phase 2: w -= alpha*v; beta = ||w||.
+template <typename T, int PHASE>
+__global__ void __launch_bounds__(256) lanczos_kernel(int64_t n, const T* __restrict__ v,
+                                                      const T* __restrict__ vprev,
+                                                      const double* __restrict__ beta_prev,
+                                                      T* __restrict__ w, T* __restrict__ Hdiag,
+                                                      T* __restrict__ Hsub, T* __restrict__ Hsup,
+                                                      double* __restrict__ inv, double* partials,
+                                                      unsigned* counter) {
+  constexpr int ND = n_doubles<T>();
+  __shared__ double sm[32];
+  double s0 = 0.0, s1 = 0.0;
+  const double bp = (PHASE == 1 && vprev) ? *beta_prev : 0.0;
+  T alpha = s_zero<T>();
+  if (PHASE == 2) alpha = *Hdiag;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    T wi = w[i];
+    const T vi = ldg(v + i);
+    if (PHASE == 1) {
+      if (vprev) wi = s_sub(wi, s_scale(ldg(vprev + i), bp));
+      w[i] = wi;
+      const T d = s_cfma(vi, wi, s_zero<T>());
+      s0 += s_real(d);
+      if (ND == 2) s1 += reinterpret_cast<const cplx&>(d).im;
+    } else {
+      wi = s_sub(wi, s_mul(alpha, vi));
+      w[i] = wi;
+      s0 += s_abs2(wi);
+    }
+  }
+  s0 = block_sum(s0, sm);
+  if (PHASE == 1 && ND == 2) s1 = block_sum(s1, sm);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = s0;
+    partials[2 * blockIdx.x + 1] = s1;
+  }
+  if (last_block(counter)) {
+    if (PHASE == 1) {
+      reduce_partials(partials, gridDim.x, 2, ND, [&](int i, double s) {
+        reinterpret_cast<double*>(Hdiag)[i] = s;
+      });
+    } else {
+      reduce_partials(partials, gridDim.x, 2, 1, [&](int, double s) {
+        const double b = sqrt(s);
+        reinterpret_cast<double*>(Hsub)[0] = b;
+        reinterpret_cast<double*>(Hsup)[0] = b;
+        if (ND == 2) {
+          reinterpret_cast<double*>(Hsub)[1] = 0.0;
+          reinterpret_cast<double*>(Hsup)[1] = 0.0;
+        }
+        inv[0] = 1.0 / b;
+      });
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *counter = 0;
+  }
+}
+
+int blocks_for(int64_t n, int threads, int cap) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return int(b);
+}
+
+void post_launch(const char* what) { cuda_check(cudaGetLastError(), what); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+template <typename T>
+static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st) {
+  const EpiT<T> et = to_epi<T>(e);
+  const bool has_x = (e.s_x[0] != 0.0 || e.s_x[1] != 0.0);
+  const T* xt = static_cast<const T*>(x);
+  T* ot = static_cast<T*>(out);
+  const T* val = static_cast<const T*>(A->d_val);
+  if (A->fmt == PPF_FMT_SELL) {
+    const int64_t warps = A->nslices;
+    const int blocks = int((warps * 32 + 255) / 256);
+    if (blocks == 0) return;
+    if constexpr (sizeof(T) == 8) {
+      if (A->C == 64) {
+        sell2_kernel<<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
+                                             reinterpret_cast<const double*>(val), xt, ot, et,
+                                             has_x);
+        post_launch("sell2_kernel");
+        return;
+      }
+    }
+    if (A->d_perm)
+      sell1_kernel<T, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
+                                                    val, xt, ot, et, has_x, A->d_perm);
+    else
+      sell1_kernel<T, false><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
+                                                     val, xt, ot, et, has_x, nullptr);
+    post_launch("sell1_kernel");
+  } else {
+    const int G = A->csr_group;
+    const int64_t threads = A->n_local * G;
+    const int blocks = int((threads + 255) / 256);
+    if (blocks == 0) return;
+#define PPF_CSR(GG)                                                                           \
+  case GG:                                                                                    \
+    csr_kernel<T, GG><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, \
+                                              has_x);                                         \
+    break;
+    switch (G) {
+      PPF_CSR(2)
+      PPF_CSR(4)
+      PPF_CSR(8)
+      PPF_CSR(16)
+      PPF_CSR(32)
+      default:
+        fail(PPF_EINVAL, "bad CSR group");
+    }
+#undef PPF_CSR
+    post_launch("csr_kernel");
+  }
+}
+
+void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st) {
+  if (A->dtype == PPF_R64)
+    spmv_t<double>(A, x, out, e, st);
+  else
+    spmv_t<cplx>(A, x, out, e, st);
+}
+
+void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st) {
+  if (A->send_total == 0) return;
+  const int blocks = int((A->send_total + 255) / 256);
+  if (A->dtype == PPF_R64)
+    halo_pack_kernel<double><<<blocks, 256, 0, st>>>(A->send_total, A->d_send_idx,
+                                                     static_cast<const double*>(x),
+                                                     static_cast<double*>(A->d_send));
+  else
+    halo_pack_kernel<cplx><<<blocks, 256, 0, st>>>(A->send_total, A->d_send_idx,
+                                                   static_cast<const cplx*>(x),
+                                                   static_cast<cplx*>(A->d_send));
+  post_launch("halo_pack_kernel");
+}
+
+void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st) {
+  if (A->halo_rows == 0) return;
+  const int blocks = int((A->halo_rows + 255) / 256);
+  if (A->dtype == PPF_R64)
+    halo_apply_kernel<double><<<blocks, 256, 0, st>>>(
+        A->halo_rows, A->d_halo_rows, A->d_halo_ptr, A->d_halo_col,
+        static_cast<const double*>(A->d_halo_val), static_cast<const double*>(A->d_recv),
+        static_cast<double*>(out), s_ax[0]);
+  else
+    halo_apply_kernel<cplx><<<blocks, 256, 0, st>>>(
+        A->halo_rows, A->d_halo_rows, A->d_halo_ptr, A->d_halo_col,
+        static_cast<const cplx*>(A->d_halo_val), static_cast<const cplx*>(A->d_recv),
+        static_cast<cplx*>(out), cplx{s_ax[0], s_ax[1]});
+  post_launch("halo_apply_kernel");
+}
+
+void launch_scale(ppf_dtype dt, int64_t n, const void* src, void* dst, const double* alpha_dev,
+                  double alpha_host, cudaStream_t st) {
+  const int blocks = blocks_for(n, 256, 148 * 8);
+  if (dt == PPF_R64)
+    scale_kernel<double><<<blocks, 256, 0, st>>>(n, static_cast<const double*>(src),
+                                                 static_cast<double*>(dst), alpha_dev, alpha_host);
+  else
+    scale_kernel<cplx><<<blocks, 256, 0, st>>>(n, static_cast<const cplx*>(src),
+                                               static_cast<cplx*>(dst), alpha_dev, alpha_host);
+  post_launch("scale_kernel");
+}
+
+void launch_norm(ppf_dtype dt, int64_t n, const void* v, double* out, RedScratch& rs, int grid,
+                 cudaStream_t st) {
+  const int blocks = blocks_for(n, 256, grid);
+  if (dt == PPF_R64)
+    norm_kernel<double><<<blocks, 256, 0, st>>>(n, static_cast<const double*>(v), out,
+                                                rs.partials, rs.counter);
+  else
+    norm_kernel<cplx><<<blocks, 256, 0, st>>>(n, static_cast<const cplx*>(v), out, rs.partials,
+                                              rs.counter);
+  post_launch("norm_kernel");
+}
+
+void launch_diffnorm(ppf_dtype dt, int64_t n, const void* a, const void* b, double* out,
+                     RedScratch& rs, int grid, cudaStream_t st) {
+  const int blocks = blocks_for(n, 256, grid);
+  if (dt == PPF_R64)
+    diffnorm_kernel<double><<<blocks, 256, 0, st>>>(n, static_cast<const double*>(a),
+                                                    static_cast<const double*>(b), out,
+                                                    rs.partials, rs.counter);
+  else
+    diffnorm_kernel<cplx><<<blocks, 256, 0, st>>>(n, static_cast<const cplx*>(a),
+                                                  static_cast<const cplx*>(b), out, rs.partials,
+                                                  rs.counter);
+  post_launch("diffnorm_kernel");
+}
+
+void launch_combine(ppf_dtype dt, int64_t n, const void* V, int64_t ldv, int ncols, const void* y,
+                    void* x, cudaStream_t st) {
+  const int blocks = blocks_for(n, 256, 148 * 8);
+  const size_t sm = size_t(ncols) * (dt == PPF_R64 ? 8 : 16);
+  if (dt == PPF_R64)
+    combine_kernel<double><<<blocks, 256, sm, st>>>(n, static_cast<const double*>(V), ldv, ncols,
+                                                    static_cast<const double*>(y),
+                                                    static_cast<double*>(x));
+  else
+    combine_kernel<cplx><<<blocks, 256, sm, st>>>(n, static_cast<const cplx*>(V), ldv, ncols,
+                                                  static_cast<const cplx*>(y),
+                                                  static_cast<cplx*>(x));
+  post_launch("combine_kernel");
+}
+
+template <typename T, int CPW, int RPL>
+static void cgs_t(int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
+                  const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
+                  RedScratch& rs, int grid, cudaStream_t st) {
+  const int64_t nchunks = (n + 32 * RPL - 1) / (32 * RPL);
+  int blocks = int(nchunks < grid ? nchunks : grid);
+  if (blocks < 1) blocks = 1;
+  auto Vt = static_cast<const T*>(V);
+  auto wt = static_cast<T*>(w);
+  auto ci = static_cast<const T*>(coef_in);
+  auto co = static_cast<T*>(coef_out);
+  auto hc = static_cast<T*>(Hcol);
+  auto hs = static_cast<T*>(Hsub);
+  switch (mode) {
+    case 0:
+      cgs_kernel<T, CPW, RPL, 0><<<blocks, 256, 0, st>>>(n, Vt, ldv, ncols, wt, ci, co, hc, hs, inv,
+                                                         rs.partials, rs.counter);
+      break;
+    case 1:
+      cgs_kernel<T, CPW, RPL, 1><<<blocks, 256, 0, st>>>(n, Vt, ldv, ncols, wt, ci, co, hc, hs, inv,
+                                                         rs.partials, rs.counter);
+      break;
+    default:
+      cgs_kernel<T, CPW, RPL, 2><<<blocks, 256, 0, st>>>(n, Vt, ldv, ncols, wt, ci, co, hc, hs, inv,
+                                                         rs.partials, rs.counter);
+  }
+  post_launch("cgs_kernel");
+}
+
+template <typename T>
+static void cgs_dispatch(int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
+                         const void* ci, void* co, void* hc, void* hs, double* inv, RedScratch& rs,
+                         int grid, cudaStream_t st) {
+  const int cpw = (ncols + CGS_WARPS - 1) / CGS_WARPS;
+  if (cpw <= 1)
+    cgs_t<T, 1, 4>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+  else if (cpw <= 2)
+    cgs_t<T, 2, 4>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+  else if (cpw <= 4)
+    cgs_t<T, 4, 2>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+  else if (cpw <= 8)
+    cgs_t<T, 8, 1>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+  else if (cpw <= 16)
+    cgs_t<T, 16, 1>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+  else if (cpw <= 32)
+    cgs_t<T, 32, 1>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+  else
+    fail(PPF_EINVAL, "too many basis vectors for the CGS kernel (max 256)");
+}
+
+void launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
+                const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
+                RedScratch& rs, int grid, cudaStream_t st) {
+  if (dt == PPF_R64)
+    cgs_dispatch<double>(mode, n, V, ldv, ncols, w, coef_in, coef_out, Hcol, Hsub, inv, rs, grid,
+                         st);
+  else
+    cgs_dispatch<cplx>(mode, n, V, ldv, ncols, w, coef_in, coef_out, Hcol, Hsub, inv, rs, grid,
+                       st);
+}
+
+void launch_lanczos(ppf_dtype dt, int phase, int64_t n, const void* v, const void* vprev,
+                    const double* beta_prev, void* w, void* Hdiag, void* Hsub, void* Hsup,
+                    double* inv, RedScratch& rs, int grid, cudaStream_t st) {
+  const int blocks = blocks_for(n, 256, grid);
+#define PPF_LZ(T)                                                                                \
+  if (phase == 1)                                                                                \
+    lanczos_kernel<T, 1><<<blocks, 256, 0, st>>>(                                                \
+        n, static_cast<const T*>(v), static_cast<const T*>(vprev), beta_prev, static_cast<T*>(w), \
+        static_cast<T*>(Hdiag), static_cast<T*>(Hsub), static_cast<T*>(Hsup), inv, rs.partials,  \
+        rs.counter);                                                                             \
+  else                                                                                           \
+    lanczos_kernel<T, 2><<<blocks, 256, 0, st>>>(                                                \
+        n, static_cast<const T*>(v), static_cast<const T*>(vprev), beta_prev, static_cast<T*>(w), \
+        static_cast<T*>(Hdiag), static_cast<T*>(Hsub), static_cast<T*>(Hsup), inv, rs.partials,  \
+        rs.counter);
+  if (dt == PPF_R64) {
+    PPF_LZ(double)
+  } else {
+    PPF_LZ(cplx)
+  }
+#undef PPF_LZ
+  post_launch("lanczos_kernel");
+}
+
+}  // namespace ppf

@@ -1,0 +1,251 @@
+// Internal declarations of the ppf library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <complex>
+#include <string>
+#include <vector>
+
+#include "../../include/ppf.h"
+
+#ifndef PPF_HD
+#ifdef __CUDACC__
+#define PPF_HD __host__ __device__ __forceinline__
+#else
+#define PPF_HD inline
+#endif
+#endif
+
+namespace ppf {
+
+// ---------------------------------------------------------------------------
+// Scalar types: double (PPF_R64) and an interleaved complex (PPF_C128).
+// ---------------------------------------------------------------------------
+struct alignas(16) cplx {
+  double re, im;
+};
+
+PPF_HD double s_real(double a) { return a; }
+PPF_HD double s_real(cplx a) { return a.re; }
+PPF_HD double s_conj(double a) { return a; }
+PPF_HD cplx s_conj(cplx a) { return {a.re, -a.im}; }
+PPF_HD double s_add(double a, double b) { return a + b; }
+PPF_HD cplx s_add(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
+PPF_HD double s_sub(double a, double b) { return a - b; }
+PPF_HD cplx s_sub(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
+PPF_HD double s_mul(double a, double b) { return a * b; }
+PPF_HD cplx s_mul(cplx a, cplx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+// a*b + c
+PPF_HD double s_fma(double a, double b, double c) { return fma(a, b, c); }
+PPF_HD cplx s_fma(cplx a, cplx b, cplx c) {
+  return {fma(a.re, b.re, fma(-a.im, b.im, c.re)), fma(a.re, b.im, fma(a.im, b.re, c.im))};
+}
+// conj(a)*b + c
+PPF_HD double s_cfma(double a, double b, double c) { return fma(a, b, c); }
+PPF_HD cplx s_cfma(cplx a, cplx b, cplx c) {
+  return {fma(a.re, b.re, fma(a.im, b.im, c.re)), fma(a.re, b.im, fma(-a.im, b.re, c.im))};
+}
+PPF_HD double s_abs2(double a) { return a * a; }
+PPF_HD double s_abs2(cplx a) { return a.re * a.re + a.im * a.im; }
+PPF_HD double s_scale(double a, double s) { return a * s; }
+PPF_HD cplx s_scale(cplx a, double s) { return {a.re * s, a.im * s}; }
+template <typename T> PPF_HD T s_zero();
+template <> PPF_HD double s_zero<double>() { return 0.0; }
+template <> PPF_HD cplx s_zero<cplx>() { return {0.0, 0.0}; }
+template <typename T> PPF_HD T s_from(double re, double im);
+template <> PPF_HD double s_from<double>(double re, double) { return re; }
+template <> PPF_HD cplx s_from<cplx>(double re, double im) { return {re, im}; }
+template <typename T> PPF_HD constexpr int n_doubles() { return sizeof(T) / sizeof(double); }
+
+using zc = std::complex<double>;
+
+// ---------------------------------------------------------------------------
+// Errors
+// ---------------------------------------------------------------------------
+struct Error {
+  ppf_status st;
+  std::string msg;
+};
+[[noreturn]] void fail(ppf_status st, const std::string& msg);
+void set_last_error(const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define PPF_CUDA(call) ::ppf::cuda_check((call), #call)
+#define PPF_REQUIRE(cond, msg) \
+  do {                         \
+    if (!(cond)) ::ppf::fail(PPF_EINVAL, msg); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Matrix layout
+// ---------------------------------------------------------------------------
+// SELL-C-sigma: slice s covers (permuted) local rows [s*C, s*C + C); its
+// entries start at slice_ptr[s] (a multiple of C) and are stored
+// [k][row-in-slice]: entry k of row r is at slice_ptr[s] + k*C + (r - s*C).
+// Padding entries have val = 0 and col = the first row of the slice.
+// CSR: row_ptr (int64) / col (int32) / val.
+// Columns of the diagonal block are LOCAL indices; the off-diagonal (halo)
+// block is a compact CSR over the rows that touch other ranks, columns index
+// the halo receive buffer.
+struct HostBlock {
+  int64_t rows = 0;
+  int64_t nslices = 0;
+  std::vector<int64_t> ptr;    // SELL slice_ptr [nslices+1] or CSR row_ptr [rows+1]
+  std::vector<int32_t> col;
+  std::vector<double> val;     // n_doubles per entry
+  std::vector<int32_t> perm;   // SELL sigma > 1: perm[pos] = original local row
+};
+
+struct HostHalo {
+  std::vector<int32_t> rows;     // local rows with off-rank columns
+  std::vector<int64_t> ptr;      // [rows.size()+1]
+  std::vector<int32_t> col;      // index into the recv buffer
+  std::vector<double> val;
+};
+
+}  // namespace ppf
+
+struct ppf_plan {
+  ppf_dtype dtype;
+  int64_t n_global, row0, n_local, nnz;
+  int nranks, rank;
+  std::vector<int64_t> bounds;
+  ppf_format fmt;
+  int C, sigma;
+  ppf::HostBlock diag;
+  ppf::HostHalo halo;
+  std::vector<std::vector<int64_t>> recv;   // per peer: global indices received (sorted)
+  std::vector<int64_t> recv_off;            // per peer offset into the recv buffer
+  std::vector<std::vector<int64_t>> send;   // per peer: local rows to send
+  bool sends_set = false;
+};
+
+struct ppf_mat {
+  ppf_ctx* ctx;
+  ppf_dtype dtype;
+  ppf_format fmt;
+  int64_t n_global, row0, n_local, nnz, stored;
+  int C, sigma;
+  int nranks, rank;
+  int64_t nslices;
+  const int64_t* d_ptr;     // slice_ptr or row_ptr
+  const int32_t* d_col;
+  const void* d_val;
+  const int32_t* d_perm;    // null unless sigma > 1
+  int csr_group;            // lanes per row for the CSR kernel
+  // halo (nranks > 1)
+  int64_t halo_rows, halo_nnz, halo_total, send_total;
+  const int32_t* d_halo_rows;
+  const int64_t* d_halo_ptr;
+  const int32_t* d_halo_col;
+  const void* d_halo_val;
+  void* d_recv;             // halo_total scalars
+  void* d_send;             // send_total scalars
+  const int32_t* d_send_idx;
+  std::vector<int64_t> recv_count, recv_off, send_count, send_off;  // per peer
+};
+
+struct ppf_poly {
+  int kind;                         // ppf_poly_kind
+  int deg;
+  double a, b;                      // Chebyshev interval
+  std::vector<double> c;            // Chebyshev coefficients c_0..c_deg
+  std::vector<ppf::zc> nodes, dd;   // Newton form (Leja order)
+};
+
+namespace ppf {
+
+struct HistRec {
+  int m;
+  double est, err;
+  long long mvms;
+};
+
+}  // namespace ppf
+
+struct ppf_ctx {
+  int device, rank, nranks;
+  cudaStream_t stream;
+  void* nccl_comm;            // ncclComm_t when nranks > 1
+  int num_sms;
+  // pinned host staging for H columns and y
+  void* h_pinned;
+  size_t h_pinned_bytes;
+  cudaEvent_t ev;
+  // last run
+  std::vector<ppf::HistRec> hist;
+  std::vector<double> lastH;  // (m+1) x m, n_doubles per entry, column-major ld = m+1
+  int last_m;
+  double last_beta0;
+  ppf_dtype last_dtype;
+  long long launches;
+};
+
+namespace ppf {
+
+// ---------------------------------------------------------------------------
+// Host dense routines (dense.cpp)
+// ---------------------------------------------------------------------------
+// y = beta0 * T^{-1/2} e1 for symmetric tridiagonal T (diag d[m], offdiag e[m-1]).
+void tridiag_invsqrt_e1(int m, const double* d, const double* e, double beta0, double* y);
+// Complex Schur H = Q T Q^H of a general m x m matrix (column-major, ld = m).
+void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q);
+// y = beta0 * H^{-1/2} e1 via Schur -> triangular sqrt -> solve.
+void general_invsqrt_e1(int m, const std::vector<zc>& H, double beta0, std::vector<zc>& y);
+// Eigenvalues of a general complex m x m matrix (column-major).
+std::vector<zc> eigenvalues(int m, std::vector<zc> H);
+
+// ---------------------------------------------------------------------------
+// Polynomials (poly.cpp)
+// ---------------------------------------------------------------------------
+void chebyshev_coefficients(double a, double b, int deg, std::vector<double>& c);
+double chebyshev_eval(const ppf_poly& q, double z);
+zc poly_eval(const ppf_poly& q, zc z);
+std::vector<zc> leja_order(const std::vector<zc>& nodes);
+std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& nodes);
+
+// ---------------------------------------------------------------------------
+// Device kernels (kernels.cu): host-side launchers
+// ---------------------------------------------------------------------------
+struct Epi {          // out = s_ax*(A x) + s_x*x + s_z*z + s_u*u
+  double s_ax[2], s_x[2], s_z[2], s_u[2];
+  const void* z;      // may be null (s_z ignored)
+  const void* u;      // may be null (s_u ignored)
+};
+
+void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st);
+void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
+void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st);
+
+struct RedScratch {   // reduction scratch (device)
+  double* partials;   // [max_blocks * max_vals * 2]
+  unsigned* counter;  // zero-initialised, self-resetting
+  int max_blocks;
+};
+// dst = alpha * src (alpha read from device double *alpha_dev if non-null, else alpha_host)
+void launch_scale(ppf_dtype dt, int64_t n, const void* src, void* dst, const double* alpha_dev,
+                  double alpha_host, cudaStream_t st);
+// res[0] = ||v||^2 partial -> nrm_out[0] = ||v||, nrm_out[1] = 1/||v||
+void launch_norm(ppf_dtype dt, int64_t n, const void* v, double* nrm_out, RedScratch& rs, int grid,
+                 cudaStream_t st);
+// CGS kernels on V (ld = ldv, columns 0..ncols-1), w (in place).
+//   mode 0: coef_out[0:ncols] = V^H w
+//   mode 1: w -= V coef_in ; coef_out = V^H w ; H[:,j] = coef_in + coef_out
+//   mode 2: w -= V coef_in ; H[j+1,j] = ||w||, inv[0] = 1/||w||
+void launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
+                const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
+                RedScratch& rs, int grid, cudaStream_t st);
+// Lanczos: phase 1: w -= beta_prev * vprev (if vprev); alpha = v^H w -> Hdiag (real part kept)
+//          phase 2: w -= alpha v; beta = ||w|| -> Hsub, Hsup; inv = 1/beta
+void launch_lanczos(ppf_dtype dt, int phase, int64_t n, const void* v, const void* vprev,
+                    const double* beta_prev, void* w, void* Hdiag, void* Hsub, void* Hsup,
+                    double* inv, RedScratch& rs, int grid, cudaStream_t st);
+// x = V y (y device, ncols entries)
+void launch_combine(ppf_dtype dt, int64_t n, const void* V, int64_t ldv, int ncols, const void* y,
+                    void* x, cudaStream_t st);
+// out[0] = ||a - b||, out[1] = ||b||
+void launch_diffnorm(ppf_dtype dt, int64_t n, const void* a, const void* b, double* out,
+                     RedScratch& rs, int grid, cudaStream_t st);
+
+}  // namespace ppf

@@ -1,0 +1,678 @@
+// The run (layers L2-L5): Algorithm 1 of the paper on the device,
+// f(H_m) on the host, x = V_m y_m on the device.
+//
+// Per step j (0-based; basis column j is v_{j+1} of the paper):
+//   u = A v_j                      -> U            (1 SpMV)
+//   y = q(A) u                     -> Y            (deg fused SpMV launches)
+//   w = q(A) y                     -> V[:, j+1]    (deg fused SpMV launches)
+//   orthogonalise w in place (Lanczos: 2 fused sweeps; CGS2: 3 fused sweeps)
+//   v_{j+1} = w / h_{j+1,j}        (scale)
+// H lives on the device; the host reads it only at checkpoints (estimate /
+// true error) and at the end.  q(A) is the Clenshaw recurrence (P:332,
+// reading Q4) or the Newton-Horner scheme, each SpMV's epilogue
+// carrying the recurrence's vector updates.
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "ppf_internal.h"
+
+namespace ppf {
+
+namespace {
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WsLayout {
+  int64_t ldv;       // leading dimension of V and vector length (padded)
+  int ldh;           // leading dimension of H
+  size_t V, U, Y, T0, T1, T2, H, hbuf, gbuf, ybuf, scal, partials, counter, total;
+  int max_blocks;
+  int max_vals;
+};
+
+WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms) {
+  const size_t sc = dt == PPF_R64 ? 8 : 16;
+  WsLayout L{};
+  L.ldv = (n + 63) & ~int64_t(63);
+  L.ldh = m_max + 2;
+  L.max_blocks = std::max(4 * num_sms, 256);
+  L.max_vals = (m_max + 2) * 2;
+  size_t o = 0;
+  const size_t vec = al256(size_t(L.ldv) * sc);
+  L.V = o;
+  o += vec * size_t(m_max + 1);
+  L.U = o;
+  o += vec;
+  L.Y = o;
+  o += vec;
+  L.T0 = o;
+  o += vec;
+  L.T1 = o;
+  o += vec;
+  L.T2 = o;
+  o += vec;
+  L.H = o;
+  o += al256(size_t(L.ldh) * (m_max + 1) * sc);
+  L.hbuf = o;
+  o += al256(size_t(m_max + 2) * sc);
+  L.gbuf = o;
+  o += al256(size_t(m_max + 2) * sc);
+  L.ybuf = o;
+  o += al256(size_t(m_max + 2) * sc);
+  L.scal = o;
+  o += 256;
+  L.partials = o;
+  o += al256(size_t(L.max_blocks) * L.max_vals * 8);
+  L.counter = o;
+  o += 256;
+  L.total = o;
+  return L;
+}
+
+// scalar slots (doubles) in the scal area
+enum { S_BETA0 = 0, S_INV0 = 1, S_INV = 2, S_ERR = 4, S_REF = 5 };
+
+struct Runner {
+  ppf_ctx* ctx;
+  ppf_mat* A;
+  const ppf_poly* q;  // may be null for the plain (Ritz setup) operator
+  ppf_dtype dt;
+  int64_t n;
+  size_t sc;
+  WsLayout L;
+  char* w;
+  cudaStream_t st;
+  RedScratch rs;
+  int grid_vec, grid_cgs;
+  long long launches = 0;
+
+  Runner(ppf_ctx* c, ppf_mat* a, const ppf_poly* qq, int m_max, void* work, size_t bytes)
+      : ctx(c), A(a), q(qq), dt(a->dtype), n(a->n_local) {
+    sc = dt == PPF_R64 ? 8 : 16;
+    L = ws_layout(n, dt, m_max, c->num_sms);
+    if (!work || bytes < L.total) fail(PPF_EWORKSPACE, "workspace too small");
+    if (reinterpret_cast<uintptr_t>(work) & 255) fail(PPF_EINVAL, "workspace not 256-B aligned");
+    w = static_cast<char*>(work);
+    st = c->stream;
+    rs.partials = reinterpret_cast<double*>(w + L.partials);
+    rs.counter = reinterpret_cast<unsigned*>(w + L.counter);
+    rs.max_blocks = L.max_blocks;
+    grid_vec = std::min(L.max_blocks, 4 * c->num_sms);
+    grid_cgs = std::min(L.max_blocks, 2 * c->num_sms);
+    PPF_CUDA(cudaMemsetAsync(w + L.counter, 0, 256, st));
+    PPF_CUDA(cudaMemsetAsync(w + L.H, 0, size_t(L.ldh) * (m_max + 1) * sc, st));
+  }
+
+  void* V(int j) { return w + L.V + size_t(j) * al256(size_t(L.ldv) * sc); }
+  void* vec(size_t off) { return w + off; }
+  void* Hp(int i, int j) { return w + L.H + (size_t(i) + size_t(j) * L.ldh) * sc; }
+  double* scal(int i) { return reinterpret_cast<double*>(w + L.scal) + i; }
+
+  // ----- SpMV with halo exchange (nranks > 1) -----
+  void spmv(const void* x, void* out, const Epi& e) {
+    if (A->nranks > 1) exchange(x);
+    launch_spmv(A, x, out, e, st);
+    ++launches;
+    if (A->nranks > 1 && A->halo_rows) {
+      launch_halo_apply(A, out, e.s_ax, st);
+      ++launches;
+    }
+  }
+
+  void exchange(const void* x) {
+    launch_halo_pack(A, x, st);
+    ++launches;
+    auto comm = static_cast<ncclComm_t>(ctx->nccl_comm);
+    const int nd = int(sc / 8);
+    if (ncclGroupStart() != ncclSuccess) fail(PPF_ENCCL, "ncclGroupStart");
+    for (int p = 0; p < A->nranks; ++p) {
+      if (A->send_count[p])
+        if (ncclSend(static_cast<char*>(A->d_send) + A->send_off[p] * sc, A->send_count[p] * nd,
+                     ncclDouble, p, comm, st) != ncclSuccess)
+          fail(PPF_ENCCL, "ncclSend");
+      if (A->recv_count[p])
+        if (ncclRecv(static_cast<char*>(A->d_recv) + A->recv_off[p] * sc, A->recv_count[p] * nd,
+                     ncclDouble, p, comm, st) != ncclSuccess)
+          fail(PPF_ENCCL, "ncclRecv");
+    }
+    if (ncclGroupEnd() != ncclSuccess) fail(PPF_ENCCL, "ncclGroupEnd");
+  }
+
+  static Epi epi(zc sax, zc sx, zc sz, const void* z, zc su, const void* u) {
+    Epi e;
+    e.s_ax[0] = sax.real();
+    e.s_ax[1] = sax.imag();
+    e.s_x[0] = sx.real();
+    e.s_x[1] = sx.imag();
+    e.s_z[0] = sz.real();
+    e.s_z[1] = sz.imag();
+    e.s_u[0] = su.real();
+    e.s_u[1] = su.imag();
+    e.z = z;
+    e.u = u;
+    return e;
+  }
+
+  // out = c * in (complex c allowed for C128)
+  void lincomb(const void* in, void* out, zc c) {
+    // a SpMV-free scaled copy: reuse the SpMV epilogue would need A; use scale
+    if (c.imag() != 0.0 && dt == PPF_R64) fail(PPF_EINVAL, "complex coefficient on a real operator");
+    if (c.imag() == 0.0) {
+      launch_scale(dt, n, in, out, nullptr, c.real(), st);
+      ++launches;
+    } else {
+      fail(PPF_EINVAL, "degree-0 complex Newton polynomial not supported");
+    }
+  }
+
+  // out = q(A) in.  T0..T2 rotation buffers; in/out distinct from them.
+  void apply_q(const void* in, void* out) {
+    void* T[3] = {vec(L.T0), vec(L.T1), vec(L.T2)};
+    const int d = q->deg;
+    if (q->kind == PPF_POLY_CHEBYSHEV) {
+      const double alpha = 2.0 / (q->b - q->a), beta = -(q->a + q->b) / (q->b - q->a);
+      const std::vector<double>& c = q->c;
+      if (d == 0) {
+        lincomb(in, out, c[0]);
+        return;
+      }
+      if (d == 1) {  // out = Ahat(c1 u) + c0 u
+        spmv(in, out, epi(alpha * c[1], beta * c[1] + c[0], 0.0, nullptr, 0.0, nullptr));
+        return;
+      }
+      // b_{d-1} = 2 Ahat (c_d u) + c_{d-1} u
+      spmv(in, T[0], epi(2.0 * alpha * c[d], 2.0 * beta * c[d] + c[d - 1], 0.0, nullptr, 0.0,
+                         nullptr));
+      // index of buffers holding b_{i+1} (cur) and b_{i+2} (prev); b_d = c_d u is implicit
+      int cur = 0, prev = -1;
+      for (int i = d - 2; i >= 1; --i) {
+        int nxt = 0;
+        while (nxt == cur || nxt == prev) ++nxt;
+        if (prev < 0)  // b_{i+2} = b_d = c_d u
+          spmv(T[cur], T[nxt], epi(2.0 * alpha, 2.0 * beta, 0.0, nullptr, c[i] - c[d], in));
+        else
+          spmv(T[cur], T[nxt], epi(2.0 * alpha, 2.0 * beta, -1.0, T[prev], c[i], in));
+        prev = cur;
+        cur = nxt;
+      }
+      // out = Ahat b_1 - b_2 + c_0 u
+      if (prev < 0)
+        spmv(T[cur], out, epi(alpha, beta, 0.0, nullptr, c[0] - c[d], in));
+      else
+        spmv(T[cur], out, epi(alpha, beta, -1.0, T[prev], c[0], in));
+    } else {
+      // Horner on the Newton form: w = dd_d v; w = (A - theta_j) w + dd_j v, j = d-1..0
+      const auto& dd = q->dd;
+      const auto& th = q->nodes;
+      if (d == 0) {
+        lincomb(in, out, dd[0]);
+        return;
+      }
+      if (d == 1) {
+        spmv(in, out, epi(dd[1], -th[0] * dd[1] + dd[0], 0.0, nullptr, 0.0, nullptr));
+        return;
+      }
+      spmv(in, T[0], epi(dd[d], -th[d - 1] * dd[d] + dd[d - 1], 0.0, nullptr, 0.0, nullptr));
+      int cur = 0;
+      for (int j = d - 2; j >= 1; --j) {
+        const int nxt = (cur + 1) % 2;
+        spmv(T[cur], T[nxt], epi(1.0, -th[j], 0.0, nullptr, dd[j], in));
+        cur = nxt;
+      }
+      spmv(T[cur], out, epi(1.0, -th[0], 0.0, nullptr, dd[0], in));
+    }
+  }
+
+  // w = Op v_j into V[j+1]; Op = A q(A)^2 (three stages) or A (q == null).
+  void op_apply(int j) {
+    if (!q) {
+      spmv(V(j), V(j + 1), epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
+      return;
+    }
+    spmv(V(j), vec(L.U), epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
+    apply_q(vec(L.U), vec(L.Y));
+    apply_q(vec(L.Y), V(j + 1));
+  }
+
+  void orthogonalise(int j, bool lanczos) {
+    if (lanczos) {
+      const double* bprev = j > 0 ? reinterpret_cast<const double*>(Hp(j, j - 1)) : nullptr;
+      launch_lanczos(dt, 1, n, V(j), j > 0 ? V(j - 1) : nullptr, bprev, V(j + 1), Hp(j, j),
+                     nullptr, nullptr, nullptr, rs, grid_vec, st);
+      launch_lanczos(dt, 2, n, V(j), nullptr, nullptr, V(j + 1), Hp(j, j), Hp(j + 1, j),
+                     Hp(j, j + 1), scal(S_INV), rs, grid_vec, st);
+      launches += 2;
+    } else {
+      void* hb = vec(L.hbuf);
+      void* gb = vec(L.gbuf);
+      launch_cgs(dt, 0, n, V(0), L.ldv, j + 1, V(j + 1), nullptr, hb, nullptr, nullptr, nullptr,
+                 rs, grid_cgs, st);
+      launch_cgs(dt, 1, n, V(0), L.ldv, j + 1, V(j + 1), hb, gb, Hp(0, j), nullptr, nullptr, rs,
+                 grid_cgs, st);
+      launch_cgs(dt, 2, n, V(0), L.ldv, j + 1, V(j + 1), gb, nullptr, nullptr, Hp(j + 1, j),
+                 scal(S_INV), rs, grid_cgs, st);
+      launches += 3;
+    }
+    launch_scale(dt, n, V(j + 1), V(j + 1), scal(S_INV), 0.0, st);
+    ++launches;
+  }
+
+  // start: V0 = s/||s||  (||s|| -> scal(S_BETA0))
+  void normalise_start() {
+    launch_norm(dt, n, V(0), scal(S_BETA0), rs, grid_vec, st);
+    launch_scale(dt, n, V(0), V(0), scal(S_INV0), 0.0, st);
+    launches += 2;
+  }
+
+  // copy H[0:rows, 0:cols] (and beta0) to pinned host; wait.
+  void fetch_H(int rows, int cols, std::vector<zc>& Hh, double& beta0) {
+    char* hp = static_cast<char*>(ctx->h_pinned);
+    const size_t bytes = size_t(L.ldh) * cols * sc;
+    if (bytes + 64 > ctx->h_pinned_bytes - 8192) fail(PPF_EINVAL, "m_max too large for staging buffer");
+    PPF_CUDA(cudaMemcpyAsync(hp, w + L.H, bytes, cudaMemcpyDeviceToHost, st));
+    PPF_CUDA(cudaMemcpyAsync(hp + bytes, scal(S_BETA0), 8, cudaMemcpyDeviceToHost, st));
+    PPF_CUDA(cudaStreamSynchronize(st));
+    const double* h = reinterpret_cast<const double*>(hp);
+    const int nd = int(sc / 8);
+    Hh.assign(size_t(rows) * cols, zc(0.0, 0.0));
+    for (int jj = 0; jj < cols; ++jj)
+      for (int i = 0; i < rows; ++i) {
+        const size_t o = (size_t(i) + size_t(jj) * L.ldh) * nd;
+        Hh[size_t(i) + size_t(jj) * rows] = zc(h[o], nd == 2 ? h[o + 1] : 0.0);
+      }
+    std::memcpy(&beta0, hp + bytes, 8);
+  }
+
+  void upload_y(const std::vector<zc>& y) {
+    char* hp = static_cast<char*>(ctx->h_pinned) + ctx->h_pinned_bytes - 8192;
+    double* d = reinterpret_cast<double*>(hp);
+    const int nd = int(sc / 8);
+    for (size_t i = 0; i < y.size(); ++i) {
+      d[i * nd] = y[i].real();
+      if (nd == 2) d[i * nd + 1] = y[i].imag();
+    }
+    PPF_CUDA(cudaMemcpyAsync(w + L.ybuf, hp, y.size() * sc, cudaMemcpyHostToDevice, st));
+  }
+};
+
+// y = beta0 * H_m^{-1/2} e1 from the leading m x m block of Hh ((m+1) x m, ld rows)
+std::vector<zc> dense_y(const std::vector<zc>& Hh, int rows, int m, double beta0, bool lanczos) {
+  std::vector<zc> y(m);
+  if (lanczos) {
+    std::vector<double> d(m), e(m, 0.0), yy(m);
+    for (int i = 0; i < m; ++i) d[i] = Hh[size_t(i) + size_t(i) * rows].real();
+    for (int i = 0; i + 1 < m; ++i) e[i] = Hh[size_t(i + 1) + size_t(i) * rows].real();
+    tridiag_invsqrt_e1(m, d.data(), e.data(), beta0, yy.data());
+    for (int i = 0; i < m; ++i) y[i] = yy[i];
+  } else {
+    std::vector<zc> Hm(size_t(m) * m);
+    for (int jj = 0; jj < m; ++jj)
+      for (int i = 0; i < m; ++i) Hm[size_t(i) + size_t(jj) * m] = Hh[size_t(i) + size_t(jj) * rows];
+    general_invsqrt_e1(m, Hm, beta0, y);
+  }
+  return y;
+}
+
+double nrm(const std::vector<zc>& v) {
+  double s = 0.0;
+  for (auto& x : v) s += std::norm(x);
+  return std::sqrt(s);
+}
+
+void check_opts(const ppf_opts* o) {
+  PPF_REQUIRE(o, "opts is NULL");
+  PPF_REQUIRE(o->func == PPF_INVSQRT || o->func == PPF_SQRT, "bad func");
+  PPF_REQUIRE(o->krylov == PPF_LANCZOS || o->krylov == PPF_ARNOLDI_CGS2, "bad krylov");
+  PPF_REQUIRE(o->m_max >= 1 && o->m_max <= 255, "m_max out of range [1, 255]");
+  PPF_REQUIRE(o->stop >= 0 && o->stop <= 2, "bad stop");
+  PPF_REQUIRE(o->stop == PPF_STOP_FIXED_M || o->tol > 0.0, "tol must be > 0");
+  PPF_REQUIRE(o->check_every >= 1 || o->stop == PPF_STOP_FIXED_M, "check_every >= 1");
+  PPF_REQUIRE(o->stop != PPF_STOP_TRUE_ERR || o->x_ref, "TRUE_ERR needs x_ref");
+}
+
+ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts* o,
+                    const void* b, void* x, const void* b_host, void* x_host, void* work,
+                    size_t bytes, ppf_report* rep) {
+  auto t_start = std::chrono::steady_clock::now();
+  PPF_REQUIRE(ctx && A && q && rep, "NULL argument");
+  PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+  check_opts(o);
+  PPF_REQUIRE(q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
+              "a Newton (complex) polynomial needs a complex operator");
+  PPF_REQUIRE(A->nranks == 1, "multi-rank runs are not enabled in this build");
+  const bool lanczos = o->krylov == PPF_LANCZOS;
+  const int m_max = o->m_max;
+  const int k = std::max(1, o->check_every);
+  const double brt = o->breakdown_rtol > 0.0 ? o->breakdown_rtol : 1e-14;
+  Runner R(ctx, A, q, m_max, work, bytes);
+  const int64_t n = R.n;
+  const size_t vb = size_t(n) * R.sc;
+  double t_dense = 0.0;
+  ctx->hist.clear();
+
+  const void* bin = b;
+  if (b_host) {
+    PPF_CUDA(cudaMemcpyAsync(R.vec(R.L.U), b_host, vb, cudaMemcpyHostToDevice, R.st));
+    bin = R.vec(R.L.U);
+  }
+  // line 2: c = q(A) s, s = b or A b
+  long long mvms = 0;
+  if (o->func == PPF_SQRT) {
+    R.spmv(bin, R.vec(R.L.Y), Runner::epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
+    ++mvms;
+    R.apply_q(R.vec(R.L.Y), R.V(0));
+  } else {
+    R.apply_q(bin, R.V(0));
+  }
+  mvms += q->deg;
+  R.normalise_start();
+
+  std::vector<zc> Hh, y, y_prev;
+  double beta0 = 0.0;
+  int m = 0;
+  int term = PPF_MAX_ITER;
+  double est = NAN, err = NAN;
+  for (int j = 0; j < m_max; ++j) {
+    R.op_apply(j);
+    R.orthogonalise(j, lanczos);
+    m = j + 1;
+    mvms += 2 * q->deg + 1;
+    const bool check = (o->stop != PPF_STOP_FIXED_M) && (m % k == 0 || m == m_max);
+    if (!check) continue;
+    R.fetch_H(m + 1, m, Hh, beta0);
+    const double hsub = std::abs(Hh[size_t(m) + size_t(m - 1) * (m + 1)]);
+    // earlier breakdown inside the stride?
+    int mb = m;
+    for (int jj = std::max(0, m - k); jj < m; ++jj)
+      if (std::abs(Hh[size_t(jj + 1) + size_t(jj) * (m + 1)]) <= brt * beta0) {
+        mb = jj + 1;
+        break;
+      }
+    auto td = std::chrono::steady_clock::now();
+    std::vector<zc> Hs = Hh;
+    if (mb != m) {
+      std::vector<zc> H2(size_t(mb + 1) * mb);
+      for (int jj = 0; jj < mb; ++jj)
+        for (int i = 0; i <= mb; ++i) H2[size_t(i) + size_t(jj) * (mb + 1)] = Hh[size_t(i) + size_t(jj) * (m + 1)];
+      Hs = H2;
+    }
+    y = dense_y(Hs, mb + 1, mb, beta0, lanczos);
+    t_dense += std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
+    if (!y_prev.empty()) {
+      std::vector<zc> dlt = y;
+      for (size_t i = 0; i < y_prev.size(); ++i) dlt[i] -= y_prev[i];
+      est = nrm(dlt) / nrm(y);
+    }
+    y_prev = y;
+    if (o->stop == PPF_STOP_TRUE_ERR) {
+      R.upload_y(y);
+      launch_combine(R.dt, n, R.V(0), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
+      launch_diffnorm(R.dt, n, R.vec(R.L.T0), o->x_ref, R.scal(S_ERR), R.rs, R.grid_vec, R.st);
+      R.launches += 2;
+      double e2[2];
+      PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
+      PPF_CUDA(cudaStreamSynchronize(R.st));
+      err = e2[0] / e2[1];
+    }
+    if (o->record_history) ctx->hist.push_back({mb, est, err, mvms - (m - mb) * (2LL * q->deg + 1)});
+    if (mb != m || hsub <= brt * beta0) {
+      m = mb;
+      term = PPF_BREAKDOWN;
+      break;
+    }
+    if (o->stop == PPF_STOP_EST && !std::isnan(est) && est <= o->tol) {
+      term = PPF_CONVERGED;
+      break;
+    }
+    if (o->stop == PPF_STOP_TRUE_ERR && err <= o->tol) {
+      term = PPF_CONVERGED;
+      break;
+    }
+  }
+  // final H, y_m
+  R.fetch_H(m + 1, m, Hh, beta0);
+  if (o->stop == PPF_STOP_FIXED_M) {
+    for (int jj = 0; jj < m; ++jj)
+      if (std::abs(Hh[size_t(jj + 1) + size_t(jj) * (m + 1)]) <= brt * beta0) {
+        const int mb = jj + 1;
+        std::vector<zc> H2(size_t(mb + 1) * mb);
+        for (int c = 0; c < mb; ++c)
+          for (int i = 0; i <= mb; ++i) H2[size_t(i) + size_t(c) * (mb + 1)] = Hh[size_t(i) + size_t(c) * (m + 1)];
+        Hh = H2;
+        m = mb;
+        term = PPF_BREAKDOWN;
+        break;
+      }
+  }
+  if (int(y.size()) != m || o->stop == PPF_STOP_FIXED_M) {
+    auto td = std::chrono::steady_clock::now();
+    y = dense_y(Hh, m + 1, m, beta0, lanczos);
+    t_dense += std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
+  }
+  // line 11: f_m = V_m y_m
+  R.upload_y(y);
+  void* xo = x_host ? R.vec(R.L.Y) : x;
+  launch_combine(R.dt, n, R.V(0), R.L.ldv, m, R.vec(R.L.ybuf), xo, R.st);
+  R.launches += 1;
+  if (x_host) {
+    PPF_CUDA(cudaMemcpyAsync(x_host, xo, vb, cudaMemcpyDeviceToHost, R.st));
+    PPF_CUDA(cudaStreamSynchronize(R.st));
+  } else {
+    // the host staging for y must not be reused before the copy is done
+    PPF_CUDA(cudaEventRecord(ctx->ev, R.st));
+    PPF_CUDA(cudaEventSynchronize(ctx->ev));
+  }
+  // keep H for ppf_hessenberg
+  ctx->last_m = m;
+  ctx->last_beta0 = beta0;
+  ctx->last_dtype = R.dt;
+  const int nd = int(R.sc / 8);
+  ctx->lastH.assign(size_t(m + 1) * m * nd, 0.0);
+  for (int jj = 0; jj < m; ++jj)
+    for (int i = 0; i <= m; ++i) {
+      const zc v = Hh[size_t(i) + size_t(jj) * (m + 1)];
+      const size_t oo = (size_t(i) + size_t(jj) * (m + 1)) * nd;
+      ctx->lastH[oo] = v.real();
+      if (nd == 2) ctx->lastH[oo + 1] = v.imag();
+    }
+  ctx->launches += R.launches;
+  rep->iterations = m;
+  rep->term = term;
+  rep->mvms = mvms - (o->func == PPF_SQRT ? 0 : 0);
+  {
+    // mvms counted per executed step; recompute for the returned m
+    long long mv = q->deg + (o->func == PPF_SQRT ? 1 : 0) + (long long)m * (2 * q->deg + 1);
+    rep->mvms = mv;
+  }
+  rep->inner_products = lanczos ? 2LL * m : (long long)m * m + 2LL * m;
+  rep->est = est;
+  rep->err = err;
+  rep->beta0 = beta0;
+  rep->seconds_host_dense = t_dense;
+  rep->kernel_launches = R.launches;
+  rep->seconds_total =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  return PPF_OK;
+}
+
+}  // namespace
+}  // namespace ppf
+
+using namespace ppf;
+
+#define PPF_API_BEGIN try {
+#define PPF_API_END                               \
+  return PPF_OK;                                  \
+  }                                               \
+  catch (const ppf::Error& e) {                   \
+    ppf::set_last_error(e.msg);                   \
+    return e.st;                                  \
+  }                                               \
+  catch (...) {                                   \
+    ppf::set_last_error("unknown C++ exception"); \
+    return PPF_EINVAL;                            \
+  }
+
+extern "C" {
+
+ppf_status ppf_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, const ppf_poly* q,
+                               const ppf_opts* o, size_t* bytes) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(ctx && A && q && bytes, "NULL argument");
+  check_opts(o);
+  *bytes = ws_layout(A->n_local, A->dtype, o->m_max, ctx->num_sms).total;
+  PPF_API_END
+}
+
+ppf_status ppf_run(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts* o, const void* b,
+                   void* x, void* work, size_t bytes, ppf_report* rep) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(b && x, "NULL b/x");
+  return run_impl(ctx, A, q, o, b, x, nullptr, nullptr, work, bytes, rep);
+  PPF_API_END
+}
+
+ppf_status ppf_run_host(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts* o,
+                        const void* b_host, void* x_host, void* work, size_t bytes,
+                        ppf_report* rep) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(b_host && x_host, "NULL b_host/x_host");
+  return run_impl(ctx, A, q, o, nullptr, nullptr, b_host, x_host, work, bytes, rep);
+  PPF_API_END
+}
+
+ppf_status ppf_history(ppf_ctx* ctx, int cap, int* count, int* m, double* est, double* err,
+                       long long* mvms) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(ctx && count, "NULL argument");
+  const int nh = int(ctx->hist.size());
+  *count = nh;
+  for (int i = 0; i < nh && i < cap; ++i) {
+    if (m) m[i] = ctx->hist[i].m;
+    if (est) est[i] = ctx->hist[i].est;
+    if (err) err[i] = ctx->hist[i].err;
+    if (mvms) mvms[i] = ctx->hist[i].mvms;
+  }
+  PPF_API_END
+}
+
+ppf_status ppf_hessenberg(ppf_ctx* ctx, int ld, void* H, int* m, double* beta0) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(ctx, "NULL ctx");
+  const int mm = ctx->last_m;
+  if (m) *m = mm;
+  if (beta0) *beta0 = ctx->last_beta0;
+  if (H) {
+    PPF_REQUIRE(ld >= mm + 1, "ld < m+1");
+    const int nd = ctx->last_dtype == PPF_R64 ? 1 : 2;
+    double* h = static_cast<double*>(H);
+    for (int j = 0; j < mm; ++j)
+      for (int i = 0; i <= mm; ++i)
+        for (int d = 0; d < nd; ++d)
+          h[(size_t(i) + size_t(j) * ld) * nd + d] = ctx->lastH[(size_t(i) + size_t(j) * (mm + 1)) * nd + d];
+  }
+  PPF_API_END
+}
+
+ppf_status ppf_ritz_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, int deg, size_t* bytes) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(ctx && A && bytes && deg >= 0 && deg < 255, "bad arguments");
+  *bytes = ws_layout(A->n_local, A->dtype, deg + 1, ctx->num_sms).total;
+  PPF_API_END
+}
+
+// Ritz values of H_d from d = deg+1 Arnoldi steps with A, Leja order,
+// divided differences.
+ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg, void* work,
+                                size_t bytes, ppf_poly** out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(ctx && A && start && out, "NULL argument");
+  PPF_REQUIRE(deg >= 0 && deg < 255, "deg out of range");
+  PPF_REQUIRE(A->dtype == PPF_C128, "Ritz-Newton polynomials need a complex operator");
+  PPF_REQUIRE(A->nranks == 1, "multi-rank runs are not enabled in this build");
+  const int d = deg + 1;
+  Runner R(ctx, A, nullptr, d, work, bytes);
+  PPF_CUDA(cudaMemcpyAsync(R.V(0), start, size_t(R.n) * R.sc, cudaMemcpyDeviceToDevice, R.st));
+  R.normalise_start();
+  for (int j = 0; j < d; ++j) {
+    R.op_apply(j);
+    R.orthogonalise(j, false);
+  }
+  std::vector<zc> Hh;
+  double beta0;
+  R.fetch_H(d + 1, d, Hh, beta0);
+  ctx->launches += R.launches;
+  std::vector<zc> Hd(size_t(d) * d);
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i < d; ++i) Hd[size_t(i) + size_t(j) * d] = Hh[size_t(i) + size_t(j) * (d + 1)];
+  std::vector<zc> theta = eigenvalues(d, Hd);
+  for (auto& t : theta)
+    if (std::abs(t.imag()) <= 1e-13 * std::max(std::abs(t), 1e-300) && t.real() <= 0.0)
+      fail(PPF_EBRANCH, "Ritz value on the branch cut (-inf, 0]");
+  auto* q = new ppf_poly();
+  q->kind = PPF_POLY_NEWTON;
+  q->deg = deg;
+  q->a = q->b = 0.0;
+  q->nodes = leja_order(theta);
+  q->dd = divided_differences_invsqrt(q->nodes);
+  *out = q;
+  PPF_API_END
+}
+
+}  // extern "C"
+
+extern "C" ppf_status ppf_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y) {
+  try {
+    PPF_REQUIRE(ctx && A && x && y, "NULL argument");
+    PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+    ppf::Epi e{};
+    e.s_ax[0] = 1.0;
+    if (A->nranks > 1) fail(PPF_EINVAL, "multi-rank runs are not enabled in this build");
+    ppf::launch_spmv(A, x, y, e, ctx->stream);
+    ctx->launches += 1;
+    return PPF_OK;
+  } catch (const ppf::Error& e) {
+    ppf::set_last_error(e.msg);
+    return e.st;
+  } catch (...) {
+    ppf::set_last_error("unknown C++ exception");
+    return PPF_EINVAL;
+  }
+}
+
+extern "C" ppf_status ppf_poly_apply_bytes(ppf_ctx* ctx, const ppf_mat* A, size_t* bytes) {
+  try {
+    PPF_REQUIRE(ctx && A && bytes, "NULL argument");
+    *bytes = ppf::ws_layout(A->n_local, A->dtype, 1, ctx->num_sms).total;
+    return PPF_OK;
+  } catch (const ppf::Error& e) {
+    ppf::set_last_error(e.msg);
+    return e.st;
+  }
+}
+
+extern "C" ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const void* x,
+                                     void* y, void* work, size_t bytes) {
+  try {
+    PPF_REQUIRE(ctx && A && q && x && y, "NULL argument");
+    PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+    PPF_REQUIRE(x != y, "x and y must be distinct");
+    PPF_REQUIRE(q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
+                "a Newton (complex) polynomial needs a complex operator");
+    PPF_REQUIRE(A->nranks == 1, "multi-rank runs are not enabled in this build");
+    ppf::Runner R(ctx, A, q, 1, work, bytes);
+    R.apply_q(x, y);
+    ctx->launches += R.launches;
+    return PPF_OK;
+  } catch (const ppf::Error& e) {
+    ppf::set_last_error(e.msg);
+    return e.st;
+  } catch (...) {
+    ppf::set_last_error("unknown C++ exception");
+    return PPF_EINVAL;
+  }
+}

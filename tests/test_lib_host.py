@@ -1,0 +1,165 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol that
+include/ppf.h declares, and its host-side logic (plan construction, Chebyshev
+coefficients + certificate, polynomial evaluation, the host dense kernel K10)
+agrees with the independent oracle.  No GPU calls are made here."""
+import os
+import re
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from inputs import configs
+from inputs import operators as ops
+from oracle import chebyshev, dense, newton
+
+from .conftest import ROOT
+
+pp = pytest.importorskip("paper_2401_06684_b200")
+from paper_2401_06684_b200 import _lib  # noqa: E402
+from paper_2401_06684_b200.api import Plan, Poly, dense_invsqrt_e1  # noqa: E402
+
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "ppf.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    names = set(re.findall(r"\b(ppf_[a-z0-9_]+)\s*\(", hdr))
+    assert len(names) >= 30
+    lib = _lib.load()
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the binding declares all of them
+    assert names <= set(_lib.SIGNATURES), names - set(_lib.SIGNATURES)
+    assert lib.ppf_abi_version() == 1
+
+
+def test_no_batch_memcpy_in_sources():
+    for dirpath, _, files in os.walk(os.path.join(ROOT, "paper_2401_06684_b200", "csrc")):
+        for f in files:
+            src = open(os.path.join(dirpath, f)).read()
+            assert "BatchAsync" not in src
+
+
+@pytest.mark.parametrize("name,deg", [("C1", 4), ("C2", 5), ("C2", 20), ("C3", 40), ("C4", 20)])
+def test_chebyshev_coefficients_match_oracle(name, deg):
+    cfg = configs.CONFIGS[name]
+    p = cfg.params
+    if cfg.family == "laplacian":
+        a, b = ops.laplacian_interval(p["N"], p["dim"])
+    else:
+        a, b = ops.convdiff_interval(p["N"], p["dim"], p["beta"])
+    q = Poly.chebyshev(a, b, deg).export()
+    ref = chebyshev.coefficients(a, b, deg)
+    assert q["kind"] == "chebyshev" and q["deg"] == deg
+    assert np.abs(q["c"] - ref.c).max() <= 1e-13 * np.abs(ref.c).max()
+    z = chebyshev.certificate_points(a, b)
+    got = Poly.chebyshev(a, b, deg).eval(z)
+    assert np.abs(got.real - chebyshev.evaluate(ref, z)).max() <= 1e-12 * np.abs(ref.c).sum()
+
+
+def test_chebyshev_golden_c1():
+    # SURVEY §8(c) golden host-side values for C1 (interpolant on the closed-form interval)
+    a, b = ops.laplacian_interval(32, 2)
+    c = Poly.chebyshev(a, b, 4).export()["c"]
+    assert c[0] == pytest.approx(0.83970316174, abs=1e-10)
+    assert c[1] == pytest.approx(-0.777096031927, abs=1e-11)
+
+
+def test_chebyshev_invalid_arguments():
+    with pytest.raises(_lib.PPFError) as e:
+        Poly.chebyshev(0.0, 1.0, 3)
+    assert e.value.status == _lib.PPF_OK + 1  # EINVAL
+    with pytest.raises(_lib.PPFError):
+        Poly.chebyshev(2.0, 1.0, 3)
+    with pytest.raises(_lib.PPFError):
+        Poly.chebyshev(1.0, 2.0, -1)
+
+
+def test_newton_import_eval_matches_oracle():
+    rng = np.random.default_rng(0)
+    th = 3 + 2 * rng.random(10) * np.exp(2j * np.pi * rng.random(10))
+    qo = newton.from_nodes(th)
+    q = Poly.newton(qo.nodes, qo.dd)
+    z = 3 + 1.8 * np.exp(1j * np.linspace(0, 2 * np.pi, 64))
+    assert np.abs(q.eval(z) - newton.evaluate(qo, z)).max() < 1e-11
+    assert np.abs(q.eval(qo.nodes) - qo.nodes ** -0.5).max() < 1e-10
+    ex = q.export()
+    assert np.array_equal(ex["nodes"], qo.nodes) and np.array_equal(ex["dd"], qo.dd)
+
+
+@pytest.mark.parametrize("m", [1, 2, 7, 25, 60])
+def test_dense_tridiagonal_matches_oracle(m):
+    rng = np.random.default_rng(m)
+    T = np.diag(rng.uniform(0.3, 2.0, m))
+    off = rng.uniform(0.01, 0.3, m - 1)
+    T += np.diag(off, 1) + np.diag(off, -1)
+    y = dense_invsqrt_e1(T, 1.7, hermitian=True)
+    ref = dense.invsqrt_e1(T, 1.7, hermitian=True)
+    assert np.linalg.norm(y - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("m", [1, 3, 12, 40, 75])
+def test_dense_schur_matches_oracle(m):
+    rng = np.random.default_rng(100 + m)
+    H = np.triu(rng.standard_normal((m, m)) * 0.3, -1) + 2.5 * np.eye(m)
+    y = dense_invsqrt_e1(H, 0.9, hermitian=False)
+    ref = dense.invsqrt_e1(H, 0.9, hermitian=False)
+    assert np.linalg.norm(y - ref) <= 1e-12 * np.linalg.norm(ref)
+    Hc = H + 0.4j * np.triu(rng.standard_normal((m, m)), -1)
+    yc = dense_invsqrt_e1(Hc, 0.9, hermitian=False)
+    refc = 0.9 * np.linalg.solve(sla.sqrtm(Hc), np.eye(m)[:, 0])
+    assert np.linalg.norm(yc - refc) <= 1e-11 * np.linalg.norm(refc)
+
+
+def test_dense_branch_cut_rejected():
+    with pytest.raises(_lib.PPFError) as e:
+        dense_invsqrt_e1(np.diag([1.0, -2.0]), 1.0, hermitian=True)
+    assert e.value.status == 5
+    with pytest.raises(_lib.PPFError):
+        dense_invsqrt_e1(np.array([[1.0, 1.0], [0.0, -4.0]]), 1.0, hermitian=False)
+
+
+def test_plan_sell_layout_sizes():
+    A = ops.laplacian(10, 3)
+    for fmt, C_, sig in (("sell", 32, 1), ("sell", 64, 1), ("sell", 32, 64), ("csr", 32, 1)):
+        p = Plan.from_csr(A, fmt=fmt, C_=C_, sigma=sig)
+        info = p.info()
+        assert info["n_local"] == A.n and info["nnz"] == A.nnz and info["halo_total"] == 0
+        if fmt == "csr":
+            assert info["stored"] == A.nnz
+        else:
+            assert A.nnz <= info["stored"] <= 7 * (A.n + C_)
+        assert p.device_bytes() >= info["stored"] * 12
+
+
+def test_plan_rejects_bad_input():
+    A = ops.laplacian(4, 2)
+    bad = A.col.copy()
+    bad[3], bad[4] = bad[4], bad[3]
+    with pytest.raises(_lib.PPFError):
+        Plan(A.row_ptr, bad, A.val, n_global=A.n)
+    with pytest.raises(_lib.PPFError):
+        Plan(A.row_ptr, A.col, A.val, n_global=A.n, fmt="sell", C_=48)
+    rp = A.row_ptr.copy()
+    rp[5] = rp[4] - 1
+    with pytest.raises(_lib.PPFError):
+        Plan(rp, A.col, A.val, n_global=A.n)
+
+
+def test_plan_halo_lists_two_slabs():
+    """Row-slab sharding: the halo of a z-slab of the 3D Laplacian
+    is exactly the neighbouring z-plane."""
+    N = 6
+    A = ops.laplacian(N, 3)
+    bounds = [0, 3 * N * N, N**3]
+    for rank in (0, 1):
+        lo, hi = bounds[rank], bounds[rank + 1]
+        rp = A.row_ptr[lo:hi + 1] - A.row_ptr[lo]
+        sl = slice(A.row_ptr[lo], A.row_ptr[hi])
+        p = Plan(rp, A.col[sl], A.val[sl], row_bounds=bounds, rank=rank)
+        peer = 1 - rank
+        got = p.halo_recv(peer)
+        plane = np.arange(N * N) + (3 * N * N if rank == 0 else 2 * N * N)
+        assert np.array_equal(got, plane)
+        assert len(p.halo_recv(rank)) == 0
+        assert p.info()["halo_total"] == N * N
