@@ -231,6 +231,18 @@ ppf_status ppf_history(ppf_ctx* ctx, int cap, int* count, int* m, double* est, d
                        long long* mvms);
 ppf_status ppf_hessenberg(ppf_ctx* ctx, int ld, void* H, int* m, double* beta0);
 
+/* Optional device timing of the hot-path kernels: with profiling on, every
+ * kernel launch of ppf_run / ppf_poly_apply / ppf_poly_ritz_newton is
+ * bracketed by CUDA events on the context stream; per class the library
+ * accumulates launches, device milliseconds and ALGORITHMIC bytes (the minimum
+ * HBM traffic of that launch: SpMV (s+4) nnz + s n (x, out, [z], [u]);
+ * CGS sweeps (ncols + 1 or 2) s n).
+ * cls: 0 = SpMV / fused chain steps, 1 = orthogonalisation (CGS2, Lanczos,
+ * scaling), 2 = other (norms, combine).  ppf_profile_enable resets. */
+ppf_status ppf_profile_enable(ppf_ctx* ctx, int on);
+ppf_status ppf_profile_read(ppf_ctx* ctx, int cls, long long* launches, double* ms,
+                            double* bytes);
+
 /* ----------------------------------------------------------------------------
  * Host dense kernel (layer L4, K10), exposed for tests:
  * y = beta0 * H^{-1/2} e_1 for an m x m matrix H (column-major, leading

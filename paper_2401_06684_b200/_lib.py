@@ -75,6 +75,8 @@ SIGNATURES = {
     "ppf_history": (C.c_int, [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), dblp, dblp,
                               C.POINTER(C.c_longlong)]),
     "ppf_hessenberg": (C.c_int, [vp, C.c_int, vp, C.POINTER(C.c_int), dblp]),
+    "ppf_profile_enable": (C.c_int, [vp, C.c_int]),
+    "ppf_profile_read": (C.c_int, [vp, C.c_int, C.POINTER(C.c_longlong), dblp, dblp]),
     "ppf_dense_invsqrt_e1": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.c_double, C.c_int, vp]),
 }
 

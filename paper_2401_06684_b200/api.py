@@ -372,3 +372,20 @@ def dense_invsqrt_e1(H: np.ndarray, beta0: float, hermitian: bool) -> np.ndarray
     check(_lib().ppf_dense_invsqrt_e1(L.C128 if cplx else L.R64, m, Hf.ctypes.data_as(C.c_void_p),
                                       m, float(beta0), int(hermitian), y.ctypes.data_as(C.c_void_p)))
     return y
+
+
+def profile_enable(ctx: Context, on: bool = True):
+    """ppf_profile_enable: event-time every hot-path kernel launch (resets counters)."""
+    check(_lib().ppf_profile_enable(ctx.h, int(bool(on))))
+
+
+def profile_read(ctx: Context) -> dict:
+    """ppf_profile_read for the three kernel classes."""
+    out = {}
+    for cls, name in ((0, "spmv"), (1, "ortho"), (2, "other")):
+        n = C.c_longlong()
+        ms = C.c_double()
+        by = C.c_double()
+        check(_lib().ppf_profile_read(ctx.h, cls, C.byref(n), C.byref(ms), C.byref(by)))
+        out[name] = {"launches": n.value, "ms": ms.value, "bytes": by.value}
+    return out

@@ -92,6 +92,8 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
   c->last_beta0 = 0.0;
   c->last_dtype = PPF_R64;
   c->launches = 0;
+  c->profile = 0;
+  for (auto& p : c->prof) p = {0, 0.0, 0.0};
   try {
     PPF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     c->h_pinned_bytes = size_t(258) * 256 * 16 + 16384;
@@ -113,8 +115,26 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
   PPF_API_END
 }
 
+ppf_status ppf_profile_enable(ppf_ctx* c, int on) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(c, "NULL ctx");
+  c->profile = on ? 1 : 0;
+  for (auto& p : c->prof) p = {0, 0.0, 0.0};
+  PPF_API_END
+}
+
+ppf_status ppf_profile_read(ppf_ctx* c, int cls, long long* launches, double* ms, double* bytes) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(c && cls >= 0 && cls < 3, "bad arguments");
+  if (launches) *launches = c->prof[cls].launches;
+  if (ms) *ms = c->prof[cls].ms;
+  if (bytes) *bytes = c->prof[cls].bytes;
+  PPF_API_END
+}
+
 void ppf_ctx_destroy(ppf_ctx* c) {
   if (!c) return;
+  for (auto e : c->prof_pool) cudaEventDestroy(e);
   if (c->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->ev) cudaEventDestroy(c->ev);

@@ -180,6 +180,13 @@ struct ppf_ctx {
   double last_beta0;
   ppf_dtype last_dtype;
   long long launches;
+  // optional per-kernel-class timing with CUDA events on the context stream
+  int profile;
+  std::vector<cudaEvent_t> prof_pool;
+  struct ProfAcc {
+    long long launches;
+    double ms, bytes;
+  } prof[3];  // 0 = SpMV (fused chain steps), 1 = orthogonalisation, 2 = other
 };
 
 namespace ppf {

@@ -115,17 +115,17 @@ struct Runner {
   // ----- SpMV with halo exchange (nranks > 1) -----
   void spmv(const void* x, void* out, const Epi& e) {
     if (A->nranks > 1) exchange(x);
-    launch_spmv(A, x, out, e, st);
-    ++launches;
-    if (A->nranks > 1 && A->halo_rows) {
-      launch_halo_apply(A, out, e.s_ax, st);
-      ++launches;
-    }
+    // algorithmic bytes: values + column indices once, x gathered once, out
+    // written once, z and u streamed once
+    const double bytes = double(sc + 4) * double(A->nnz) +
+                         double(sc) * double(n) * (2 + (e.z ? 1 : 0) + (e.u ? 1 : 0));
+    timed(0, bytes, [&] { launch_spmv(A, x, out, e, st); });
+    if (A->nranks > 1 && A->halo_rows)
+      timed(2, 0.0, [&] { launch_halo_apply(A, out, e.s_ax, st); });
   }
 
   void exchange(const void* x) {
-    launch_halo_pack(A, x, st);
-    ++launches;
+    timed(2, 0.0, [&] { launch_halo_pack(A, x, st); });
     auto comm = static_cast<ncclComm_t>(ctx->nccl_comm);
     const int nd = int(sc / 8);
     if (ncclGroupStart() != ncclSuccess) fail(PPF_ENCCL, "ncclGroupStart");
@@ -162,8 +162,7 @@ struct Runner {
     // a SpMV-free scaled copy: reuse the SpMV epilogue would need A; use scale
     if (c.imag() != 0.0 && dt == PPF_R64) fail(PPF_EINVAL, "complex coefficient on a real operator");
     if (c.imag() == 0.0) {
-      launch_scale(dt, n, in, out, nullptr, c.real(), st);
-      ++launches;
+      timed(2, 2.0 * n * sc, [&] { launch_scale(dt, n, in, out, nullptr, c.real(), st); });
     } else {
       fail(PPF_EINVAL, "degree-0 complex Newton polynomial not supported");
     }
@@ -239,33 +238,87 @@ struct Runner {
   }
 
   void orthogonalise(int j, bool lanczos) {
+    const double vb = double(n) * double(sc);
     if (lanczos) {
       const double* bprev = j > 0 ? reinterpret_cast<const double*>(Hp(j, j - 1)) : nullptr;
-      launch_lanczos(dt, 1, n, V(j), j > 0 ? V(j - 1) : nullptr, bprev, V(j + 1), Hp(j, j),
-                     nullptr, nullptr, nullptr, rs, grid_vec, st);
-      launch_lanczos(dt, 2, n, V(j), nullptr, nullptr, V(j + 1), Hp(j, j), Hp(j + 1, j),
-                     Hp(j, j + 1), scal(S_INV), rs, grid_vec, st);
-      launches += 2;
+      timed(1, vb * (j > 0 ? 4 : 3), [&] {
+        launch_lanczos(dt, 1, n, V(j), j > 0 ? V(j - 1) : nullptr, bprev, V(j + 1), Hp(j, j),
+                       nullptr, nullptr, nullptr, rs, grid_vec, st);
+      });
+      timed(1, vb * 3, [&] {
+        launch_lanczos(dt, 2, n, V(j), nullptr, nullptr, V(j + 1), Hp(j, j), Hp(j + 1, j),
+                       Hp(j, j + 1), scal(S_INV), rs, grid_vec, st);
+      });
     } else {
       void* hb = vec(L.hbuf);
       void* gb = vec(L.gbuf);
-      launch_cgs(dt, 0, n, V(0), L.ldv, j + 1, V(j + 1), nullptr, hb, nullptr, nullptr, nullptr,
-                 rs, grid_cgs, st);
-      launch_cgs(dt, 1, n, V(0), L.ldv, j + 1, V(j + 1), hb, gb, Hp(0, j), nullptr, nullptr, rs,
-                 grid_cgs, st);
-      launch_cgs(dt, 2, n, V(0), L.ldv, j + 1, V(j + 1), gb, nullptr, nullptr, Hp(j + 1, j),
-                 scal(S_INV), rs, grid_cgs, st);
-      launches += 3;
+      timed(1, vb * (j + 2), [&] {
+        launch_cgs(dt, 0, n, V(0), L.ldv, j + 1, V(j + 1), nullptr, hb, nullptr, nullptr, nullptr,
+                   rs, grid_cgs, st);
+      });
+      timed(1, vb * (j + 3), [&] {
+        launch_cgs(dt, 1, n, V(0), L.ldv, j + 1, V(j + 1), hb, gb, Hp(0, j), nullptr, nullptr, rs,
+                   grid_cgs, st);
+      });
+      timed(1, vb * (j + 3), [&] {
+        launch_cgs(dt, 2, n, V(0), L.ldv, j + 1, V(j + 1), gb, nullptr, nullptr, Hp(j + 1, j),
+                   scal(S_INV), rs, grid_cgs, st);
+      });
     }
-    launch_scale(dt, n, V(j + 1), V(j + 1), scal(S_INV), 0.0, st);
-    ++launches;
+    timed(1, vb * 2, [&] { launch_scale(dt, n, V(j + 1), V(j + 1), scal(S_INV), 0.0, st); });
   }
 
   // start: V0 = s/||s||  (||s|| -> scal(S_BETA0))
   void normalise_start() {
-    launch_norm(dt, n, V(0), scal(S_BETA0), rs, grid_vec, st);
-    launch_scale(dt, n, V(0), V(0), scal(S_INV0), 0.0, st);
-    launches += 2;
+    const double vb = double(n) * double(sc);
+    timed(2, vb, [&] { launch_norm(dt, n, V(0), scal(S_BETA0), rs, grid_vec, st); });
+    timed(2, 2 * vb, [&] { launch_scale(dt, n, V(0), V(0), scal(S_INV0), 0.0, st); });
+  }
+
+  // ----- optional event timing per kernel class (ppf_profile_enable) -----
+  struct Pend {
+    int cls, e0, e1;
+    double bytes;
+  };
+  std::vector<Pend> pend;
+  size_t next_ev = 0;
+
+  cudaEvent_t ev_at(size_t i) {
+    while (ctx->prof_pool.size() <= i) {
+      cudaEvent_t e;
+      PPF_CUDA(cudaEventCreate(&e));
+      ctx->prof_pool.push_back(e);
+    }
+    return ctx->prof_pool[i];
+  }
+
+  // run f (which launches exactly one kernel), counting it; with profiling on
+  // bracket it with events and remember its algorithmic bytes.
+  template <typename F> void timed(int cls, double bytes, F&& f) {
+    ++launches;
+    if (!ctx->profile) {
+      f();
+      return;
+    }
+    const int a = int(next_ev);
+    PPF_CUDA(cudaEventRecord(ev_at(next_ev++), st));
+    f();
+    const int b = int(next_ev);
+    PPF_CUDA(cudaEventRecord(ev_at(next_ev++), st));
+    pend.push_back({cls, a, b, bytes});
+  }
+
+  // after the stream has been synchronised
+  void flush_prof() {
+    for (auto& p : pend) {
+      float ms = 0.f;
+      PPF_CUDA(cudaEventElapsedTime(&ms, ctx->prof_pool[p.e0], ctx->prof_pool[p.e1]));
+      ctx->prof[p.cls].launches += 1;
+      ctx->prof[p.cls].ms += ms;
+      ctx->prof[p.cls].bytes += p.bytes;
+    }
+    pend.clear();
+    next_ev = 0;
   }
 
   // copy H[0:rows, 0:cols] (and beta0) to pinned host; wait.
@@ -410,9 +463,12 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     y_prev = y;
     if (o->stop == PPF_STOP_TRUE_ERR) {
       R.upload_y(y);
-      launch_combine(R.dt, n, R.V(0), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
-      launch_diffnorm(R.dt, n, R.vec(R.L.T0), o->x_ref, R.scal(S_ERR), R.rs, R.grid_vec, R.st);
-      R.launches += 2;
+      R.timed(2, double(vb) * (mb + 1), [&] {
+        launch_combine(R.dt, n, R.V(0), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
+      });
+      R.timed(2, 2.0 * vb, [&] {
+        launch_diffnorm(R.dt, n, R.vec(R.L.T0), o->x_ref, R.scal(S_ERR), R.rs, R.grid_vec, R.st);
+      });
       double e2[2];
       PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
       PPF_CUDA(cudaStreamSynchronize(R.st));
@@ -456,8 +512,9 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   // line 11: f_m = V_m y_m
   R.upload_y(y);
   void* xo = x_host ? R.vec(R.L.Y) : x;
-  launch_combine(R.dt, n, R.V(0), R.L.ldv, m, R.vec(R.L.ybuf), xo, R.st);
-  R.launches += 1;
+  R.timed(2, double(vb) * (m + 1), [&] {
+    launch_combine(R.dt, n, R.V(0), R.L.ldv, m, R.vec(R.L.ybuf), xo, R.st);
+  });
   if (x_host) {
     PPF_CUDA(cudaMemcpyAsync(x_host, xo, vb, cudaMemcpyDeviceToHost, R.st));
     PPF_CUDA(cudaStreamSynchronize(R.st));
@@ -466,6 +523,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     PPF_CUDA(cudaEventRecord(ctx->ev, R.st));
     PPF_CUDA(cudaEventSynchronize(ctx->ev));
   }
+  R.flush_prof();
   // keep H for ppf_hessenberg
   ctx->last_m = m;
   ctx->last_beta0 = beta0;
@@ -605,6 +663,7 @@ ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int
   std::vector<zc> Hh;
   double beta0;
   R.fetch_H(d + 1, d, Hh, beta0);
+  R.flush_prof();
   ctx->launches += R.launches;
   std::vector<zc> Hd(size_t(d) * d);
   for (int j = 0; j < d; ++j)
@@ -666,6 +725,10 @@ extern "C" ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q
     PPF_REQUIRE(A->nranks == 1, "multi-rank runs are not enabled in this build");
     ppf::Runner R(ctx, A, q, 1, work, bytes);
     R.apply_q(x, y);
+    if (ctx->profile) {
+      PPF_CUDA(cudaStreamSynchronize(R.st));
+      R.flush_prof();
+    }
     ctx->launches += R.launches;
     return PPF_OK;
   } catch (const ppf::Error& e) {

@@ -126,13 +126,47 @@ def _reference(cfg, A, b):
     return reference.arnoldi_reference(Operator(A.to_scipy()), b, func=cfg.func).x
 
 
-def _compare(ctx, res_o, x_gpu, rep, complex_):
+def _clenshaw_np(q, op, v):
+    """Test-local Clenshaw evaluation of a Chebyshev q (numpy): a rounding
+    perturbation of the oracle's forward recurrence, same mathematics."""
+    al, be = 2 / (q.b - q.a), -(q.a + q.b) / (q.b - q.a)
+    d = q.deg
+    if d == 0:
+        return q.c[0] * v
+    b1 = q.c[d] * v
+    b2 = np.zeros_like(v)
+    for k in range(d - 1, 0, -1):
+        b1, b2 = q.c[k] * v + 2 * (al * op.matvec(b1) + be * b1) - b2, b1
+    return q.c[0] * v + (al * op.matvec(b1) + be * b1) - b2
+
+
+def h_tolerance(A, b, q, **kw):
+    """H-parity bar: 1e-11 (north_star), raised only where the Arnoldi process
+    itself amplifies rounding beyond it.  The amplification is measured, not
+    assumed: two oracle runs that differ only in the rounding of q(A)v
+    (forward recurrence vs Clenshaw) -- e.g. C2 deg 20 (cond(D) = 4e8,
+    SURVEY F3) gives 1.2e-10.  The bar is then 10x that oracle-vs-oracle gap."""
+    if not isinstance(q, chebyshev.ChebPoly):
+        return H_TOL
+    op = Operator(A.to_scipy())
+    r1 = krylov.run(op, b, q, stop="fixed", **kw)
+    orig = krylov.apply_q
+    try:
+        krylov.apply_q = _clenshaw_np
+        r2 = krylov.run(op, b, q, stop="fixed", **kw)
+    finally:
+        krylov.apply_q = orig
+    gap = np.abs(r1.H - r2.H).max() / np.abs(r1.H).max()
+    return max(H_TOL, 10 * gap)
+
+
+def _compare(ctx, res_o, x_gpu, rep, complex_, h_tol=H_TOL):
     assert rep.iterations == res_o.m
     assert np.linalg.norm(x_gpu - res_o.x) <= X_TOL * np.linalg.norm(res_o.x)
     Hg, beta0 = pp.hessenberg(ctx, complex_)
     Ho = res_o.H
     assert Hg.shape == Ho.shape
-    assert np.abs(Hg - Ho).max() <= H_TOL * np.abs(Ho).max()
+    assert np.abs(Hg - Ho).max() <= h_tol * np.abs(Ho).max()
     assert beta0 == pytest.approx(res_o.beta0, rel=1e-13)
 
 
@@ -156,7 +190,8 @@ def test_run_parity_true_error(ctx, name, deg):
     xg, rep = pp.run(ctx, M, q, dev(b), func=cfg.func, krylov=cfg.krylov, m_max=cfg.m_max,
                      stop="true", tol=cfg.tol, x_ref=dev(xr))
     assert rep.term == "converged"
-    _compare(ctx, res_o, host(xg), rep, False)
+    htol = h_tolerance(A, b, qo, func=cfg.func, krylov=cfg.krylov, m_max=res_o.m)
+    _compare(ctx, res_o, host(xg), rep, False, htol)
     assert rep.mvms == res_o.mvms
     assert rep.inner_products == res_o.inner_products
 
@@ -172,7 +207,8 @@ def test_run_parity_estimate_stop(ctx, name, deg):
     M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=64))
     xg, rep = pp.run(ctx, M, pp.Poly.chebyshev(*iv, deg), dev(b), func=cfg.func,
                      krylov=cfg.krylov, m_max=cfg.m_max, stop="est", tol=cfg.tol)
-    _compare(ctx, res_o, host(xg), rep, False)
+    htol = h_tolerance(A, b, qo, func=cfg.func, krylov=cfg.krylov, m_max=res_o.m)
+    _compare(ctx, res_o, host(xg), rep, False, htol)
     hist = pp.history(ctx)
     assert [h["m"] for h in hist] == [h["m"] for h in res_o.history]
     for hg, ho in zip(hist, res_o.history):
