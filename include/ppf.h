@@ -78,9 +78,12 @@ int ppf_abi_version(void);
  * ppf_nccl_unique_id: writes 128 bytes (an ncclUniqueId) to host `out128`; call
  *   on rank 0 and broadcast the bytes (e.g. torch.distributed) to the others.
  * ppf_ctx_create: device = CUDA ordinal; cuda_stream = cudaStream_t to enqueue
- *   on (NULL = the legacy default stream).  nranks > 1 requires id128 (the
- *   broadcast unique id) and initialises an NCCL communicator; nranks == 1
- *   ignores id128.
+ *   on (NULL = the legacy default stream).  nranks > 1 with id128 (the
+ *   broadcast unique id) initialises an NCCL communicator; nranks > 1 with
+ *   id128 == NULL creates a context WITHOUT a communicator whose halo exchange
+ *   is done by the caller through ppf_halo_pack / ppf_halo_buffers /
+ *   ppf_spmv_local (testing the sharded SpMV in one process); ppf_run and
+ *   ppf_spmv then return PPF_ESTATE.  nranks == 1 ignores id128.
  * ------------------------------------------------------------------------- */
 ppf_status ppf_nccl_unique_id(void* out128);
 ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128,
@@ -128,6 +131,17 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* plan, void* device_buf,
                           size_t bytes, ppf_mat** out);
 ppf_status ppf_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
 void ppf_mat_destroy(ppf_mat* A);
+/* Pieces of the sharded SpMV, for callers that move the halo
+ * themselves: ppf_halo_pack gathers this rank's boundary entries of x (device)
+ * into the send buffer; ppf_halo_buffers returns the device send / receive
+ * buffers (per-peer segments in peer order, lengths from the plan's lists:
+ * send segment of peer p = the rows set by ppf_plan_set_halo_send(p), receive
+ * segment of peer p = ppf_plan_halo_recv(p)); ppf_spmv_local computes y = A x
+ * from the local x and the CURRENT receive buffer (diagonal block + halo block)
+ * without communicating. */
+ppf_status ppf_halo_pack(ppf_ctx* ctx, ppf_mat* A, const void* x);
+ppf_status ppf_halo_buffers(ppf_mat* A, void** send, void** recv);
+ppf_status ppf_spmv_local(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
 
 /* ----------------------------------------------------------------------------
  * Preconditioning polynomial q ~ z^{-1/2} (layer L1), a host object.

@@ -59,6 +59,9 @@ SIGNATURES = {
     "ppf_mat_create": (C.c_int, [vp, vp, vp, C.c_size_t, C.POINTER(vp)]),
     "ppf_spmv": (C.c_int, [vp, vp, vp, vp]),
     "ppf_mat_destroy": (None, [vp]),
+    "ppf_halo_pack": (C.c_int, [vp, vp, vp]),
+    "ppf_halo_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
+    "ppf_spmv_local": (C.c_int, [vp, vp, vp, vp]),
     "ppf_poly_chebyshev": (C.c_int, [C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
     "ppf_ritz_workspace_bytes": (C.c_int, [vp, vp, C.c_int, C.POINTER(C.c_size_t)]),
     "ppf_poly_ritz_newton": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_size_t, C.POINTER(vp)]),

@@ -389,3 +389,34 @@ def profile_read(ctx: Context) -> dict:
         check(_lib().ppf_profile_read(ctx.h, cls, C.byref(n), C.byref(ms), C.byref(by)))
         out[name] = {"launches": n.value, "ms": ms.value, "bytes": by.value}
     return out
+
+
+class _CudaBuf:
+    """Exposes a raw device pointer to torch through __cuda_array_interface__."""
+
+    def __init__(self, ptr: int, n: int, complex_: bool):
+        self.__cuda_array_interface__ = {
+            "shape": (n,), "typestr": "<c16" if complex_ else "<f8",
+            "data": (ptr, False), "version": 2, "strides": None}
+
+
+def halo_pack(ctx: Context, A: Matrix, x):
+    """ppf_halo_pack: gather this rank's boundary entries of x into the send buffer."""
+    check(_lib().ppf_halo_pack(ctx.h, A.h, C.c_void_p(x.data_ptr())))
+
+
+def halo_buffers(A: Matrix, send_total: int, recv_total: int):
+    """ppf_halo_buffers as torch views (no copy) of the device send / recv buffers."""
+    torch = _torch()
+    s, r = C.c_void_p(), C.c_void_p()
+    check(_lib().ppf_halo_buffers(A.h, C.byref(s), C.byref(r)))
+    cplx = A.dtype == L.C128
+    dev = torch.device(f"cuda:{A.ctx.device}")
+    sb = torch.as_tensor(_CudaBuf(s.value or 0, send_total, cplx), device=dev) if send_total else None
+    rb = torch.as_tensor(_CudaBuf(r.value or 0, recv_total, cplx), device=dev) if recv_total else None
+    return sb, rb
+
+
+def spmv_local(ctx: Context, A: Matrix, x, y):
+    """ppf_spmv_local: y = A x from local x and the current receive buffer."""
+    check(_lib().ppf_spmv_local(ctx.h, A.h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr())))

@@ -80,7 +80,6 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
   PPF_API_BEGIN
   PPF_REQUIRE(out, "out is NULL");
   PPF_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank/nranks");
-  PPF_REQUIRE(nranks == 1 || id128, "nranks > 1 needs the NCCL unique id");
   PPF_CUDA(cudaSetDevice(device));
   auto* c = new ppf_ctx();
   c->device = device;
@@ -99,7 +98,7 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
     c->h_pinned_bytes = size_t(258) * 256 * 16 + 16384;
     PPF_CUDA(cudaHostAlloc(&c->h_pinned, c->h_pinned_bytes, cudaHostAllocDefault));
     PPF_CUDA(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
-    if (nranks > 1) {
+    if (nranks > 1 && id128) {
       ncclUniqueId id;
       std::memcpy(&id, id128, 128);
       ncclComm_t comm;

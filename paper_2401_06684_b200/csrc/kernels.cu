@@ -256,7 +256,7 @@ __global__ void scale_kernel(int64_t n, const T* __restrict__ src, T* __restrict
 template <typename T>
 __global__ void __launch_bounds__(256) norm_kernel(int64_t n, const T* __restrict__ v,
                                                    double* __restrict__ out, double* partials,
-                                                   unsigned* counter) {
+                                                   unsigned* counter, double* raw) {
   __shared__ double sm[32];
   double s = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -266,11 +266,55 @@ __global__ void __launch_bounds__(256) norm_kernel(int64_t n, const T* __restric
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
   if (last_block(counter)) {
     reduce_partials(partials, gridDim.x, 1, 1, [&](int, double t) {
-      const double nrm = sqrt(t);
-      out[0] = nrm;
-      out[1] = 1.0 / nrm;
+      if (raw) {  // multi-rank: rank-local sum, finalised after the allreduce
+        raw[0] = t;
+      } else {
+        const double nrm = sqrt(t);
+        out[0] = nrm;
+        out[1] = 1.0 / nrm;
+      }
       *counter = 0;
     });
+  }
+}
+
+// Finalisation of a reduction after the cross-rank allreduce of its raw sums
+// (op codes FIN_* in ppf_internal.h).
+__global__ void finalize_kernel(int op, int nv, int nd, const double* __restrict__ raw,
+                                double* o0, double* o1, double* o2, const double* ci) {
+  const int i = threadIdx.x;
+  switch (op) {
+    case FIN_NORM:
+      if (i == 0) {
+        o0[0] = sqrt(raw[0]);
+        o0[1] = 1.0 / o0[0];
+      }
+      break;
+    case FIN_SQRT:
+      if (i < nv) o0[i] = sqrt(raw[i]);
+      break;
+    case FIN_COEF:
+      for (int k = i; k < nv; k += blockDim.x) {
+        o0[k] = raw[k];
+        if (o1) o1[k] = ci[k] + raw[k];
+      }
+      break;
+    case FIN_SUBNORM:
+    case FIN_LZ2:
+      if (i == 0) {
+        const double b = sqrt(raw[0]);
+        o0[0] = b;
+        if (nd == 2) o0[1] = 0.0;
+        if (op == FIN_LZ2) {
+          o1[0] = b;
+          if (nd == 2) o1[1] = 0.0;
+        }
+        o2[0] = 1.0 / b;
+      }
+      break;
+    case FIN_LZ1:
+      if (i < nd) o0[i] = raw[i];
+      break;
   }
 }
 
@@ -278,7 +322,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) diffnorm_kernel(int64_t n, const T* __restrict__ a,
                                                        const T* __restrict__ b,
                                                        double* __restrict__ out, double* partials,
-                                                       unsigned* counter) {
+                                                       unsigned* counter, double* raw) {
   __shared__ double sm[32];
   double s = 0.0, t = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -294,7 +338,12 @@ __global__ void __launch_bounds__(256) diffnorm_kernel(int64_t n, const T* __res
     partials[2 * blockIdx.x + 1] = t;
   }
   if (last_block(counter)) {
-    reduce_partials(partials, gridDim.x, 2, 2, [&](int i, double v) { out[i] = sqrt(v); });
+    reduce_partials(partials, gridDim.x, 2, 2, [&](int i, double v) {
+      if (raw)
+        raw[i] = v;
+      else
+        out[i] = sqrt(v);
+    });
     __syncthreads();
     if (threadIdx.x == 0) *counter = 0;
   }
@@ -317,111 +366,102 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t n, const T* __rest
 }
 
 // ---------------------------------------------------------------------------
-// CGS2 sweeps.  Block = 8 warps; warp w owns columns c = w + 8 t (t < CPW);
-// lanes own rows (RPL rows per lane per chunk).  Grid-stride over row chunks.
+// CGS2 sweeps (K5/K6/K7) on a column tile [c0, c0+nct) of V, nct <= NC.
+// One row per thread per iteration (grid-stride), the row's nct basis values
+// held in registers; no block barrier inside the row loop.  Flags:
+//   UPD : w -= V_tile coef_in_tile          (w written back)
+//   PROJ: coef_out_tile = V_tile^H w        (after UPD if both)
+//   NRM : ||w||^2 -> Hsub = ||w||, inv = 1/||w||
+// With PROJ|UPD the finalisation also writes Hcol = coef_in + coef_out.
 // ---------------------------------------------------------------------------
-constexpr int CGS_WARPS = 8;
+constexpr int F_UPD = 1, F_PROJ = 2, F_NRM = 4;
 
-template <typename T, int CPW, int RPL, int MODE>
-__global__ void __launch_bounds__(256) cgs_kernel(int64_t n, const T* __restrict__ V, int64_t ldv,
-                                                  int ncols, T* __restrict__ w,
+template <typename T, int NC, int FL>
+__global__ void __launch_bounds__(256, (NC * sizeof(T) <= 128) ? 4 : 2)
+    cgs_kernel(int64_t n, const T* __restrict__ V, int64_t ldv,
+                                                  int nct, T* __restrict__ w,
                                                   const T* __restrict__ coef_in,
                                                   T* __restrict__ coef_out, T* __restrict__ Hcol,
                                                   T* __restrict__ Hsub, double* __restrict__ inv,
-                                                  double* partials, unsigned* counter) {
+                                                  double* partials, unsigned* counter,
+                                                  double* raw) {
   constexpr int ND = n_doubles<T>();
-  constexpr int ROWS = 32 * RPL;
-  __shared__ T red[CGS_WARPS][ROWS];
-  __shared__ T cin[CGS_WARPS * CPW];
-  __shared__ double smn[32];
+  constexpr bool UPD = FL & F_UPD, PROJ = FL & F_PROJ, NRM = FL & F_NRM;
+  __shared__ T cin[NC];
+  __shared__ double red[8][NC * ND + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (MODE != 0) {
-    for (int c = threadIdx.x; c < ncols; c += blockDim.x) cin[c] = coef_in[c];
+  if (UPD) {
+    for (int c = threadIdx.x; c < nct; c += blockDim.x) cin[c] = coef_in[c];
     __syncthreads();
   }
-  T acc[CPW];
+  T acc[NC];
 #pragma unroll
-  for (int t = 0; t < CPW; ++t) acc[t] = s_zero<T>();
+  for (int c = 0; c < NC; ++c) acc[c] = s_zero<T>();
   double nrm = 0.0;
-  const int64_t nchunks = (n + ROWS - 1) / ROWS;
-  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const int64_t r0 = ch * ROWS + lane;
-    T vreg[CPW][RPL];
-    T wv[RPL];
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const T* vp = V + r;
+    T wr = w[r];
+    if (UPD) {
+      T s = s_zero<T>();
 #pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int64_t r = r0 + 32 * i;
-      wv[i] = (r < n) ? w[r] : s_zero<T>();
+      for (int c = 0; c < NC; ++c)
+        if (c < nct) s = s_fma(ldg(vp + int64_t(c) * ldv), cin[c], s);
+      wr = s_sub(wr, s);
+      w[r] = wr;
     }
+    if (NRM) nrm += s_abs2(wr);
+    if (PROJ) {
+      // with UPD these re-reads of the row's basis values hit L1 (just loaded
+      // by this thread); keeping them in registers would halve the occupancy
 #pragma unroll
-    for (int t = 0; t < CPW; ++t) {
-      const int c = warp + CGS_WARPS * t;
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
-        const int64_t r = r0 + 32 * i;
-        vreg[t][i] = (c < ncols && r < n) ? ldg(V + int64_t(c) * ldv + r) : s_zero<T>();
-      }
-    }
-    if (MODE != 0) {
-      // phase 1: w' = w - V coef_in (warp partials over own columns, then smem)
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
-        T p = s_zero<T>();
-#pragma unroll
-        for (int t = 0; t < CPW; ++t) {
-          const int c = warp + CGS_WARPS * t;
-          if (c < ncols) p = s_fma(vreg[t][i], cin[c], p);
-        }
-        red[warp][lane + 32 * i] = p;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int i = 0; i < RPL; ++i) {
-        T s = s_zero<T>();
-#pragma unroll
-        for (int q = 0; q < CGS_WARPS; ++q) s = s_add(s, red[q][lane + 32 * i]);
-        wv[i] = s_sub(wv[i], s);
-        const int64_t r = r0 + 32 * i;
-        if (warp == 0 && r < n) w[r] = wv[i];
-        if (MODE == 2 && warp == 0) nrm += s_abs2(wv[i]);
-      }
-      __syncthreads();
-    }
-    if (MODE != 2) {
-#pragma unroll
-      for (int t = 0; t < CPW; ++t)
-#pragma unroll
-        for (int i = 0; i < RPL; ++i) acc[t] = s_cfma(vreg[t][i], wv[i], acc[t]);
+      for (int c = 0; c < NC; ++c)
+        if (c < nct) acc[c] = s_cfma(ldg(vp + int64_t(c) * ldv), wr, acc[c]);
     }
   }
-  // publish per-block partials
-  if (MODE != 2) {
+  // block partials
+  if (PROJ) {
 #pragma unroll
-    for (int t = 0; t < CPW; ++t) {
-      const int c = warp + CGS_WARPS * t;
-      double* a = reinterpret_cast<double*>(&acc[t]);
+    for (int c = 0; c < NC; ++c) {
+      if (c < nct) {
+        const double* a = reinterpret_cast<const double*>(&acc[c]);
 #pragma unroll
-      for (int d = 0; d < ND; ++d) {
-        const double s = warp_sum(a[d]);
-        if (lane == 0 && c < ncols) partials[int64_t(blockIdx.x) * ncols * ND + c * ND + d] = s;
+        for (int d = 0; d < ND; ++d) {
+          const double s = warp_sum(a[d]);
+          if (lane == 0) red[warp][c * ND + d] = s;
+        }
       }
     }
-  } else {
+    __syncthreads();
+    const int nw = blockDim.x >> 5;
+    for (int i = threadIdx.x; i < nct * ND; i += blockDim.x) {
+      double s = 0.0;
+      for (int q = 0; q < nw; ++q) s += red[q][i];
+      partials[int64_t(blockIdx.x) * nct * ND + i] = s;
+    }
+  }
+  if (NRM) {
+    __shared__ double smn[32];
     const double s = block_sum(nrm, smn);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
   }
   if (last_block(counter)) {
-    if (MODE != 2) {
-      reduce_partials(partials, gridDim.x, ncols * ND, ncols * ND, [&](int i, double s) {
-        double* co = reinterpret_cast<double*>(coef_out);
-        co[i] = s;
-        if (MODE == 1) {
-          const double* ci = reinterpret_cast<const double*>(coef_in);
-          reinterpret_cast<double*>(Hcol)[i] = ci[i] + s;
+    if (PROJ) {
+      reduce_partials(partials, gridDim.x, nct * ND, nct * ND, [&](int i, double s) {
+        if (raw) {
+          raw[i] = s;
+          return;
         }
+        reinterpret_cast<double*>(coef_out)[i] = s;
+        if (Hcol) reinterpret_cast<double*>(Hcol)[i] = reinterpret_cast<const double*>(coef_in)[i] + s;
       });
-    } else {
+    }
+    if (NRM) {
       reduce_partials(partials, gridDim.x, 1, 1, [&](int, double s) {
+        if (raw) {
+          raw[0] = s;
+          return;
+        }
         const double nr = sqrt(s);
         double* hs = reinterpret_cast<double*>(Hsub);
         hs[0] = nr;
@@ -443,7 +483,7 @@ __global__ void __launch_bounds__(256) lanczos_kernel(int64_t n, const T* __rest
                                                       T* __restrict__ w, T* __restrict__ Hdiag,
                                                       T* __restrict__ Hsub, T* __restrict__ Hsup,
                                                       double* __restrict__ inv, double* partials,
-                                                      unsigned* counter) {
+                                                      unsigned* counter, double* raw) {
   constexpr int ND = n_doubles<T>();
   __shared__ double sm[32];
   double s0 = 0.0, s1 = 0.0;
@@ -475,10 +515,17 @@ __global__ void __launch_bounds__(256) lanczos_kernel(int64_t n, const T* __rest
   if (last_block(counter)) {
     if (PHASE == 1) {
       reduce_partials(partials, gridDim.x, 2, ND, [&](int i, double s) {
-        reinterpret_cast<double*>(Hdiag)[i] = s;
+        if (raw)
+          raw[i] = s;
+        else
+          reinterpret_cast<double*>(Hdiag)[i] = s;
       });
     } else {
       reduce_partials(partials, gridDim.x, 2, 1, [&](int, double s) {
+        if (raw) {
+          raw[0] = s;
+          return;
+        }
         const double b = sqrt(s);
         reinterpret_cast<double*>(Hsub)[0] = b;
         reinterpret_cast<double*>(Hsup)[0] = b;
@@ -613,11 +660,19 @@ void launch_norm(ppf_dtype dt, int64_t n, const void* v, double* out, RedScratch
   const int blocks = blocks_for(n, 256, grid);
   if (dt == PPF_R64)
     norm_kernel<double><<<blocks, 256, 0, st>>>(n, static_cast<const double*>(v), out,
-                                                rs.partials, rs.counter);
+                                                rs.partials, rs.counter, rs.raw);
   else
     norm_kernel<cplx><<<blocks, 256, 0, st>>>(n, static_cast<const cplx*>(v), out, rs.partials,
-                                              rs.counter);
+                                              rs.counter, rs.raw);
   post_launch("norm_kernel");
+}
+
+void launch_finalize(int op, int nv, int nd, const double* raw, void* o0, void* o1, void* o2,
+                     const void* ci, cudaStream_t st) {
+  finalize_kernel<<<1, 256, 0, st>>>(op, nv, nd, raw, static_cast<double*>(o0),
+                                     static_cast<double*>(o1), static_cast<double*>(o2),
+                                     static_cast<const double*>(ci));
+  post_launch("finalize_kernel");
 }
 
 void launch_diffnorm(ppf_dtype dt, int64_t n, const void* a, const void* b, double* out,
@@ -626,11 +681,11 @@ void launch_diffnorm(ppf_dtype dt, int64_t n, const void* a, const void* b, doub
   if (dt == PPF_R64)
     diffnorm_kernel<double><<<blocks, 256, 0, st>>>(n, static_cast<const double*>(a),
                                                     static_cast<const double*>(b), out,
-                                                    rs.partials, rs.counter);
+                                                    rs.partials, rs.counter, rs.raw);
   else
     diffnorm_kernel<cplx><<<blocks, 256, 0, st>>>(n, static_cast<const cplx*>(a),
                                                   static_cast<const cplx*>(b), out, rs.partials,
-                                                  rs.counter);
+                                                  rs.counter, rs.raw);
   post_launch("diffnorm_kernel");
 }
 
@@ -649,65 +704,88 @@ void launch_combine(ppf_dtype dt, int64_t n, const void* V, int64_t ldv, int nco
   post_launch("combine_kernel");
 }
 
-template <typename T, int CPW, int RPL>
-static void cgs_t(int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
-                  const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
-                  RedScratch& rs, int grid, cudaStream_t st) {
-  const int64_t nchunks = (n + 32 * RPL - 1) / (32 * RPL);
-  int blocks = int(nchunks < grid ? nchunks : grid);
+// raw (multi-rank): where this launch's rank-local sums go (tile offset applied)
+template <typename T, int NC, int FL>
+static void cgs_go(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* ci, T* co, T* hc,
+                   T* hs, double* inv, RedScratch& rs, double* raw, int grid, cudaStream_t st) {
+  int64_t b = (n + 255) / 256;
+  int blocks = int(b < grid ? b : grid);
   if (blocks < 1) blocks = 1;
-  auto Vt = static_cast<const T*>(V);
-  auto wt = static_cast<T*>(w);
-  auto ci = static_cast<const T*>(coef_in);
-  auto co = static_cast<T*>(coef_out);
-  auto hc = static_cast<T*>(Hcol);
-  auto hs = static_cast<T*>(Hsub);
-  switch (mode) {
-    case 0:
-      cgs_kernel<T, CPW, RPL, 0><<<blocks, 256, 0, st>>>(n, Vt, ldv, ncols, wt, ci, co, hc, hs, inv,
-                                                         rs.partials, rs.counter);
-      break;
-    case 1:
-      cgs_kernel<T, CPW, RPL, 1><<<blocks, 256, 0, st>>>(n, Vt, ldv, ncols, wt, ci, co, hc, hs, inv,
-                                                         rs.partials, rs.counter);
-      break;
-    default:
-      cgs_kernel<T, CPW, RPL, 2><<<blocks, 256, 0, st>>>(n, Vt, ldv, ncols, wt, ci, co, hc, hs, inv,
-                                                         rs.partials, rs.counter);
-  }
+  cgs_kernel<T, NC, FL><<<blocks, 256, 0, st>>>(n, V, ldv, nct, w, ci, co, hc, hs, inv,
+                                                rs.partials, rs.counter, raw);
   post_launch("cgs_kernel");
 }
 
-template <typename T>
-static void cgs_dispatch(int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
-                         const void* ci, void* co, void* hc, void* hs, double* inv, RedScratch& rs,
-                         int grid, cudaStream_t st) {
-  const int cpw = (ncols + CGS_WARPS - 1) / CGS_WARPS;
-  if (cpw <= 1)
-    cgs_t<T, 1, 4>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
-  else if (cpw <= 2)
-    cgs_t<T, 2, 4>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
-  else if (cpw <= 4)
-    cgs_t<T, 4, 2>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
-  else if (cpw <= 8)
-    cgs_t<T, 8, 1>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
-  else if (cpw <= 16)
-    cgs_t<T, 16, 1>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
-  else if (cpw <= 32)
-    cgs_t<T, 32, 1>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+template <typename T, int FL>
+static void cgs_nc(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* ci, T* co, T* hc,
+                   T* hs, double* inv, RedScratch& rs, int grid, cudaStream_t st, int c0 = 0) {
+  constexpr int ND = n_doubles<T>();
+  double* raw = rs.raw ? rs.raw + ((FL & F_PROJ) ? c0 * ND : 0) : nullptr;
+  if (nct <= 4)
+    cgs_go<T, 4, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
+  else if (nct <= 8)
+    cgs_go<T, 8, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
+  else if (nct <= 16)
+    cgs_go<T, 16, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
   else
-    fail(PPF_EINVAL, "too many basis vectors for the CGS kernel (max 256)");
+    cgs_go<T, 32, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
 }
 
-void launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
-                const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
-                RedScratch& rs, int grid, cudaStream_t st) {
+template <typename T>
+static int cgs_dispatch(int mode, int64_t n, const void* Vv, int64_t ldv, int ncols, void* wv,
+                        const void* civ, void* cov, void* hcv, void* hsv, double* inv,
+                        RedScratch& rs, int grid, cudaStream_t st) {
+  constexpr int TILE = 32;
+  auto V = static_cast<const T*>(Vv);
+  auto w = static_cast<T*>(wv);
+  auto ci = static_cast<const T*>(civ);
+  auto co = static_cast<T*>(cov);
+  auto hc = static_cast<T*>(hcv);
+  auto hs = static_cast<T*>(hsv);
+  int launches = 0;
+  if (ncols <= TILE) {
+    if (mode == 0)
+      cgs_nc<T, F_PROJ>(n, V, ldv, ncols, w, nullptr, co, nullptr, nullptr, nullptr, rs, grid, st);
+    else if (mode == 1)
+      cgs_nc<T, F_UPD | F_PROJ>(n, V, ldv, ncols, w, ci, co, hc, nullptr, nullptr, rs, grid, st);
+    else
+      cgs_nc<T, F_UPD | F_NRM>(n, V, ldv, ncols, w, ci, nullptr, nullptr, hs, inv, rs, grid, st);
+    return 1;
+  }
+  // tiled: updates over all tiles first, then projections / norm
+  if (mode != 0) {
+    for (int c0 = 0; c0 < ncols; c0 += TILE) {
+      const int nct = ncols - c0 < TILE ? ncols - c0 : TILE;
+      const bool last = c0 + TILE >= ncols;
+      if (mode == 2 && last)
+        cgs_nc<T, F_UPD | F_NRM>(n, V + int64_t(c0) * ldv, ldv, nct, w, ci + c0, nullptr, nullptr,
+                                 hs, inv, rs, grid, st);
+      else
+        cgs_nc<T, F_UPD>(n, V + int64_t(c0) * ldv, ldv, nct, w, ci + c0, nullptr, nullptr, nullptr,
+                         nullptr, rs, grid, st);
+      ++launches;
+    }
+  }
+  if (mode != 2) {
+    for (int c0 = 0; c0 < ncols; c0 += TILE) {
+      const int nct = ncols - c0 < TILE ? ncols - c0 : TILE;
+      cgs_nc<T, F_PROJ>(n, V + int64_t(c0) * ldv, ldv, nct, w, mode == 1 ? ci + c0 : nullptr,
+                        co + c0, mode == 1 ? hc + c0 : nullptr, nullptr, nullptr, rs, grid, st,
+                        c0);
+      ++launches;
+    }
+  }
+  return launches;
+}
+
+int launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
+               const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
+               RedScratch& rs, int grid, cudaStream_t st) {
   if (dt == PPF_R64)
-    cgs_dispatch<double>(mode, n, V, ldv, ncols, w, coef_in, coef_out, Hcol, Hsub, inv, rs, grid,
-                         st);
-  else
-    cgs_dispatch<cplx>(mode, n, V, ldv, ncols, w, coef_in, coef_out, Hcol, Hsub, inv, rs, grid,
-                       st);
+    return cgs_dispatch<double>(mode, n, V, ldv, ncols, w, coef_in, coef_out, Hcol, Hsub, inv, rs,
+                                grid, st);
+  return cgs_dispatch<cplx>(mode, n, V, ldv, ncols, w, coef_in, coef_out, Hcol, Hsub, inv, rs,
+                            grid, st);
 }
 
 void launch_lanczos(ppf_dtype dt, int phase, int64_t n, const void* v, const void* vprev,
@@ -719,12 +797,12 @@ void launch_lanczos(ppf_dtype dt, int phase, int64_t n, const void* v, const voi
     lanczos_kernel<T, 1><<<blocks, 256, 0, st>>>(                                                \
         n, static_cast<const T*>(v), static_cast<const T*>(vprev), beta_prev, static_cast<T*>(w), \
         static_cast<T*>(Hdiag), static_cast<T*>(Hsub), static_cast<T*>(Hsup), inv, rs.partials,  \
-        rs.counter);                                                                             \
+        rs.counter, rs.raw);                                                                     \
   else                                                                                           \
     lanczos_kernel<T, 2><<<blocks, 256, 0, st>>>(                                                \
         n, static_cast<const T*>(v), static_cast<const T*>(vprev), beta_prev, static_cast<T*>(w), \
         static_cast<T*>(Hdiag), static_cast<T*>(Hsub), static_cast<T*>(Hsup), inv, rs.partials,  \
-        rs.counter);
+        rs.counter, rs.raw);
   if (dt == PPF_R64) {
     PPF_LZ(double)
   } else {

@@ -229,7 +229,13 @@ struct RedScratch {   // reduction scratch (device)
   double* partials;   // [max_blocks * max_vals * 2]
   unsigned* counter;  // zero-initialised, self-resetting
   int max_blocks;
+  // multi-rank: when non-null the last block stores the rank-local sums here
+  // (no finalisation); the caller allreduces them and calls launch_finalize
+  double* raw = nullptr;
 };
+enum { FIN_NORM = 0, FIN_SQRT = 1, FIN_COEF = 2, FIN_SUBNORM = 3, FIN_LZ1 = 4, FIN_LZ2 = 5 };
+void launch_finalize(int op, int nv, int nd, const double* raw, void* o0, void* o1, void* o2,
+                     const void* ci, cudaStream_t st);
 // dst = alpha * src (alpha read from device double *alpha_dev if non-null, else alpha_host)
 void launch_scale(ppf_dtype dt, int64_t n, const void* src, void* dst, const double* alpha_dev,
                   double alpha_host, cudaStream_t st);
@@ -240,7 +246,7 @@ void launch_norm(ppf_dtype dt, int64_t n, const void* v, double* nrm_out, RedScr
 //   mode 0: coef_out[0:ncols] = V^H w
 //   mode 1: w -= V coef_in ; coef_out = V^H w ; H[:,j] = coef_in + coef_out
 //   mode 2: w -= V coef_in ; H[j+1,j] = ||w||, inv[0] = 1/||w||
-void launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
+int launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
                 const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
                 RedScratch& rs, int grid, cudaStream_t st);
 // Lanczos: phase 1: w -= beta_prev * vprev (if vprev); alpha = v^H w -> Hdiag (real part kept)

@@ -29,7 +29,7 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 struct WsLayout {
   int64_t ldv;       // leading dimension of V and vector length (padded)
   int ldh;           // leading dimension of H
-  size_t V, U, Y, T0, T1, T2, H, hbuf, gbuf, ybuf, scal, partials, counter, total;
+  size_t V, U, Y, T0, T1, T2, H, hbuf, gbuf, ybuf, scal, partials, counter, raw, total;
   int max_blocks;
   int max_vals;
 };
@@ -39,7 +39,7 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms) {
   WsLayout L{};
   L.ldv = (n + 63) & ~int64_t(63);
   L.ldh = m_max + 2;
-  L.max_blocks = std::max(4 * num_sms, 256);
+  L.max_blocks = std::max(8 * num_sms, 256);
   L.max_vals = (m_max + 2) * 2;
   size_t o = 0;
   const size_t vec = al256(size_t(L.ldv) * sc);
@@ -69,12 +69,35 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms) {
   o += al256(size_t(L.max_blocks) * L.max_vals * 8);
   L.counter = o;
   o += 256;
+  L.raw = o;
+  o += al256(size_t(L.max_vals) * 8);
   L.total = o;
   return L;
 }
 
 // scalar slots (doubles) in the scal area
 enum { S_BETA0 = 0, S_INV0 = 1, S_INV = 2, S_ERR = 4, S_REF = 5 };
+
+// Halo exchange of the packed boundary entries: one grouped
+// NCCL send/recv per peer with a non-empty list, on the compute stream.
+void halo_sendrecv(ppf_ctx* ctx, ppf_mat* A, cudaStream_t st) {
+  auto comm = static_cast<ncclComm_t>(ctx->nccl_comm);
+  if (!comm) fail(PPF_ESTATE, "nranks > 1 needs a context with an NCCL communicator");
+  const size_t sc = A->dtype == PPF_R64 ? 8 : 16;
+  const int nd = int(sc / 8);
+  if (ncclGroupStart() != ncclSuccess) fail(PPF_ENCCL, "ncclGroupStart");
+  for (int p = 0; p < A->nranks; ++p) {
+    if (A->send_count[p])
+      if (ncclSend(static_cast<char*>(A->d_send) + A->send_off[p] * sc, A->send_count[p] * nd,
+                   ncclDouble, p, comm, st) != ncclSuccess)
+        fail(PPF_ENCCL, "ncclSend");
+    if (A->recv_count[p])
+      if (ncclRecv(static_cast<char*>(A->d_recv) + A->recv_off[p] * sc, A->recv_count[p] * nd,
+                   ncclDouble, p, comm, st) != ncclSuccess)
+        fail(PPF_ENCCL, "ncclRecv");
+  }
+  if (ncclGroupEnd() != ncclSuccess) fail(PPF_ENCCL, "ncclGroupEnd");
+}
 
 struct Runner {
   ppf_ctx* ctx;
@@ -89,6 +112,17 @@ struct Runner {
   RedScratch rs;
   int grid_vec, grid_cgs;
   long long launches = 0;
+  bool dist = false;  // row-slab sharded over nranks > 1 (NCCL)
+
+  // multi-rank: allreduce the rank-local sums a reduction kernel left in rs.raw,
+  // then finalise them (sqrt, H entries, 1/norm) on the device; no-op on 1 rank.
+  void reduce_fin(int op, int nv, void* o0, void* o1, void* o2, const void* ci) {
+    if (!dist) return;
+    if (ncclAllReduce(rs.raw, rs.raw, size_t(nv), ncclDouble, ncclSum,
+                      static_cast<ncclComm_t>(ctx->nccl_comm), st) != ncclSuccess)
+      fail(PPF_ENCCL, "ncclAllReduce");
+    timed(2, 0.0, [&] { launch_finalize(op, nv, int(sc / 8), rs.raw, o0, o1, o2, ci, st); });
+  }
 
   Runner(ppf_ctx* c, ppf_mat* a, const ppf_poly* qq, int m_max, void* work, size_t bytes)
       : ctx(c), A(a), q(qq), dt(a->dtype), n(a->n_local) {
@@ -101,8 +135,13 @@ struct Runner {
     rs.partials = reinterpret_cast<double*>(w + L.partials);
     rs.counter = reinterpret_cast<unsigned*>(w + L.counter);
     rs.max_blocks = L.max_blocks;
+    dist = A->nranks > 1;
+    if (dist) {
+      if (!c->nccl_comm) fail(PPF_ESTATE, "nranks > 1 needs a context with an NCCL communicator");
+      rs.raw = reinterpret_cast<double*>(w + L.raw);
+    }
     grid_vec = std::min(L.max_blocks, 4 * c->num_sms);
-    grid_cgs = std::min(L.max_blocks, 2 * c->num_sms);
+    grid_cgs = std::min(L.max_blocks, 4 * c->num_sms);
     PPF_CUDA(cudaMemsetAsync(w + L.counter, 0, 256, st));
     PPF_CUDA(cudaMemsetAsync(w + L.H, 0, size_t(L.ldh) * (m_max + 1) * sc, st));
   }
@@ -112,8 +151,42 @@ struct Runner {
   void* Hp(int i, int j) { return w + L.H + (size_t(i) + size_t(j) * L.ldh) * sc; }
   double* scal(int i) { return reinterpret_cast<double*>(w + L.scal) + i; }
 
+  // ----- recording of a step's SpMV sequence (for look-ahead enqueueing) -----
+  struct Call {
+    const void* x;
+    void* out;
+    Epi e;
+    bool scale;   // out = c * x (degree-0 polynomial) instead of an SpMV
+    double c;
+  };
+  std::vector<Call>* rec = nullptr;
+
+  void play(const Call& c) {
+    if (c.scale)
+      timed(2, 2.0 * n * sc, [&] { launch_scale(dt, n, c.x, c.out, nullptr, c.c, st); });
+    else
+      spmv_now(c.x, c.out, c.e);
+  }
+
+  // the SpMV / scale sequence of step j (w = Op v_j), not launched
+  std::vector<Call> record_step(int j) {
+    std::vector<Call> v;
+    rec = &v;
+    op_apply(j);
+    rec = nullptr;
+    return v;
+  }
+
   // ----- SpMV with halo exchange (nranks > 1) -----
   void spmv(const void* x, void* out, const Epi& e) {
+    if (rec) {
+      rec->push_back({x, out, e, false, 0.0});
+      return;
+    }
+    spmv_now(x, out, e);
+  }
+
+  void spmv_now(const void* x, void* out, const Epi& e) {
     if (A->nranks > 1) exchange(x);
     // algorithmic bytes: values + column indices once, x gathered once, out
     // written once, z and u streamed once
@@ -126,20 +199,7 @@ struct Runner {
 
   void exchange(const void* x) {
     timed(2, 0.0, [&] { launch_halo_pack(A, x, st); });
-    auto comm = static_cast<ncclComm_t>(ctx->nccl_comm);
-    const int nd = int(sc / 8);
-    if (ncclGroupStart() != ncclSuccess) fail(PPF_ENCCL, "ncclGroupStart");
-    for (int p = 0; p < A->nranks; ++p) {
-      if (A->send_count[p])
-        if (ncclSend(static_cast<char*>(A->d_send) + A->send_off[p] * sc, A->send_count[p] * nd,
-                     ncclDouble, p, comm, st) != ncclSuccess)
-          fail(PPF_ENCCL, "ncclSend");
-      if (A->recv_count[p])
-        if (ncclRecv(static_cast<char*>(A->d_recv) + A->recv_off[p] * sc, A->recv_count[p] * nd,
-                     ncclDouble, p, comm, st) != ncclSuccess)
-          fail(PPF_ENCCL, "ncclRecv");
-    }
-    if (ncclGroupEnd() != ncclSuccess) fail(PPF_ENCCL, "ncclGroupEnd");
+    halo_sendrecv(ctx, A, st);
   }
 
   static Epi epi(zc sax, zc sx, zc sz, const void* z, zc su, const void* u) {
@@ -162,6 +222,10 @@ struct Runner {
     // a SpMV-free scaled copy: reuse the SpMV epilogue would need A; use scale
     if (c.imag() != 0.0 && dt == PPF_R64) fail(PPF_EINVAL, "complex coefficient on a real operator");
     if (c.imag() == 0.0) {
+      if (rec) {
+        rec->push_back({in, out, Epi{}, true, c.real()});
+        return;
+      }
       timed(2, 2.0 * n * sc, [&] { launch_scale(dt, n, in, out, nullptr, c.real(), st); });
     } else {
       fail(PPF_EINVAL, "degree-0 complex Newton polynomial not supported");
@@ -245,25 +309,32 @@ struct Runner {
         launch_lanczos(dt, 1, n, V(j), j > 0 ? V(j - 1) : nullptr, bprev, V(j + 1), Hp(j, j),
                        nullptr, nullptr, nullptr, rs, grid_vec, st);
       });
+      reduce_fin(FIN_LZ1, int(sc / 8), Hp(j, j), nullptr, nullptr, nullptr);
       timed(1, vb * 3, [&] {
         launch_lanczos(dt, 2, n, V(j), nullptr, nullptr, V(j + 1), Hp(j, j), Hp(j + 1, j),
                        Hp(j, j + 1), scal(S_INV), rs, grid_vec, st);
       });
+      reduce_fin(FIN_LZ2, 1, Hp(j + 1, j), Hp(j, j + 1), scal(S_INV), nullptr);
     } else {
       void* hb = vec(L.hbuf);
       void* gb = vec(L.gbuf);
+      // launch_cgs returns the number of kernels it issued (column tiles of 32)
+      const int nv = (j + 1) * int(sc / 8);
       timed(1, vb * (j + 2), [&] {
-        launch_cgs(dt, 0, n, V(0), L.ldv, j + 1, V(j + 1), nullptr, hb, nullptr, nullptr, nullptr,
-                   rs, grid_cgs, st);
+        launches += launch_cgs(dt, 0, n, V(0), L.ldv, j + 1, V(j + 1), nullptr, hb, nullptr,
+                               nullptr, nullptr, rs, grid_cgs, st) - 1;
       });
+      reduce_fin(FIN_COEF, nv, hb, nullptr, nullptr, nullptr);
       timed(1, vb * (j + 3), [&] {
-        launch_cgs(dt, 1, n, V(0), L.ldv, j + 1, V(j + 1), hb, gb, Hp(0, j), nullptr, nullptr, rs,
-                   grid_cgs, st);
+        launches += launch_cgs(dt, 1, n, V(0), L.ldv, j + 1, V(j + 1), hb, gb, Hp(0, j), nullptr,
+                               nullptr, rs, grid_cgs, st) - 1;
       });
+      reduce_fin(FIN_COEF, nv, gb, Hp(0, j), nullptr, hb);
       timed(1, vb * (j + 3), [&] {
-        launch_cgs(dt, 2, n, V(0), L.ldv, j + 1, V(j + 1), gb, nullptr, nullptr, Hp(j + 1, j),
-                   scal(S_INV), rs, grid_cgs, st);
+        launches += launch_cgs(dt, 2, n, V(0), L.ldv, j + 1, V(j + 1), gb, nullptr, nullptr,
+                               Hp(j + 1, j), scal(S_INV), rs, grid_cgs, st) - 1;
       });
+      reduce_fin(FIN_SUBNORM, 1, Hp(j + 1, j), nullptr, scal(S_INV), nullptr);
     }
     timed(1, vb * 2, [&] { launch_scale(dt, n, V(j + 1), V(j + 1), scal(S_INV), 0.0, st); });
   }
@@ -272,6 +343,7 @@ struct Runner {
   void normalise_start() {
     const double vb = double(n) * double(sc);
     timed(2, vb, [&] { launch_norm(dt, n, V(0), scal(S_BETA0), rs, grid_vec, st); });
+    reduce_fin(FIN_NORM, 1, scal(S_BETA0), nullptr, nullptr, nullptr);
     timed(2, 2 * vb, [&] { launch_scale(dt, n, V(0), V(0), scal(S_INV0), 0.0, st); });
   }
 
@@ -323,12 +395,25 @@ struct Runner {
 
   // copy H[0:rows, 0:cols] (and beta0) to pinned host; wait.
   void fetch_H(int rows, int cols, std::vector<zc>& Hh, double& beta0) {
+    fetch_H_async(cols);
+    fetch_H_wait(rows, cols, Hh, beta0);
+  }
+
+  // enqueue the D2H copy of H[:, 0:cols] and beta0, then an event
+  void fetch_H_async(int cols) {
     char* hp = static_cast<char*>(ctx->h_pinned);
     const size_t bytes = size_t(L.ldh) * cols * sc;
     if (bytes + 64 > ctx->h_pinned_bytes - 8192) fail(PPF_EINVAL, "m_max too large for staging buffer");
     PPF_CUDA(cudaMemcpyAsync(hp, w + L.H, bytes, cudaMemcpyDeviceToHost, st));
     PPF_CUDA(cudaMemcpyAsync(hp + bytes, scal(S_BETA0), 8, cudaMemcpyDeviceToHost, st));
-    PPF_CUDA(cudaStreamSynchronize(st));
+    PPF_CUDA(cudaEventRecord(ctx->ev, st));
+  }
+
+  // wait for fetch_H_async (work enqueued after it keeps running)
+  void fetch_H_wait(int rows, int cols, std::vector<zc>& Hh, double& beta0) {
+    char* hp = static_cast<char*>(ctx->h_pinned);
+    const size_t bytes = size_t(L.ldh) * cols * sc;
+    PPF_CUDA(cudaEventSynchronize(ctx->ev));
     const double* h = reinterpret_cast<const double*>(hp);
     const int nd = int(sc / 8);
     Hh.assign(size_t(rows) * cols, zc(0.0, 0.0));
@@ -396,7 +481,6 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   check_opts(o);
   PPF_REQUIRE(q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
               "a Newton (complex) polynomial needs a complex operator");
-  PPF_REQUIRE(A->nranks == 1, "multi-rank runs are not enabled in this build");
   const bool lanczos = o->krylov == PPF_LANCZOS;
   const int m_max = o->m_max;
   const int k = std::max(1, o->check_every);
@@ -429,14 +513,34 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   int m = 0;
   int term = PPF_MAX_ITER;
   double est = NAN, err = NAN;
+  // Look-ahead: at a checkpoint the host waits for H while the first LOOKAHEAD
+  // mat-vecs of the next step (which only read v_{j+1}) already run, so the
+  // device does not idle during the D2H copy, f(H_m) and the relaunch.  If the
+  // run stops there, that work (<= LOOKAHEAD SpMVs) is discarded.
+  const int LOOKAHEAD = (o->stop == PPF_STOP_EST) ? 2 : 0;
+  std::vector<Runner::Call> calls = R.record_step(0);
+  size_t played = 0;
   for (int j = 0; j < m_max; ++j) {
-    R.op_apply(j);
+    for (; played < calls.size(); ++played) R.play(calls[played]);
     R.orthogonalise(j, lanczos);
     m = j + 1;
     mvms += 2 * q->deg + 1;
     const bool check = (o->stop != PPF_STOP_FIXED_M) && (m % k == 0 || m == m_max);
-    if (!check) continue;
-    R.fetch_H(m + 1, m, Hh, beta0);
+    const bool more = j + 1 < m_max;
+    if (!check) {
+      if (more) {
+        calls = R.record_step(j + 1);
+        played = 0;
+      }
+      continue;
+    }
+    R.fetch_H_async(m);
+    if (more) {
+      calls = R.record_step(j + 1);
+      played = 0;
+      for (; played < calls.size() && played < size_t(LOOKAHEAD); ++played) R.play(calls[played]);
+    }
+    R.fetch_H_wait(m + 1, m, Hh, beta0);
     const double hsub = std::abs(Hh[size_t(m) + size_t(m - 1) * (m + 1)]);
     // earlier breakdown inside the stride?
     int mb = m;
@@ -469,6 +573,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
       R.timed(2, 2.0 * vb, [&] {
         launch_diffnorm(R.dt, n, R.vec(R.L.T0), o->x_ref, R.scal(S_ERR), R.rs, R.grid_vec, R.st);
       });
+      R.reduce_fin(FIN_SQRT, 2, R.scal(S_ERR), nullptr, nullptr, nullptr);
       double e2[2];
       PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
       PPF_CUDA(cudaStreamSynchronize(R.st));
@@ -651,7 +756,6 @@ ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int
   PPF_REQUIRE(ctx && A && start && out, "NULL argument");
   PPF_REQUIRE(deg >= 0 && deg < 255, "deg out of range");
   PPF_REQUIRE(A->dtype == PPF_C128, "Ritz-Newton polynomials need a complex operator");
-  PPF_REQUIRE(A->nranks == 1, "multi-rank runs are not enabled in this build");
   const int d = deg + 1;
   Runner R(ctx, A, nullptr, d, work, bytes);
   PPF_CUDA(cudaMemcpyAsync(R.V(0), start, size_t(R.n) * R.sc, cudaMemcpyDeviceToDevice, R.st));
@@ -690,9 +794,17 @@ extern "C" ppf_status ppf_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y)
     PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
     ppf::Epi e{};
     e.s_ax[0] = 1.0;
-    if (A->nranks > 1) fail(PPF_EINVAL, "multi-rank runs are not enabled in this build");
+    if (A->nranks > 1) {
+      ppf::launch_halo_pack(A, x, ctx->stream);
+      ppf::halo_sendrecv(ctx, A, ctx->stream);
+      ctx->launches += 1;
+    }
     ppf::launch_spmv(A, x, y, e, ctx->stream);
     ctx->launches += 1;
+    if (A->nranks > 1 && A->halo_rows) {
+      ppf::launch_halo_apply(A, y, e.s_ax, ctx->stream);
+      ctx->launches += 1;
+    }
     return PPF_OK;
   } catch (const ppf::Error& e) {
     ppf::set_last_error(e.msg);
@@ -722,7 +834,6 @@ extern "C" ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q
     PPF_REQUIRE(x != y, "x and y must be distinct");
     PPF_REQUIRE(q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
                 "a Newton (complex) polynomial needs a complex operator");
-    PPF_REQUIRE(A->nranks == 1, "multi-rank runs are not enabled in this build");
     ppf::Runner R(ctx, A, q, 1, work, bytes);
     R.apply_q(x, y);
     if (ctx->profile) {
@@ -737,5 +848,47 @@ extern "C" ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q
   } catch (...) {
     ppf::set_last_error("unknown C++ exception");
     return PPF_EINVAL;
+  }
+}
+
+extern "C" ppf_status ppf_halo_pack(ppf_ctx* ctx, ppf_mat* A, const void* x) {
+  try {
+    PPF_REQUIRE(ctx && A && x, "NULL argument");
+    PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+    ppf::launch_halo_pack(A, x, ctx->stream);
+    ctx->launches += A->send_total ? 1 : 0;
+    return PPF_OK;
+  } catch (const ppf::Error& e) {
+    ppf::set_last_error(e.msg);
+    return e.st;
+  }
+}
+
+extern "C" ppf_status ppf_halo_buffers(ppf_mat* A, void** send, void** recv) {
+  if (!A) {
+    ppf::set_last_error("NULL matrix");
+    return PPF_EINVAL;
+  }
+  if (send) *send = A->d_send;
+  if (recv) *recv = A->d_recv;
+  return PPF_OK;
+}
+
+extern "C" ppf_status ppf_spmv_local(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y) {
+  try {
+    PPF_REQUIRE(ctx && A && x && y, "NULL argument");
+    PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+    ppf::Epi e{};
+    e.s_ax[0] = 1.0;
+    ppf::launch_spmv(A, x, y, e, ctx->stream);
+    ctx->launches += 1;
+    if (A->halo_rows) {
+      ppf::launch_halo_apply(A, y, e.s_ax, ctx->stream);
+      ctx->launches += 1;
+    }
+    return PPF_OK;
+  } catch (const ppf::Error& e) {
+    ppf::set_last_error(e.msg);
+    return e.st;
   }
 }
