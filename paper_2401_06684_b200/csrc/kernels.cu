@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(256, (NC * sizeof(T) <= 128) ? 4 : 2)
   for (int c = 0; c < NC; ++c) acc[c] = s_zero<T>();
   double nrm = 0.0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) {
+  auto row = [&](int64_t r) {
     const T* vp = V + r;
     T wr = w[r];
     if (UPD) {
@@ -418,6 +418,42 @@ __global__ void __launch_bounds__(256, (NC * sizeof(T) <= 128) ? 4 : 2)
       for (int c = 0; c < NC; ++c)
         if (c < nct) acc[c] = s_cfma(ldg(vp + int64_t(c) * ldv), wr, acc[c]);
     }
+  };
+  if constexpr (sizeof(T) == 8) {
+    // fp64: two adjacent rows per thread with 128-bit loads (columns are
+    // 256-B aligned and ldv is even, so (r, r+1) with r even is 16-B aligned)
+    const int64_t npair = n >> 1;
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npair; p += stride) {
+      const int64_t r = 2 * p;
+      const double2* vp = reinterpret_cast<const double2*>(V + r);
+      const int64_t ldv2 = ldv >> 1;
+      double2 wr = *reinterpret_cast<const double2*>(w + r);
+      if (UPD) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c < nct) {
+            const double2 v = __ldg(vp + int64_t(c) * ldv2);
+            s0 = fma(v.x, cin[c], s0);
+            s1 = fma(v.y, cin[c], s1);
+          }
+        wr.x -= s0;
+        wr.y -= s1;
+        *reinterpret_cast<double2*>(w + r) = wr;
+      }
+      if (NRM) nrm += wr.x * wr.x + wr.y * wr.y;
+      if (PROJ) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (c < nct) {
+            const double2 v = __ldg(vp + int64_t(c) * ldv2);
+            acc[c] = fma(v.x, wr.x, fma(v.y, wr.y, acc[c]));
+          }
+      }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) row(n - 1);
+  } else {
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) row(r);
   }
   // block partials
   if (PROJ) {
