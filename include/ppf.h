@@ -131,6 +131,14 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* plan, void* device_buf,
                           size_t bytes, ppf_mat** out);
 ppf_status ppf_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
 void ppf_mat_destroy(ppf_mat* A);
+/* ppf_mat_set_split: warps per SELL slice of the SpMV kernels:
+ *   1, 2, 4 or 8 splits each slice's entry columns over that many warps whose
+ *   partial sums are added in part order in shared memory; 0 restores the
+ *   automatic choice made by ppf_mat_create (enough warp tasks for >= ~8 waves
+ *   of resident warps).  Results differ only by summation order.  CSR: no-op.
+ *   *applied (may be NULL) receives the value now in force.  PPF_EINVAL for
+ *   other values. */
+ppf_status ppf_mat_set_split(ppf_mat* A, int sell_ks, int* applied);
 /* Pieces of the sharded SpMV, for callers that move the halo
  * themselves: ppf_halo_pack gathers this rank's boundary entries of x (device)
  * into the send buffer; ppf_halo_buffers returns the device send / receive

@@ -58,6 +58,7 @@ SIGNATURES = {
     "ppf_plan_destroy": (None, [vp]),
     "ppf_mat_create": (C.c_int, [vp, vp, vp, C.c_size_t, C.POINTER(vp)]),
     "ppf_spmv": (C.c_int, [vp, vp, vp, vp]),
+    "ppf_mat_set_split": (C.c_int, [vp, C.c_int, C.POINTER(C.c_int)]),
     "ppf_mat_destroy": (None, [vp]),
     "ppf_halo_pack": (C.c_int, [vp, vp, vp]),
     "ppf_halo_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),

@@ -157,6 +157,12 @@ class Matrix:
         check(_lib().ppf_spmv(self.ctx.h, self.h, C.c_void_p(x.data_ptr()),
                               C.c_void_p(y.data_ptr())))
 
+    def set_split(self, sell_ks: int = 0) -> int:
+        """ppf_mat_set_split: warps per SELL slice (0 = automatic); returns the value in force."""
+        out = C.c_int()
+        check(_lib().ppf_mat_set_split(self.h, int(sell_ks), C.byref(out)))
+        return out.value
+
     def close(self):
         if self.h:
             _lib().ppf_mat_destroy(self.h)

@@ -22,6 +22,19 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail(PPF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Warps per SELL slice (kernels.cu sell*_kernel).  KS > 1 only pays when the
+// matrix has fewer slices than about two full blocks per SM (then each warp
+// task is too long for the machine to fill) and rows are wide enough to
+// split; every BASELINE config gets KS = 1 (measured).
+int auto_sell_ks(const ppf_mat* m, int num_sms) {
+  if (m->fmt != PPF_FMT_SELL || m->nslices == 0) return 1;
+  const double width = double(m->stored) / (double(m->nslices) * m->C);
+  const double few = 2.0 * num_sms * 8;
+  int ks = 1;
+  while (ks < 8 && double(m->nslices) * ks < few && width / (2 * ks) >= 8.0) ks *= 2;
+  return ks;
+}
+
 }  // namespace ppf
 
 using namespace ppf;
@@ -451,6 +464,7 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     while (g < 32 && g < avg) g *= 2;
     m->csr_group = g;
   }
+  m->sell_ks = auto_sell_ks(m, ctx->num_sms);
   m->halo_rows = int64_t(p->halo.rows.size());
   m->halo_nnz = int64_t(p->halo.col.size());
   m->halo_total = p->recv_off.empty() ? 0 : p->recv_off.back();
@@ -467,6 +481,15 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
 }
 
 void ppf_mat_destroy(ppf_mat* m) { delete m; }
+
+ppf_status ppf_mat_set_split(ppf_mat* A, int ks, int* applied) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(A, "NULL matrix");
+  PPF_REQUIRE(ks == 0 || ks == 1 || ks == 2 || ks == 4 || ks == 8, "sell_ks not in {0,1,2,4,8}");
+  if (A->fmt == PPF_FMT_SELL) A->sell_ks = ks ? ks : auto_sell_ks(A, A->ctx->num_sms);
+  if (applied) *applied = A->fmt == PPF_FMT_SELL ? A->sell_ks : 1;
+  PPF_API_END
+}
 
 // ---------------------------------------------------------------------------
 // Polynomials

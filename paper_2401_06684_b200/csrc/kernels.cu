@@ -44,6 +44,46 @@ __device__ __forceinline__ cplx ldg(const cplx* p) {
   return {v.x, v.y};
 }
 
+// Loads whose issue order is pinned (asm volatile is not reordered against
+// other asm volatile): the SpMV loops issue a whole batch of loads before the
+// first use.  The matrix streams (values, indices) are read once, so they
+// bypass L1 (L1::no_allocate) and leave it to the x gathers.
+__device__ __forceinline__ int ld_stream(const int32_t* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int2 ld_stream(const int2* p) {
+  int2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_stream(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ cplx ld_stream(const cplx* p) {
+  const double2 v = ld_stream(reinterpret_cast<const double2*>(p));
+  return {v.x, v.y};
+}
+// gather of x (cached in L1: stencil neighbours of adjacent rows share lines)
+__device__ __forceinline__ double ld_gather(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ cplx ld_gather(const cplx* p) {
+  double2 r;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return {r.x, r.y};
+}
+
 template <typename T>
 __device__ __forceinline__ T epilogue(const EpiT<T>& e, T ax, const T* __restrict__ x, int64_t row,
                                       bool has_x) {
@@ -55,30 +95,71 @@ __device__ __forceinline__ T epilogue(const EpiT<T>& e, T ax, const T* __restric
 }
 
 // ---------------------------------------------------------------------------
-// SELL-C-sigma SpMV + fused epilogue.  One warp per slice; R rows per lane.
+// SELL-C-sigma SpMV + fused epilogue.  KS warps per slice, one row per lane.
+//
+// KS > 1 splits a slice's entry columns k = 0..w-1 into KS contiguous parts,
+// one per warp of the same block; the parts' partial sums meet in shared
+// memory and the part-0 warp adds them in part order (deterministic) and runs
+// the epilogue.  Every warp load is still one contiguous 32-entry row of the
+// slice (512 B of complex values + 128 B of indices).  KS multiplies the warp
+// tasks for matrices with very few slices; the automatic choice is KS = 1
+// for every BASELINE config (measured on C5: KS = 1/2/4 -> 6.51/6.21/5.69
+// TB/s, the block barrier costs more than the smaller last wave saves).
+//
+// The loop body issues U = 4 entries' index loads, then their value loads and
+// x gathers, then the FMAs.  With __launch_bounds__(256, 3) ptxas keeps the
+// batch in registers (80 for complex); left at 32 registers it interleaves one
+// entry's loads with the previous FMA, and C5's 49-entry complex rows were
+// latency-bound at 5.2 TB/s (ncu: 36% "mem busy", 60 warps/SM active) instead
+// of 6.5 TB/s.
 // ---------------------------------------------------------------------------
-template <typename T, bool PERM>
-__global__ void __launch_bounds__(256) sell1_kernel(int64_t nslices, int64_t n,
+template <typename T, int KS, bool PERM>
+__global__ void __launch_bounds__(256, 3) sell1_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
                                                     const T* __restrict__ val,
                                                     const T* __restrict__ x, T* __restrict__ out,
                                                     EpiT<T> e, bool has_x,
                                                     const int32_t* __restrict__ perm) {
-  const int lane = threadIdx.x & 31;
-  const int64_t slice = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (slice >= nslices) return;
-  const int64_t base = sptr[slice];
-  const int w = int((sptr[slice + 1] - base) >> 5);
-  const int32_t* cp = col + base + lane;
-  const T* vp = val + base + lane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
+  const int part = warp % KS;
+  const bool live = slice < nslices;
   T acc = s_zero<T>();
-#pragma unroll 4
-  for (int k = 0; k < w; ++k) {
-    const int c = __ldg(cp + 32 * k);
-    const T v = ldg(vp + 32 * k);
-    acc = s_fma(v, ldg(x + c), acc);
+  if (live) {
+    const int64_t base = sptr[slice];
+    const int w = int((sptr[slice + 1] - base) >> 5);
+    const int k0 = part * w / KS, k1 = (part + 1) * w / KS;
+    const int32_t* cp = col + base + lane;
+    const T* vp = val + base + lane;
+    // batches of U entries: all U index loads, then the U value loads and the
+    // U gathers of x, then the FMAs -- U independent loads in flight per
+    // lane (left to itself the compiler issues one entry's loads at a time)
+    constexpr int U = 4;
+    int k = k0;
+    for (; k + U <= k1; k += U) {
+      int c[U];
+      T v[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) c[u] = ld_stream(cp + 32 * (k + u));
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_stream(vp + 32 * (k + u));
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = ld_gather(x + c[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = s_fma(v[u], xv[u], acc);
+    }
+    for (; k < k1; ++k) acc = s_fma(ldg(vp + 32 * k), ldg(x + __ldg(cp + 32 * k)), acc);
   }
+  if constexpr (KS > 1) {
+    __shared__ T red[8][32];
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (part != 0) return;
+#pragma unroll
+    for (int p = 1; p < KS; ++p) acc = s_add(acc, red[warp + p][lane]);
+  }
+  if (!live) return;
   const int64_t pos = slice * 32 + lane;
   if (pos < n) {
     const int64_t row = PERM ? int64_t(perm[pos]) : pos;
@@ -86,7 +167,9 @@ __global__ void __launch_bounds__(256) sell1_kernel(int64_t nslices, int64_t n,
   }
 }
 
-// two rows per lane, 128-bit loads of (val, val) and (col, col); C = 64, fp64
+// two rows per lane, 128-bit loads of (val, val) and (col, col); C = 64, fp64;
+// KS warps per slice as in sell1_kernel
+template <int KS>
 __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
@@ -94,21 +177,41 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ out, EpiT<double> e,
                                                     bool has_x) {
-  const int lane = threadIdx.x & 31;
-  const int64_t slice = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (slice >= nslices) return;
-  const int64_t base = sptr[slice];
-  const int w = int((sptr[slice + 1] - base) >> 6);
-  const int2* cp = reinterpret_cast<const int2*>(col + base) + lane;
-  const double2* vp = reinterpret_cast<const double2*>(val + base) + lane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
+  const int part = warp % KS;
+  const bool live = slice < nslices;
   double a0 = 0.0, a1 = 0.0;
+  if (live) {
+    const int64_t base = sptr[slice];
+    const int w = int((sptr[slice + 1] - base) >> 6);
+    const int k0 = part * w / KS, k1 = (part + 1) * w / KS;
+    const int2* cp = reinterpret_cast<const int2*>(col + base) + lane;
+    const double2* vp = reinterpret_cast<const double2*>(val + base) + lane;
+    // (measured: the compiler's own schedule of this loop, at 32 registers
+    // and full occupancy, streams C3/C4 at 97-98% of the measured copy
+    // bandwidth; the forced batching of sell1_kernel drops it to 72%)
 #pragma unroll 4
-  for (int k = 0; k < w; ++k) {
-    const int2 c = __ldg(cp + 32 * k);
-    const double2 v = __ldg(vp + 32 * k);
-    a0 = fma(v.x, __ldg(x + c.x), a0);
-    a1 = fma(v.y, __ldg(x + c.y), a1);
+    for (int k = k0; k < k1; ++k) {
+      const int2 c = __ldg(cp + 32 * k);
+      const double2 v = __ldg(vp + 32 * k);
+      a0 = fma(v.x, __ldg(x + c.x), a0);
+      a1 = fma(v.y, __ldg(x + c.y), a1);
+    }
   }
+  if constexpr (KS > 1) {
+    __shared__ double2 red[8][32];
+    red[warp][lane] = make_double2(a0, a1);
+    __syncthreads();
+    if (part != 0) return;
+#pragma unroll
+    for (int p = 1; p < KS; ++p) {
+      const double2 t = red[warp + p][lane];
+      a0 += t.x;
+      a1 += t.y;
+    }
+  }
+  if (!live) return;
   const int64_t r0 = slice * 64 + 2 * lane;
   if (r0 + 1 < n) {
     double2 r;
@@ -599,24 +702,42 @@ static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStrea
   T* ot = static_cast<T*>(out);
   const T* val = static_cast<const T*>(A->d_val);
   if (A->fmt == PPF_FMT_SELL) {
-    const int64_t warps = A->nslices;
-    const int blocks = int((warps * 32 + 255) / 256);
+    const int KS = A->sell_ks;
+    const int64_t spb = 8 / KS;  // slices per 256-thread block
+    const int blocks = int((A->nslices + spb - 1) / spb);
     if (blocks == 0) return;
+#define PPF_KS(launch) \
+  switch (KS) {        \
+    case 1: launch(1); break; \
+    case 2: launch(2); break; \
+    case 4: launch(4); break; \
+    default: launch(8); break; \
+  }
     if constexpr (sizeof(T) == 8) {
       if (A->C == 64) {
-        sell2_kernel<<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
-                                             reinterpret_cast<const double*>(val), xt, ot, et,
-                                             has_x);
+#define PPF_S2(K)                                                                    \
+  sell2_kernel<K><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+                                          reinterpret_cast<const double*>(val), xt, ot, et, has_x)
+        PPF_KS(PPF_S2)
+#undef PPF_S2
         post_launch("sell2_kernel");
         return;
       }
     }
-    if (A->d_perm)
-      sell1_kernel<T, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
-                                                    val, xt, ot, et, has_x, A->d_perm);
-    else
-      sell1_kernel<T, false><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
-                                                     val, xt, ot, et, has_x, nullptr);
+#define PPF_S1P(K)                                                                             \
+  sell1_kernel<T, K, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+                                                   val, xt, ot, et, has_x, A->d_perm)
+#define PPF_S1(K)                                                                               \
+  sell1_kernel<T, K, false><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+                                                    val, xt, ot, et, has_x, nullptr)
+    if (A->d_perm) {
+      PPF_KS(PPF_S1P)
+    } else {
+      PPF_KS(PPF_S1)
+    }
+#undef PPF_S1P
+#undef PPF_S1
+#undef PPF_KS
     post_launch("sell1_kernel");
   } else {
     const int G = A->csr_group;

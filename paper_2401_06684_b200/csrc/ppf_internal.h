@@ -134,6 +134,7 @@ struct ppf_mat {
   const void* d_val;
   const int32_t* d_perm;    // null unless sigma > 1
   int csr_group;            // lanes per row for the CSR kernel
+  int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks
   // halo (nranks > 1)
   int64_t halo_rows, halo_nnz, halo_total, send_total;
   const int32_t* d_halo_rows;
@@ -221,6 +222,7 @@ struct Epi {          // out = s_ax*(A x) + s_x*x + s_z*z + s_u*u
   const void* u;      // may be null (s_u ignored)
 };
 
+int auto_sell_ks(const ppf_mat* m, int num_sms);
 void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st);
 void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
 void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st);

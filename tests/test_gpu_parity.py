@@ -84,6 +84,49 @@ def test_spmv_parity(ctx, fmt, C_, sig, which):
     assert np.all(np.abs(got - ref) <= 1e-14 * absA + 1e-300)
 
 
+@pytest.mark.parametrize("ks", [1, 2, 4, 8])
+@pytest.mark.parametrize("C_", [32, 64])
+@pytest.mark.parametrize("which", ["ragged", "ragged_c", "wilson", "lap3"])
+def test_spmv_split_parity(ctx, ks, C_, which):
+    """KS warps per SELL slice (ppf_mat_set_split): the parts' partial sums are
+    combined in part order; every row must still match the oracle SpMV, for
+    slices whose width is not a multiple of KS and slices narrower than KS."""
+    if which == "ragged":
+        A = ragged_matrix(3001, 11)
+    elif which == "ragged_c":
+        A = ragged_matrix(1999, 12, complex_=True)
+    elif which == "wilson":
+        A = ops.wilson_dirac(4, -1.0, seed=5)   # 3072 rows, 49 entries each
+    else:
+        A = ops.laplacian(13, 3)
+    if np.iscomplexobj(A.val) and C_ == 64:
+        pytest.skip("C = 64 is the fp64 two-rows-per-lane layout")
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=C_, sigma=1))
+    assert M.set_split(ks) == ks
+    rng = np.random.default_rng(17)
+    x = rng.standard_normal(A.n)
+    if np.iscomplexobj(A.val):
+        x = x + 1j * rng.standard_normal(A.n)
+    xd = dev(x)
+    yd = torch.full_like(xd, float("nan"))
+    M.spmv(xd, yd)
+    ref = A.to_scipy() @ x
+    absA = abs(A.to_scipy()) @ np.abs(x)
+    assert np.all(np.abs(host(yd) - ref) <= 1e-14 * absA + 1e-300)
+    assert M.set_split(0) >= 1
+
+
+def test_auto_split_choice(ctx):
+    """The automatic split: KS = 1 for narrow rows and for matrices with many
+    slices; a few-slice matrix with wide rows is split."""
+    A = ops.wilson_dirac(4, -1.0, seed=5)     # 96 slices of 49 entries
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32, sigma=1))
+    assert M.set_split(0) == 4
+    L = ops.laplacian(13, 3)
+    M2 = pp.Matrix(ctx, pp.Plan.from_csr(L, fmt="sell", C_=64, sigma=1))
+    assert M2.set_split(0) == 1
+
+
 @pytest.mark.parametrize("fmt", ["sell", "csr"])
 @pytest.mark.parametrize("deg", [0, 1, 2, 3, 7, 20])
 def test_chebyshev_chain_parity(ctx, fmt, deg):
