@@ -53,11 +53,6 @@ __device__ __forceinline__ int ld_stream(const int32_t* p) {
   asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
-__device__ __forceinline__ int2 ld_stream(const int2* p) {
-  int2 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
@@ -470,138 +465,266 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t n, const T* __rest
 
 // ---------------------------------------------------------------------------
 // CGS2 sweeps (K5/K6/K7) on a column tile [c0, c0+nct) of V, nct <= NC.
-// One row per thread per iteration (grid-stride), the row's nct basis values
-// held in registers; no block barrier inside the row loop.  Flags:
-//   UPD : w -= V_tile coef_in_tile          (w written back)
+//
+// Persistent, warp-specialised kernel, one CTA per SM.  The rows are cut into
+// chunks of R rows.  A producer warp streams chunk after chunk into a ring of
+// S shared-memory stages with bulk async copies (cp.async.bulk, the 1-D TMA
+// path): one copy per basis column segment plus one for the w segment
+// (R*sizeof(T) contiguous bytes each), issued in parallel by the producer's
+// lanes and completing on the stage's "full" mbarrier (expect_tx).  S is as
+// deep as ~200 KB of shared memory allows, so every SM keeps 130-200 KB of
+// reads in flight whatever nct is.  R consumer threads own one row of the
+// chunk each: they read the row's basis values from shared memory once
+// (conflict-free: column segments are contiguous), keep them in registers for
+// the update and the projection, accumulate their nct projections in
+// registers across chunks, and release the stage on its "empty" mbarrier
+// (one arrival per consumer warp) -- no block-wide barrier in the loop.
+// Flags:
+//   UPD : w -= V_tile coef_in_tile          (w written back to global)
 //   PROJ: coef_out_tile = V_tile^H w        (after UPD if both)
 //   NRM : ||w||^2 -> Hsub = ||w||, inv = 1/||w||
 // With PROJ|UPD the finalisation also writes Hcol = coef_in + coef_out.
+// Block partials, then the last CTA to arrive sums them in CTA order
+// (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int F_UPD = 1, F_PROJ = 2, F_NRM = 4;
+constexpr int CGS_SMEM = 212 * 1024;  // dynamic shared memory per CTA (ring + barriers)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// shared-memory read the compiler may not hoist out of the chunk loop (the
+// nct coefficients would otherwise occupy registers next to the nct
+// accumulators and spill)
+__device__ __forceinline__ double lds_nohoist(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
+__device__ __forceinline__ cplx lds_nohoist(const cplx* p) {
+  const volatile double* q = reinterpret_cast<const volatile double*>(p);
+  return {q[0], q[1]};
+}
+
+// rows per chunk (per RPT block): 16 consumer warps x 16 rows, two lanes per
+// row; complex rows are twice as wide, so 128 rows (8 consumer warps)
+template <typename T> __host__ __device__ constexpr int cgs_rows() { return sizeof(T) == 8 ? 256 : 128; }
+template <typename T> __host__ __device__ constexpr int cgs_consumers() { return 2 * cgs_rows<T>(); }
+// padding after each column segment in shared memory (16 B): the two lanes
+// of a row read columns c and c+1 in the same instruction, which must not
+// fall in the same bank
+template <typename T> __host__ __device__ constexpr int cgs_pad() { return 16 / int(sizeof(T)); }
+
+// RPT blocks per chunk: a stage of ~48 KB whatever nct is, so the per-chunk
+// handshake stays small against the chunk's transfer time, and never fewer
+// than 2 (>= 4 KB per bulk copy for fp64) while two stages still fit:
+// measured on C4, 2-KB copies (RPT = 1) stream at ~5 TB/s, 4-KB and larger
+// at 6.9-7.9 TB/s
+template <typename T> __host__ __device__ inline int cgs_rpt(int nct) {
+  constexpr int R = cgs_rows<T>();
+  const int col = R * int(sizeof(T));  // bytes of one column segment per RPT block
+  int r = (48 * 1024) / ((nct + 1) * col);
+  if (r < 2 && 2 * (nct + 1) * (2 * col + 16) <= CGS_SMEM - 32 * 8) r = 2;
+  return r > 16 ? 16 : (r < 1 ? 1 : r);
+}
+// shared-memory elements of one stage
+template <typename T> __host__ __device__ inline int cgs_stage_elems(int nct) {
+  return (nct + 1) * (cgs_rows<T>() * cgs_rpt<T>(nct) + cgs_pad<T>());
+}
+// stages of the ring (2..16)
+template <typename T> __host__ __device__ inline int cgs_stages(int nct) {
+  const int stage = cgs_stage_elems<T>(nct) * int(sizeof(T));
+  int S = (CGS_SMEM - 32 * 8) / stage;
+  return S > 16 ? 16 : (S < 2 ? 2 : S);
+}
 
 template <typename T, int NC, int FL>
-__global__ void __launch_bounds__(256, (NC * sizeof(T) <= 128) ? 4 : 2)
-    cgs_kernel(int64_t n, const T* __restrict__ V, int64_t ldv,
-                                                  int nct, T* __restrict__ w,
-                                                  const T* __restrict__ coef_in,
-                                                  T* __restrict__ coef_out, T* __restrict__ Hcol,
-                                                  T* __restrict__ Hsub, double* __restrict__ inv,
-                                                  double* partials, unsigned* counter,
-                                                  double* raw) {
+__global__ void __launch_bounds__(cgs_consumers<T>() + 32, 1)
+    cgs_kernel(int64_t n, const T* __restrict__ V, int64_t ldv, int nct, T* __restrict__ w,
+               const T* __restrict__ coef_in, T* __restrict__ coef_out, T* __restrict__ Hcol,
+               T* __restrict__ Hsub, double* __restrict__ inv, double* partials, unsigned* counter,
+               double* raw) {
   constexpr int ND = n_doubles<T>();
+  constexpr int R = cgs_rows<T>();
+  constexpr int NW = cgs_consumers<T>() / 32;  // consumer warps; warp NW is the producer
+  constexpr int NCL = NC / 2;                  // columns per lane (c = 2 cc + h)
   constexpr bool UPD = FL & F_UPD, PROJ = FL & F_PROJ, NRM = FL & F_NRM;
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ T cin[NC];
-  __shared__ double red[8][NC * ND + 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (UPD) {
-    for (int c = threadIdx.x; c < nct; c += blockDim.x) cin[c] = coef_in[c];
-    __syncthreads();
+  __shared__ double red[NW][NC * ND + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = cgs_stages<T>(nct);
+  const int RPT = cgs_rpt<T>(nct);
+  const int RC = R * RPT;                       // rows per chunk
+  const int CS = RC + cgs_pad<T>();             // column stride in the stage
+  const int stage_elems = cgs_stage_elems<T>(nct);
+  T* ring = reinterpret_cast<T*>(smem);
+  const uint32_t full0 = smem_u32(smem + size_t(S) * stage_elems * sizeof(T));
+  const uint32_t empty0 = full0 + 8 * 16;
+  const int64_t nchunks = (n + RC - 1) / RC;
+  const int64_t nloc = blockIdx.x < nchunks ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  T acc[NC];
+  if (UPD)
+    for (int c = tid; c < nct; c += blockDim.x) cin[c] = coef_in[c];
+  __syncthreads();
+
+  T acc[NCL];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) acc[c] = s_zero<T>();
+  for (int c = 0; c < NCL; ++c) acc[c] = s_zero<T>();
   double nrm = 0.0;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  auto row = [&](int64_t r) {
-    const T* vp = V + r;
-    T wr = w[r];
-    if (UPD) {
-      T s = s_zero<T>();
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        if (c < nct) s = s_fma(ldg(vp + int64_t(c) * ldv), cin[c], s);
-      wr = s_sub(wr, s);
-      w[r] = wr;
-    }
-    if (NRM) nrm += s_abs2(wr);
-    if (PROJ) {
-      // with UPD these re-reads of the row's basis values hit L1 (just loaded
-      // by this thread); keeping them in registers would halve the occupancy
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        if (c < nct) acc[c] = s_cfma(ldg(vp + int64_t(c) * ldv), wr, acc[c]);
-    }
-  };
-  if constexpr (sizeof(T) == 8) {
-    // fp64: two adjacent rows per thread with 128-bit loads (columns are
-    // 256-B aligned and ldv is even, so (r, r+1) with r even is 16-B aligned)
-    const int64_t npair = n >> 1;
-    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < npair; p += stride) {
-      const int64_t r = 2 * p;
-      const double2* vp = reinterpret_cast<const double2*>(V + r);
-      const int64_t ldv2 = ldv >> 1;
-      double2 wr = *reinterpret_cast<const double2*>(w + r);
-      if (UPD) {
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-          if (c < nct) {
-            const double2 v = __ldg(vp + int64_t(c) * ldv2);
-            s0 = fma(v.x, cin[c], s0);
-            s1 = fma(v.y, cin[c], s1);
-          }
-        wr.x -= s0;
-        wr.y -= s1;
-        *reinterpret_cast<double2*>(w + r) = wr;
-      }
-      if (NRM) nrm += wr.x * wr.x + wr.y * wr.y;
-      if (PROJ) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-          if (c < nct) {
-            const double2 v = __ldg(vp + int64_t(c) * ldv2);
-            acc[c] = fma(v.x, wr.x, fma(v.y, wr.y, acc[c]));
-          }
+  const int h = lane & 1;
+
+  if (warp == NW) {
+    // ---- producer warp ----
+    for (int64_t i = 0; i < nloc; ++i) {
+      const int s = int(i % S);
+      if (i >= S) mbar_wait(empty0 + 8 * s, uint32_t(((i / S) - 1) & 1));
+      const int64_t r0 = (int64_t(blockIdx.x) + i * gridDim.x) * RC;
+      const int64_t rows = n - r0 < RC ? n - r0 : RC;
+      // whole 16-B units; a ragged fp64 tail reads one padding element of the
+      // column (columns are padded to a multiple of 64 entries, ldv >= n + 1)
+      const uint32_t bytes = uint32_t((rows * int64_t(sizeof(T)) + 15) & ~int64_t(15));
+      const uint32_t full = full0 + 8 * s;
+      const uint32_t dst = smem_u32(ring + size_t(s) * stage_elems);
+      if (lane == 0) mbar_expect_tx(full, bytes * uint32_t(nct + 1));
+      __syncwarp();
+      for (int c = lane; c <= nct; c += 32) {
+        const T* src = c < nct ? V + int64_t(c) * ldv + r0 : w + r0;
+        bulk_g2s(dst + uint32_t(c * CS * sizeof(T)), src, bytes, full);
       }
     }
-    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) row(n - 1);
   } else {
-    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n; r += stride) row(r);
-  }
-  // block partials
-  if (PROJ) {
+    // ---- consumer warps: lanes (2i, 2i+1) of warp q own row 16 q + i of
+    // every RPT block, lane parity h takes the columns c = h, h+2, ... ----
+    const int lrow = warp * 16 + (lane >> 1);
+    for (int64_t i = 0; i < nloc; ++i) {
+      const int s = int(i % S);
+      mbar_wait(full0 + 8 * s, uint32_t((i / S) & 1));
+      const T* tile = ring + size_t(s) * stage_elems;
+      const int64_t r0 = (int64_t(blockIdx.x) + i * gridDim.x) * RC;
+#pragma unroll 1
+      for (int k = 0; k < RPT; ++k) {
+        const int lr = k * R + lrow;
+        const int64_t r = r0 + lr;
+        const bool valid = r < n;
+        if (!__any_sync(FULL, valid)) break;  // warp-uniform: the shuffles below need every lane
+        T wr = valid ? tile[nct * CS + lr] : s_zero<T>();
+        if (UPD) {
+          // two interleaved partial sums per lane, then the pair's halves
+          T s0 = s_zero<T>(), s1 = s_zero<T>();
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      if (c < nct) {
-        const double* a = reinterpret_cast<const double*>(&acc[c]);
+          for (int cc = 0; cc < NCL; ++cc) {
+            const int c = 2 * cc + h;
+            if (valid && c < nct) {
+              if (cc & 1)
+                s1 = s_fma(tile[c * CS + lr], lds_nohoist(cin + c), s1);
+              else
+                s0 = s_fma(tile[c * CS + lr], lds_nohoist(cin + c), s0);
+            }
+          }
+          T sum = s_add(s0, s1);
+          if constexpr (ND == 1) {
+            sum += __shfl_xor_sync(FULL, sum, 1);
+          } else {
+            cplx& z = reinterpret_cast<cplx&>(sum);
+            z.re += __shfl_xor_sync(FULL, z.re, 1);
+            z.im += __shfl_xor_sync(FULL, z.im, 1);
+          }
+          wr = s_sub(wr, sum);
+          if (valid && h == 0) w[r] = wr;
+        }
+        if (NRM && valid && h == 0) nrm += s_abs2(wr);
+        if (PROJ) {
+#pragma unroll
+          for (int cc = 0; cc < NCL; ++cc) {
+            const int c = 2 * cc + h;
+            if (valid && c < nct) acc[cc] = s_cfma(tile[c * CS + lr], wr, acc[cc]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    }
+  }
+
+  // block partials (the producer warp contributes zeros)
+  if (PROJ) {
+    if (warp < NW) {
+#pragma unroll
+      for (int cc = 0; cc < NCL; ++cc) {
+        const double* a = reinterpret_cast<const double*>(&acc[cc]);
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
-          const double s = warp_sum(a[d]);
-          if (lane == 0) red[warp][c * ND + d] = s;
+          double v = a[d];
+          // sum over the lanes of equal parity: lane 0 -> column 2cc, lane 1 -> 2cc+1
+#pragma unroll
+          for (int o = 16; o > 1; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+          const int c = 2 * cc + lane;
+          if (lane < 2 && c < nct) red[warp][c * ND + d] = v;
         }
       }
     }
     __syncthreads();
-    const int nw = blockDim.x >> 5;
-    for (int i = threadIdx.x; i < nct * ND; i += blockDim.x) {
-      double s = 0.0;
-      for (int q = 0; q < nw; ++q) s += red[q][i];
-      partials[int64_t(blockIdx.x) * nct * ND + i] = s;
+    for (int q = tid; q < nct * ND; q += blockDim.x) {
+      double v = 0.0;
+      for (int k = 0; k < NW; ++k) v += red[k][q];
+      partials[int64_t(blockIdx.x) * nct * ND + q] = v;
     }
   }
   if (NRM) {
     __shared__ double smn[32];
-    const double s = block_sum(nrm, smn);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    const double v = block_sum(nrm, smn);
+    if (tid == 0) partials[blockIdx.x] = v;
   }
   if (last_block(counter)) {
     if (PROJ) {
-      reduce_partials(partials, gridDim.x, nct * ND, nct * ND, [&](int i, double s) {
+      reduce_partials(partials, gridDim.x, nct * ND, nct * ND, [&](int q, double v) {
         if (raw) {
-          raw[i] = s;
+          raw[q] = v;
           return;
         }
-        reinterpret_cast<double*>(coef_out)[i] = s;
-        if (Hcol) reinterpret_cast<double*>(Hcol)[i] = reinterpret_cast<const double*>(coef_in)[i] + s;
+        reinterpret_cast<double*>(coef_out)[q] = v;
+        if (Hcol) reinterpret_cast<double*>(Hcol)[q] = reinterpret_cast<const double*>(coef_in)[q] + v;
       });
     }
     if (NRM) {
-      reduce_partials(partials, gridDim.x, 1, 1, [&](int, double s) {
+      reduce_partials(partials, gridDim.x, 1, 1, [&](int, double v) {
         if (raw) {
-          raw[0] = s;
+          raw[0] = v;
           return;
         }
-        const double nr = sqrt(s);
+        const double nr = sqrt(v);
         double* hs = reinterpret_cast<double*>(Hsub);
         hs[0] = nr;
         if (ND == 2) hs[1] = 0.0;
@@ -609,7 +732,7 @@ __global__ void __launch_bounds__(256, (NC * sizeof(T) <= 128) ? 4 : 2)
       });
     }
     __syncthreads();
-    if (threadIdx.x == 0) *counter = 0;
+    if (tid == 0) *counter = 0;
   }
 }
 
@@ -865,13 +988,27 @@ void launch_combine(ppf_dtype dt, int64_t n, const void* V, int64_t ldv, int nco
 template <typename T, int NC, int FL>
 static void cgs_go(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* ci, T* co, T* hc,
                    T* hs, double* inv, RedScratch& rs, double* raw, int grid, cudaStream_t st) {
-  int64_t b = (n + 255) / 256;
-  int blocks = int(b < grid ? b : grid);
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    cuda_check(cudaFuncSetAttribute(cgs_kernel<T, NC, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    CGS_SMEM),
+               "cudaFuncSetAttribute(cgs_kernel)");
+    attr = true;
+  }
+  const int S = cgs_stages<T>(nct);
+  const int RC = cgs_rows<T>() * cgs_rpt<T>(nct);
+  const size_t smem = size_t(S) * cgs_stage_elems<T>(nct) * sizeof(T) + 2 * 8 * 16;  // ring + 2 x 16 mbarriers
+  const int64_t chunks = (n + RC - 1) / RC;
+  int blocks = int(chunks < grid ? chunks : grid);
   if (blocks < 1) blocks = 1;
-  cgs_kernel<T, NC, FL><<<blocks, 256, 0, st>>>(n, V, ldv, nct, w, ci, co, hc, hs, inv,
-                                                rs.partials, rs.counter, raw);
+  cgs_kernel<T, NC, FL><<<blocks, cgs_consumers<T>() + 32, smem, st>>>(
+      n, V, ldv, nct, w, ci, co, hc, hs, inv, rs.partials, rs.counter, raw);
   post_launch("cgs_kernel");
 }
+
+// column tile width per launch: 24 (fp64: two stages of 25 x 4 KB column
+// segments fit in shared memory, cgs_rpt) / 16 (complex)
+template <typename T> constexpr int cgs_tile() { return sizeof(T) == 8 ? 24 : 16; }
 
 template <typename T, int FL>
 static void cgs_nc(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* ci, T* co, T* hc,
@@ -884,15 +1021,17 @@ static void cgs_nc(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* c
     cgs_go<T, 8, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
   else if (nct <= 16)
     cgs_go<T, 16, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
-  else
+  else if constexpr (cgs_tile<T>() > 16)
     cgs_go<T, 32, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
+  else
+    fail(PPF_EINVAL, "CGS column tile too wide");
 }
 
 template <typename T>
 static int cgs_dispatch(int mode, int64_t n, const void* Vv, int64_t ldv, int ncols, void* wv,
                         const void* civ, void* cov, void* hcv, void* hsv, double* inv,
                         RedScratch& rs, int grid, cudaStream_t st) {
-  constexpr int TILE = 32;
+  constexpr int TILE = cgs_tile<T>();
   auto V = static_cast<const T*>(Vv);
   auto w = static_cast<T*>(wv);
   auto ci = static_cast<const T*>(civ);

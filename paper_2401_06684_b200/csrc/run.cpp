@@ -141,7 +141,7 @@ struct Runner {
       rs.raw = reinterpret_cast<double*>(w + L.raw);
     }
     grid_vec = std::min(L.max_blocks, 4 * c->num_sms);
-    grid_cgs = std::min(L.max_blocks, 4 * c->num_sms);
+    grid_cgs = std::min(L.max_blocks, c->num_sms);  // persistent CGS kernel: one CTA per SM
     PPF_CUDA(cudaMemsetAsync(w + L.counter, 0, 256, st));
     PPF_CUDA(cudaMemsetAsync(w + L.H, 0, size_t(L.ldh) * (m_max + 1) * sc, st));
   }
