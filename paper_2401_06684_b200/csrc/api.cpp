@@ -100,6 +100,8 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
   c->nranks = nranks;
   c->stream = static_cast<cudaStream_t>(stream);
   c->nccl_comm = nullptr;
+  c->comm_stream = nullptr;
+  c->ev_pack = c->ev_halo = nullptr;
   c->last_m = 0;
   c->last_beta0 = 0.0;
   c->last_dtype = PPF_R64;
@@ -118,6 +120,9 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
       if (ncclCommInitRank(&comm, nranks, id, rank) != ncclSuccess)
         fail(PPF_ENCCL, "ncclCommInitRank failed");
       c->nccl_comm = comm;
+      PPF_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+      PPF_CUDA(cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming));
+      PPF_CUDA(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
     }
   } catch (...) {
     delete c;
@@ -150,6 +155,9 @@ void ppf_ctx_destroy(ppf_ctx* c) {
   if (c->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->ev) cudaEventDestroy(c->ev);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   delete c;
 }
 

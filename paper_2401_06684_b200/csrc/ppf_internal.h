@@ -169,6 +169,11 @@ struct ppf_ctx {
   int device, rank, nranks;
   cudaStream_t stream;
   void* nccl_comm;            // ncclComm_t when nranks > 1
+  // halo exchange overlap (nranks > 1 with a communicator): the NCCL
+  // send/recv runs on comm_stream while the diagonal-block SpMV runs on
+  // `stream`; ev_pack / ev_halo order the two streams
+  cudaStream_t comm_stream;
+  cudaEvent_t ev_pack, ev_halo;
   int num_sms;
   // pinned host staging for H columns and y
   void* h_pinned;
@@ -226,6 +231,8 @@ int auto_sell_ks(const ppf_mat* m, int num_sms);
 void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st);
 void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
 void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st);
+// run.cpp: the sharded SpMV with communication/compute overlap
+void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e);
 
 struct RedScratch {   // reduction scratch (device)
   double* partials;   // [max_blocks * max_vals * 2]
