@@ -172,23 +172,87 @@ def test_r4_reference_vs_dense():
 
 
 @pytest.mark.slow
-def test_table1_iteration_counts():
-    """PAPER.md:438-450, Table 1 rows d = 8, 16 at the paper's own scale
-    (3D Laplacian 100^3, tol 1e-12, k = 64/d); see golden file for the reading."""
-    g = json.load(open(os.path.join(GOLDEN, "table1_counts.json")))
+def _table1_setup():
     N = 100
     A = ops.laplacian(N, 3)
     a, bb = ops.laplacian_interval(N, 3)
     b = np.random.default_rng(0).standard_normal(N**3)
     b /= np.linalg.norm(b)
-    op = Operator(A.to_scipy())
-    xr = reference.laplacian_fAb(N, 3, b)
+    return A, (a, bb), b, Operator(A.to_scipy()), reference.laplacian_fAb(N, 3, b)
+
+
+def test_table1_iteration_counts_right_preconditioning():
+    """PAPER.md:438-450, Table 1 rows d = 1, 4, 8, 16 at the paper's own scale
+    (3D Laplacian 100^3, tol 1e-12, k = 64/d) with Algorithm 2 (right
+    preconditioning) and the plain method for d = 1: iterations,
+    mvms and inner products all three exactly (see golden file)."""
+    g = json.load(open(os.path.join(GOLDEN, "table1_counts.json")))
+    A, (a, bb), b, op, xr = _table1_setup()
     for row in g["rows"]:
         d = row["d"]
-        q = chebyshev.coefficients(a, bb, d - 1)
-        assert chebyshev.certify(q) > 0                          # P:420
-        res = krylov.run(op, b, q, func="invsqrt", krylov="lanczos", m_max=200, stop="true",
-                         tol=1e-12, check_every=64 // d, x_ref=xr)
-        assert res.m == row["iterations"]
-        assert res.mvms - (d - 1) == row["mvms"]
-        assert res.inner_products == row["inner_products"]
+        q = None if d == 1 else chebyshev.coefficients(a, bb, d - 1)
+        if q is not None:
+            assert chebyshev.certify(q) > 0                      # P:420
+        res = krylov.run(op, b, q, func="invsqrt", krylov="lanczos", m_max=600, stop="true",
+                         tol=1e-12, check_every=64 // d, x_ref=xr, precond="right")
+        assert res.m == row["iterations"], d
+        assert res.mvms == row["mvms"], d
+        assert res.inner_products == row["inner_products"], d
+
+
+def test_table1_left_preconditioning_same_iterations():
+    """Left preconditioning (Algorithm 1) at Table 1's d = 16: the same 28
+    iterations, plus d-1 = 15 mvms for c = q(A)b."""
+    A, (a, bb), b, op, xr = _table1_setup()
+    q = chebyshev.coefficients(a, bb, 15)
+    res = krylov.run(op, b, q, func="invsqrt", krylov="lanczos", m_max=200, stop="true",
+                     tol=1e-12, check_every=4, x_ref=xr)
+    assert res.m == 28
+    assert res.mvms - 15 == 868
+    assert res.inner_products == 56
+
+
+@pytest.mark.parametrize("precond", ["left", "right", "plain"])
+def test_two_pass_lanczos_closed_form(precond):
+    """Two-pass Lanczos against the DST-I closed form
+    (reference R1) on a 3D Laplacian: pass 1 stops on the estimate, pass 2
+    regenerates the basis; the result must meet the tolerance against the
+    closed form and need the same m as the one-pass method."""
+    N = 14
+    A = ops.laplacian(N, 3)
+    a, bb = ops.laplacian_interval(N, 3)
+    b = np.random.default_rng(41).standard_normal(N**3)
+    xr = reference.laplacian_fAb(N, 3, b)
+    op = Operator(A.to_scipy())
+    q = None if precond == "plain" else chebyshev.coefficients(a, bb, 6)
+    pre = "left" if precond == "plain" else precond
+    one = krylov.run(op, b, q, func="invsqrt", krylov="lanczos", m_max=200, stop="est", tol=1e-10,
+                     precond=pre)
+    two = krylov.run_two_pass(op, b, q, func="invsqrt", precond=pre, m_max=200, stop="est",
+                              tol=1e-10)
+    assert two.m == one.m
+    assert np.linalg.norm(two.x - xr) <= 1e-9 * np.linalg.norm(xr)
+    assert np.allclose(two.H, one.H, rtol=0, atol=1e-12 * np.abs(one.H).max())
+    # pass 2 repeats the operator applications of steps 1..m-1
+    per_step = 1 if q is None else 2 * q.deg + 1
+    start = 0 if (q is None or pre == "right") else q.deg
+    final_q = q.deg if (q is not None and pre == "right") else 0
+    assert two.mvms == start + one.m * per_step + (one.m - 1) * per_step + final_q
+
+
+def test_right_preconditioning_nonhermitian_closed_form():
+    """Algorithm 2 with CGS2 on the 2D convection-diffusion operator, sqrt via
+    A^{-1/2}(Ab), against the long-double closed form R2."""
+    N, beta = 24, (20.0, 20.0)
+    A = ops.convdiff(N, 2, beta)
+    a, bb = ops.convdiff_interval(N, 2, beta)
+    b = np.random.default_rng(8).standard_normal(N**2)
+    xr = reference.convdiff_fAb(N, 2, beta, b, "sqrt")
+    op = Operator(A.to_scipy())
+    q = chebyshev.coefficients(a, bb, 8)
+    res = krylov.run(op, b, q, func="sqrt", krylov="cgs2", m_max=120, stop="true", tol=1e-9,
+                     x_ref=xr, precond="right")
+    assert res.term == "converged"
+    left = krylov.run(op, b, q, func="sqrt", krylov="cgs2", m_max=120, stop="true", tol=1e-9,
+                      x_ref=xr)
+    assert abs(res.m - left.m) <= 2
