@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PPF_ABI_VERSION 1
+#define PPF_ABI_VERSION 2
 
 typedef enum {
   PPF_OK = 0,
@@ -58,7 +58,17 @@ typedef enum {
 
 typedef enum { PPF_R64 = 0, PPF_C128 = 1 } ppf_dtype;
 typedef enum { PPF_INVSQRT = 0, PPF_SQRT = 1 } ppf_func;            /* SQRT = A^{-1/2}(A b) */
-typedef enum { PPF_LANCZOS = 0, PPF_ARNOLDI_CGS2 = 1 } ppf_krylov;  /* reading Q8 */
+typedef enum {
+  PPF_LANCZOS = 0,        /* Hermitian A: three-term recurrence, all basis vectors kept (reading Q8) */
+  PPF_ARNOLDI_CGS2 = 1,   /* general A: classical Gram-Schmidt with one reorthogonalisation */
+  PPF_LANCZOS_2PASS = 2   /* Hermitian A, two-pass: pass 1 assembles H_m keeping
+                             3 basis vectors, pass 2 regenerates them to form f_m */
+} ppf_krylov;
+typedef enum {
+  PPF_PREC_LEFT = 0,      /* Algorithm 1: Krylov space of A q(A)^2 from q(A)s */
+  PPF_PREC_RIGHT = 1      /* Algorithm 2: from s; f_m = Y_m (H_m^{-1/2} e_1 ||s||),
+                             y_j = q(A) v_j stored (one-pass) or f_m = q(A) V_m (...) (two-pass) */
+} ppf_precond;
 typedef enum { PPF_STOP_FIXED_M = 0, PPF_STOP_EST = 1, PPF_STOP_TRUE_ERR = 2 } ppf_stop;
 typedef enum { PPF_CONVERGED = 0, PPF_MAX_ITER = 1, PPF_BREAKDOWN = 2 } ppf_term;
 typedef enum { PPF_POLY_CHEBYSHEV = 0, PPF_POLY_NEWTON = 1 } ppf_poly_kind;
@@ -193,21 +203,24 @@ void ppf_poly_destroy(ppf_poly* q);
 /* ----------------------------------------------------------------------------
  * The run (layers L2-L5): Algorithm 1, f(H_m) on the host, x = V_m y_m.
  *
- * opts.func / krylov: see enums.  m_max >= 1 (<= 255).  stop:
+ * opts.func / krylov / precond: see enums.  q == NULL selects the plain
+ *   (unpreconditioned, d = 1) method: the Krylov space of A from s ("d = 1
+ *   corresponds to an unpreconditioned method"); precond is then ignored.
+ *   m_max >= 1 (<= 255).  stop:
  *   FIXED_M   run exactly m_max steps (unless breakdown);
  *   EST       stop at the first checkpoint m with the paper's estimate
- *             ||f_m - f_{m-k}|| / ||f_m|| = ||[y_{m-k};0] - y_m|| / ||y_m|| <= tol
- *             (P:174), k = check_every;
+ *             ||f_m - f_{m-k}|| / ||f_m|| <= tol, k = check_every.
+ *             Left / plain: = ||[y_{m-k};0] - y_m|| / ||y_m|| (V orthonormal).
+ *             Right, one-pass: formed from the iterates Y_m y_m on the device
+ *             (Y_m is not orthonormal).  Right, two-pass: the
+ *             coefficient difference is used as a proxy (DESIGN.md readings);
  *   TRUE_ERR  stop at the first checkpoint with ||f_m - x_ref|| / ||x_ref|| <= tol
- *             (x_ref device, n_local entries; for calibrating m*, reading Q11).
- * breakdown_rtol: h_{j+1,j} <= breakdown_rtol * ||c|| ends the run with
- *   term = BREAKDOWN (reading Q9; 0 selects 1e-14).
- * record_history: keep per-checkpoint (m, est, err, mvms) for ppf_history.
- * Non-convergence and breakdown are not errors (status OK, term says why).
- *
+ *             (x_ref device, n_local entries; for calibrating m*, reading Q11);
+ *             not available with PPF_LANCZOS_2PASS (PPF_EINVAL).
  * ppf_workspace_bytes: device scratch `work` needed by ppf_run for these
- *   (A, q, opts); it holds V (m_max+1 columns), 5 n-vectors and reduction
- *   scratch.
+ *   (A, q, opts); it holds V (m_max+1 columns; 4 for PPF_LANCZOS_2PASS), Y
+ *   (m_max columns, right preconditioning one-pass only), 5-6 n-vectors and
+ *   reduction scratch.
  * ppf_run: b, x device (n_local entries).  Enqueues everything on the context
  *   stream and returns once x has been enqueued; the report is valid on return.
  * ppf_run_host: the same with b_host / x_host host buffers; the H2D copy of b
@@ -227,6 +240,7 @@ typedef struct {
   const void* x_ref;   /* device, TRUE_ERR only */
   double breakdown_rtol;
   int record_history;
+  int precond;         /* ppf_precond (ABI 2) */
 } ppf_opts;
 
 typedef struct {

@@ -16,7 +16,8 @@ STATUS = {0: "PPF_OK", 1: "PPF_EINVAL", 2: "PPF_ECUDA", 3: "PPF_ENCCL", 4: "PPF_
           5: "PPF_EBRANCH", 6: "PPF_EDENSE", 7: "PPF_ESTATE"}
 R64, C128 = 0, 1
 INVSQRT, SQRT = 0, 1
-LANCZOS, ARNOLDI_CGS2 = 0, 1
+LANCZOS, ARNOLDI_CGS2, LANCZOS_2PASS = 0, 1, 2
+PREC_LEFT, PREC_RIGHT = 0, 1
 STOP_FIXED_M, STOP_EST, STOP_TRUE_ERR = 0, 1, 2
 CONVERGED, MAX_ITER, BREAKDOWN = 0, 1, 2
 POLY_CHEBYSHEV, POLY_NEWTON = 0, 1
@@ -30,7 +31,8 @@ dblp = C.POINTER(C.c_double)
 class Opts(C.Structure):
     _fields_ = [("func", C.c_int), ("krylov", C.c_int), ("m_max", C.c_int), ("stop", C.c_int),
                 ("tol", C.c_double), ("check_every", C.c_int), ("x_ref", vp),
-                ("breakdown_rtol", C.c_double), ("record_history", C.c_int)]
+                ("breakdown_rtol", C.c_double), ("record_history", C.c_int),
+                ("precond", C.c_int)]
 
 
 class Report(C.Structure):

@@ -283,12 +283,13 @@ class RunReport:
 
 _TERM = {L.CONVERGED: "converged", L.MAX_ITER: "max_iter", L.BREAKDOWN: "breakdown"}
 _FUNC = {"invsqrt": L.INVSQRT, "sqrt": L.SQRT}
-_KRY = {"lanczos": L.LANCZOS, "cgs2": L.ARNOLDI_CGS2}
+_KRY = {"lanczos": L.LANCZOS, "cgs2": L.ARNOLDI_CGS2, "lanczos2p": L.LANCZOS_2PASS}
+_PREC = {"left": L.PREC_LEFT, "right": L.PREC_RIGHT}
 _STOP = {"fixed": L.STOP_FIXED_M, "est": L.STOP_EST, "true": L.STOP_TRUE_ERR}
 
 
 def make_opts(func="invsqrt", krylov="cgs2", m_max=60, stop="fixed", tol=1e-8, check_every=1,
-              x_ref=None, breakdown_rtol=0.0, record_history=True) -> L.Opts:
+              x_ref=None, breakdown_rtol=0.0, record_history=True, precond="left") -> L.Opts:
     o = L.Opts()
     o.func = _FUNC[func]
     o.krylov = _KRY[krylov]
@@ -299,6 +300,7 @@ def make_opts(func="invsqrt", krylov="cgs2", m_max=60, stop="fixed", tol=1e-8, c
     o.x_ref = C.c_void_p(x_ref.data_ptr()) if x_ref is not None else None
     o.breakdown_rtol = float(breakdown_rtol)
     o.record_history = int(bool(record_history))
+    o.precond = _PREC[precond]
     return o
 
 
@@ -308,9 +310,14 @@ class Workspace:
     def __init__(self, ctx: Context, A: Matrix, q: Poly, opts: L.Opts):
         torch = _torch()
         nb = C.c_size_t()
-        check(_lib().ppf_workspace_bytes(ctx.h, A.h, q.h, C.byref(opts), C.byref(nb)))
+        check(_lib().ppf_workspace_bytes(ctx.h, A.h, _qh(q), C.byref(opts), C.byref(nb)))
         self.nbytes = nb.value
         self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=f"cuda:{ctx.device}")
+
+
+def _qh(q):
+    """ppf_poly handle, or NULL for the plain (unpreconditioned, d = 1) method."""
+    return None if q is None else q.h
 
 
 def _report(r: L.Report) -> RunReport:
@@ -327,7 +334,7 @@ def run(ctx: Context, A: Matrix, q: Poly, b, x=None, work: Workspace | None = No
     if x is None:
         x = torch.empty_like(b)
     rep = L.Report()
-    check(_lib().ppf_run(ctx.h, A.h, q.h, C.byref(opts), C.c_void_p(b.data_ptr()),
+    check(_lib().ppf_run(ctx.h, A.h, _qh(q), C.byref(opts), C.c_void_p(b.data_ptr()),
                          C.c_void_p(x.data_ptr()), C.c_void_p(work.buf.data_ptr()), work.nbytes,
                          C.byref(rep)))
     return x, _report(rep)
@@ -340,7 +347,7 @@ def run_host(ctx: Context, A: Matrix, q: Poly, b_host, x_host, work: Workspace |
     if work is None:
         work = Workspace(ctx, A, q, opts)
     rep = L.Report()
-    check(_lib().ppf_run_host(ctx.h, A.h, q.h, C.byref(opts), C.c_void_p(b_host.data_ptr()),
+    check(_lib().ppf_run_host(ctx.h, A.h, _qh(q), C.byref(opts), C.c_void_p(b_host.data_ptr()),
                               C.c_void_p(x_host.data_ptr()), C.c_void_p(work.buf.data_ptr()),
                               work.nbytes, C.byref(rep)))
     return x_host, _report(rep)

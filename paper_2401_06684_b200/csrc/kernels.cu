@@ -803,6 +803,28 @@ __global__ void __launch_bounds__(256) lanczos_kernel(int64_t n, const T* __rest
   }
 }
 
+// Two-pass Lanczos, pass 2: with the pass-1 recurrence
+// coefficients known on the host, regenerate the next basis vector from
+// w = Op v_j and accumulate the iterate, one sweep:
+//   v_{j+1} = (w - alpha v_j - beta_prev v_{j-1}) * inv_beta   (in place in w)
+//   x += ycoef * v_{j+1}
+template <typename T>
+__global__ void __launch_bounds__(256) lanczos_regen_kernel(int64_t n, T* __restrict__ w,
+                                                            const T* __restrict__ v,
+                                                            const T* __restrict__ vprev,
+                                                            double alpha, double beta_prev,
+                                                            double inv_beta, double ycoef,
+                                                            T* __restrict__ x) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    T t = s_sub(w[i], s_scale(ldg(v + i), alpha));
+    if (vprev) t = s_sub(t, s_scale(ldg(vprev + i), beta_prev));
+    t = s_scale(t, inv_beta);
+    w[i] = t;
+    x[i] = s_add(x[i], s_scale(t, ycoef));
+  }
+}
+
 int blocks_for(int64_t n, int threads, int cap) {
   int64_t b = (n + threads - 1) / threads;
   if (b > cap) b = cap;
@@ -967,6 +989,21 @@ void launch_diffnorm(ppf_dtype dt, int64_t n, const void* a, const void* b, doub
                                                   static_cast<const cplx*>(b), out, rs.partials,
                                                   rs.counter, rs.raw);
   post_launch("diffnorm_kernel");
+}
+
+void launch_lanczos_regen(ppf_dtype dt, int64_t n, void* w, const void* v, const void* vprev,
+                          double alpha, double beta_prev, double inv_beta, double ycoef, void* x,
+                          cudaStream_t st) {
+  const int blocks = blocks_for(n, 256, 148 * 8);
+  if (dt == PPF_R64)
+    lanczos_regen_kernel<double><<<blocks, 256, 0, st>>>(
+        n, static_cast<double*>(w), static_cast<const double*>(v), static_cast<const double*>(vprev),
+        alpha, beta_prev, inv_beta, ycoef, static_cast<double*>(x));
+  else
+    lanczos_regen_kernel<cplx><<<blocks, 256, 0, st>>>(
+        n, static_cast<cplx*>(w), static_cast<const cplx*>(v), static_cast<const cplx*>(vprev), alpha,
+        beta_prev, inv_beta, ycoef, static_cast<cplx*>(x));
+  post_launch("lanczos_regen_kernel");
 }
 
 void launch_combine(ppf_dtype dt, int64_t n, const void* V, int64_t ldv, int ncols, const void* y,

@@ -263,6 +263,10 @@ int launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, in
 void launch_lanczos(ppf_dtype dt, int phase, int64_t n, const void* v, const void* vprev,
                     const double* beta_prev, void* w, void* Hdiag, void* Hsub, void* Hsup,
                     double* inv, RedScratch& rs, int grid, cudaStream_t st);
+// two-pass Lanczos pass 2: w <- (w - alpha v - beta_prev vprev) * inv_beta; x += ycoef * w
+void launch_lanczos_regen(ppf_dtype dt, int64_t n, void* w, const void* v, const void* vprev,
+                          double alpha, double beta_prev, double inv_beta, double ycoef, void* x,
+                          cudaStream_t st);
 // x = V y (y device, ncols entries)
 void launch_combine(ppf_dtype dt, int64_t n, const void* V, int64_t ldv, int ncols, const void* y,
                     void* x, cudaStream_t st);

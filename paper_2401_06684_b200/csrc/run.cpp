@@ -26,25 +26,34 @@ namespace {
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Workspace shape: which bases the run keeps.
+enum { WS_RIGHT = 1,     // right preconditioning, one-pass: Y_m (m_max columns)
+       WS_TWOPASS = 2 }; // two-pass Lanczos: V = {v_1, ring of 3}, + accumulator XA
+
 struct WsLayout {
   int64_t ldv;       // leading dimension of V and vector length (padded)
   int ldh;           // leading dimension of H
-  size_t V, U, Y, T0, T1, T2, H, hbuf, gbuf, ybuf, scal, partials, counter, raw, total;
+  int vcols;         // columns of V
+  size_t V, Yb, U, Y, T0, T1, T2, XA, H, hbuf, gbuf, ybuf, ybuf2, scal, partials, counter, raw,
+      total;
   int max_blocks;
   int max_vals;
 };
 
-WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms) {
+WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms, int shape = 0) {
   const size_t sc = dt == PPF_R64 ? 8 : 16;
   WsLayout L{};
   L.ldv = (n + 63) & ~int64_t(63);
   L.ldh = m_max + 2;
   L.max_blocks = std::max(8 * num_sms, 256);
   L.max_vals = (m_max + 2) * 2;
+  L.vcols = (shape & WS_TWOPASS) ? 4 : m_max + 1;
   size_t o = 0;
   const size_t vec = al256(size_t(L.ldv) * sc);
   L.V = o;
-  o += vec * size_t(m_max + 1);
+  o += vec * size_t(L.vcols);
+  L.Yb = o;
+  if (shape & WS_RIGHT) o += vec * size_t(m_max);
   L.U = o;
   o += vec;
   L.Y = o;
@@ -55,6 +64,8 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms) {
   o += vec;
   L.T2 = o;
   o += vec;
+  L.XA = o;
+  if (shape & WS_TWOPASS) o += vec;
   L.H = o;
   o += al256(size_t(L.ldh) * (m_max + 1) * sc);
   L.hbuf = o;
@@ -62,6 +73,8 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms) {
   L.gbuf = o;
   o += al256(size_t(m_max + 2) * sc);
   L.ybuf = o;
+  o += al256(size_t(m_max + 2) * sc);
+  L.ybuf2 = o;
   o += al256(size_t(m_max + 2) * sc);
   L.scal = o;
   o += 256;
@@ -73,6 +86,13 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms) {
   o += al256(size_t(L.max_vals) * 8);
   L.total = o;
   return L;
+}
+
+int ws_shape(const ppf_poly* q, const ppf_opts* o) {
+  int s = 0;
+  if (o->krylov == PPF_LANCZOS_2PASS) s |= WS_TWOPASS;
+  else if (q && o->precond == PPF_PREC_RIGHT) s |= WS_RIGHT;
+  return s;
 }
 
 // scalar slots (doubles) in the scal area
@@ -150,10 +170,16 @@ struct Runner {
     timed(2, 0.0, [&] { launch_finalize(op, nv, int(sc / 8), rs.raw, o0, o1, o2, ci, st); });
   }
 
-  Runner(ppf_ctx* c, ppf_mat* a, const ppf_poly* qq, int m_max, void* work, size_t bytes)
+  bool right = false;    // Algorithm 2 (y_j = q(A) v_j first, w = A q(A) y_j)
+  bool twopass = false;  // V is {v_1, ring of 3}
+
+  Runner(ppf_ctx* c, ppf_mat* a, const ppf_poly* qq, int m_max, void* work, size_t bytes,
+         int shape = 0, bool right_prec = false)
       : ctx(c), A(a), q(qq), dt(a->dtype), n(a->n_local) {
     sc = dt == PPF_R64 ? 8 : 16;
-    L = ws_layout(n, dt, m_max, c->num_sms);
+    L = ws_layout(n, dt, m_max, c->num_sms, shape);
+    right = right_prec && q;
+    twopass = shape & WS_TWOPASS;
     if (!work || bytes < L.total) fail(PPF_EWORKSPACE, "workspace too small");
     if (reinterpret_cast<uintptr_t>(work) & 255) fail(PPF_EINVAL, "workspace not 256-B aligned");
     w = static_cast<char*>(work);
@@ -173,6 +199,11 @@ struct Runner {
   }
 
   void* V(int j) { return w + L.V + size_t(j) * al256(size_t(L.ldv) * sc); }
+  void* Yb(int j) { return w + L.Yb + size_t(j) * al256(size_t(L.ldv) * sc); }
+  // basis vectors of step j: v_j (source), w -> v_{j+1} (destination), v_{j-1}
+  void* vsrc(int j) { return twopass ? V(1 + j % 3) : V(j); }
+  void* vdst(int j) { return twopass ? V(1 + (j + 1) % 3) : V(j + 1); }
+  void* vprv(int j) { return j == 0 ? nullptr : (twopass ? V(1 + (j + 2) % 3) : V(j - 1)); }
   void* vec(size_t off) { return w + off; }
   void* Hp(int i, int j) { return w + L.H + (size_t(i) + size_t(j) * L.ldh) * sc; }
   double* scal(int i) { return reinterpret_cast<double*>(w + L.scal) + i; }
@@ -315,15 +346,23 @@ struct Runner {
     }
   }
 
-  // w = Op v_j into V[j+1]; Op = A q(A)^2 (three stages) or A (q == null).
+  // w = Op v_j into vdst(j).  Op = A (q == null, plain method);
+  // left (Alg 1 line 4): u = A v_j, y = q(A)u, w = q(A)y;
+  // right (Alg 2 line 4): y_j = q(A)v_j (kept in Y_m one-pass), u = q(A)y_j, w = A u.
   void op_apply(int j) {
+    const Epi plain = epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr);
     if (!q) {
-      spmv(V(j), V(j + 1), epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
-      return;
+      spmv(vsrc(j), vdst(j), plain);
+    } else if (right) {
+      void* yj = twopass ? vec(L.Y) : Yb(j);
+      apply_q(vsrc(j), yj);
+      apply_q(yj, vec(L.U));
+      spmv(vec(L.U), vdst(j), plain);
+    } else {
+      spmv(vsrc(j), vec(L.U), plain);
+      apply_q(vec(L.U), vec(L.Y));
+      apply_q(vec(L.Y), vdst(j));
     }
-    spmv(V(j), vec(L.U), epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
-    apply_q(vec(L.U), vec(L.Y));
-    apply_q(vec(L.Y), V(j + 1));
   }
 
   void orthogonalise(int j, bool lanczos) {
@@ -331,12 +370,12 @@ struct Runner {
     if (lanczos) {
       const double* bprev = j > 0 ? reinterpret_cast<const double*>(Hp(j, j - 1)) : nullptr;
       timed(1, vb * (j > 0 ? 4 : 3), [&] {
-        launch_lanczos(dt, 1, n, V(j), j > 0 ? V(j - 1) : nullptr, bprev, V(j + 1), Hp(j, j),
-                       nullptr, nullptr, nullptr, rs, grid_vec, st);
+        launch_lanczos(dt, 1, n, vsrc(j), vprv(j), bprev, vdst(j), Hp(j, j), nullptr, nullptr,
+                       nullptr, rs, grid_vec, st);
       });
       reduce_fin(FIN_LZ1, int(sc / 8), Hp(j, j), nullptr, nullptr, nullptr);
       timed(1, vb * 3, [&] {
-        launch_lanczos(dt, 2, n, V(j), nullptr, nullptr, V(j + 1), Hp(j, j), Hp(j + 1, j),
+        launch_lanczos(dt, 2, n, vsrc(j), nullptr, nullptr, vdst(j), Hp(j, j), Hp(j + 1, j),
                        Hp(j, j + 1), scal(S_INV), rs, grid_vec, st);
       });
       reduce_fin(FIN_LZ2, 1, Hp(j + 1, j), Hp(j, j + 1), scal(S_INV), nullptr);
@@ -361,7 +400,7 @@ struct Runner {
       });
       reduce_fin(FIN_SUBNORM, 1, Hp(j + 1, j), nullptr, scal(S_INV), nullptr);
     }
-    timed(1, vb * 2, [&] { launch_scale(dt, n, V(j + 1), V(j + 1), scal(S_INV), 0.0, st); });
+    timed(1, vb * 2, [&] { launch_scale(dt, n, vdst(j), vdst(j), scal(S_INV), 0.0, st); });
   }
 
   // start: V0 = s/||s||  (||s|| -> scal(S_BETA0))
@@ -450,15 +489,17 @@ struct Runner {
     std::memcpy(&beta0, hp + bytes, 8);
   }
 
-  void upload_y(const std::vector<zc>& y) {
-    char* hp = static_cast<char*>(ctx->h_pinned) + ctx->h_pinned_bytes - 8192;
+  void upload_y(const std::vector<zc>& y, size_t dst_off = size_t(-1), int slot = 0) {
+    if (dst_off == size_t(-1)) dst_off = L.ybuf;
+    char* hp = static_cast<char*>(ctx->h_pinned) + ctx->h_pinned_bytes - 8192 + slot * 4096;
     double* d = reinterpret_cast<double*>(hp);
     const int nd = int(sc / 8);
     for (size_t i = 0; i < y.size(); ++i) {
       d[i * nd] = y[i].real();
       if (nd == 2) d[i * nd + 1] = y[i].imag();
     }
-    PPF_CUDA(cudaMemcpyAsync(w + L.ybuf, hp, y.size() * sc, cudaMemcpyHostToDevice, st));
+    if (y.size() * sc > 4096) fail(PPF_EINVAL, "m too large for the coefficient staging buffer");
+    PPF_CUDA(cudaMemcpyAsync(w + dst_off, hp, y.size() * sc, cudaMemcpyHostToDevice, st));
   }
 };
 
@@ -489,28 +530,37 @@ double nrm(const std::vector<zc>& v) {
 void check_opts(const ppf_opts* o) {
   PPF_REQUIRE(o, "opts is NULL");
   PPF_REQUIRE(o->func == PPF_INVSQRT || o->func == PPF_SQRT, "bad func");
-  PPF_REQUIRE(o->krylov == PPF_LANCZOS || o->krylov == PPF_ARNOLDI_CGS2, "bad krylov");
+  PPF_REQUIRE(o->krylov == PPF_LANCZOS || o->krylov == PPF_ARNOLDI_CGS2 ||
+                  o->krylov == PPF_LANCZOS_2PASS,
+              "bad krylov");
+  PPF_REQUIRE(o->precond == PPF_PREC_LEFT || o->precond == PPF_PREC_RIGHT, "bad precond");
   PPF_REQUIRE(o->m_max >= 1 && o->m_max <= 255, "m_max out of range [1, 255]");
   PPF_REQUIRE(o->stop >= 0 && o->stop <= 2, "bad stop");
   PPF_REQUIRE(o->stop == PPF_STOP_FIXED_M || o->tol > 0.0, "tol must be > 0");
   PPF_REQUIRE(o->check_every >= 1 || o->stop == PPF_STOP_FIXED_M, "check_every >= 1");
   PPF_REQUIRE(o->stop != PPF_STOP_TRUE_ERR || o->x_ref, "TRUE_ERR needs x_ref");
+  PPF_REQUIRE(o->stop != PPF_STOP_TRUE_ERR || o->krylov != PPF_LANCZOS_2PASS,
+              "TRUE_ERR needs the basis: not available with the two-pass method");
 }
 
 ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts* o,
                     const void* b, void* x, const void* b_host, void* x_host, void* work,
                     size_t bytes, ppf_report* rep) {
   auto t_start = std::chrono::steady_clock::now();
-  PPF_REQUIRE(ctx && A && q && rep, "NULL argument");
+  PPF_REQUIRE(ctx && A && rep, "NULL argument");
   PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
   check_opts(o);
-  PPF_REQUIRE(q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
+  PPF_REQUIRE(!q || q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
               "a Newton (complex) polynomial needs a complex operator");
-  const bool lanczos = o->krylov == PPF_LANCZOS;
+  const bool twopass = o->krylov == PPF_LANCZOS_2PASS;
+  const bool lanczos = o->krylov != PPF_ARNOLDI_CGS2;
+  const bool right = q && o->precond == PPF_PREC_RIGHT;
+  const int deg = q ? q->deg : 0;
+  const long long per_step = q ? 2LL * deg + 1 : 1;   // mvms per preconditioned step
   const int m_max = o->m_max;
   const int k = std::max(1, o->check_every);
   const double brt = o->breakdown_rtol > 0.0 ? o->breakdown_rtol : 1e-14;
-  Runner R(ctx, A, q, m_max, work, bytes);
+  Runner R(ctx, A, q, m_max, work, bytes, ws_shape(q, o), right);
   const int64_t n = R.n;
   const size_t vb = size_t(n) * R.sc;
   double t_dense = 0.0;
@@ -521,17 +571,26 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     PPF_CUDA(cudaMemcpyAsync(R.vec(R.L.U), b_host, vb, cudaMemcpyHostToDevice, R.st));
     bin = R.vec(R.L.U);
   }
-  // line 2: c = q(A) s, s = b or A b
+  // start (Alg 1 line 2 / Alg 2 line 2): s = b or A b; left: c = q(A) s;
+  // right / plain: c = s.  v_1 = c / ||c||.
   long long mvms = 0;
+  const void* s_vec = bin;
   if (o->func == PPF_SQRT) {
-    R.spmv(bin, R.vec(R.L.Y), Runner::epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
+    void* sdst = (right || !q) ? R.V(0) : R.vec(R.L.Y);
+    R.spmv(bin, sdst, Runner::epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
     ++mvms;
-    R.apply_q(R.vec(R.L.Y), R.V(0));
-  } else {
-    R.apply_q(bin, R.V(0));
+    s_vec = sdst;
   }
-  mvms += q->deg;
+  if (right || !q) {
+    if (s_vec != R.V(0))
+      PPF_CUDA(cudaMemcpyAsync(R.V(0), s_vec, vb, cudaMemcpyDeviceToDevice, R.st));
+  } else {
+    R.apply_q(s_vec, R.V(0));
+    mvms += deg;
+  }
   R.normalise_start();
+  if (twopass) PPF_CUDA(cudaMemcpyAsync(R.vsrc(0), R.V(0), vb, cudaMemcpyDeviceToDevice, R.st));
+  const long long mvms_start = mvms;
 
   std::vector<zc> Hh, y, y_prev;
   double beta0 = 0.0;
@@ -541,15 +600,18 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   // Look-ahead: at a checkpoint the host waits for H while the first LOOKAHEAD
   // mat-vecs of the next step (which only read v_{j+1}) already run, so the
   // device does not idle during the D2H copy, f(H_m) and the relaunch.  If the
-  // run stops there, that work (<= LOOKAHEAD SpMVs) is discarded.
-  const int LOOKAHEAD = (o->stop == PPF_STOP_EST) ? 2 : 0;
+  // run stops there, that work (<= LOOKAHEAD SpMVs) is discarded.  Not with
+  // right preconditioning one-pass, whose checkpoint itself uses the device.
+  const int LOOKAHEAD = (o->stop == PPF_STOP_EST && !(right && !twopass)) ? 2 : 0;
+  // the basis the iterate is combined from: V_m, or Y_m (right, one-pass)
+  auto basis0 = [&]() -> const void* { return (right && !twopass) ? R.Yb(0) : R.V(0); };
   std::vector<Runner::Call> calls = R.record_step(0);
   size_t played = 0;
   for (int j = 0; j < m_max; ++j) {
     for (; played < calls.size(); ++played) R.play(calls[played]);
     R.orthogonalise(j, lanczos);
     m = j + 1;
-    mvms += 2 * q->deg + 1;
+    mvms += per_step;
     const bool check = (o->stop != PPF_STOP_FIXED_M) && (m % k == 0 || m == m_max);
     const bool more = j + 1 < m_max;
     if (!check) {
@@ -585,15 +647,39 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     y = dense_y(Hs, mb + 1, mb, beta0, lanczos);
     t_dense += std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
     if (!y_prev.empty()) {
-      std::vector<zc> dlt = y;
-      for (size_t i = 0; i < y_prev.size(); ++i) dlt[i] -= y_prev[i];
-      est = nrm(dlt) / nrm(y);
+      if (right && !twopass) {
+        // Y_m is not orthonormal: ||f_m - f_{m-k}|| / ||f_m|| from the iterates
+        // themselves: T0 = Y_m y_m, T1 = Y_m [y_{m-k}; 0]
+        std::vector<zc> yp(y.size(), zc(0.0, 0.0));
+        for (size_t i = 0; i < y_prev.size(); ++i) yp[i] = y_prev[i];
+        R.upload_y(y, R.L.ybuf, 0);
+        R.upload_y(yp, R.L.ybuf2, 1);
+        R.timed(2, double(vb) * (mb + 1), [&] {
+          launch_combine(R.dt, n, basis0(), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
+        });
+        R.timed(2, double(vb) * (mb + 1), [&] {
+          launch_combine(R.dt, n, basis0(), R.L.ldv, mb, R.vec(R.L.ybuf2), R.vec(R.L.T1), R.st);
+        });
+        R.timed(2, 2.0 * vb, [&] {
+          launch_diffnorm(R.dt, n, R.vec(R.L.T1), R.vec(R.L.T0), R.scal(S_ERR), R.rs, R.grid_vec,
+                          R.st);
+        });
+        R.reduce_fin(FIN_SQRT, 2, R.scal(S_ERR), nullptr, nullptr, nullptr);
+        double e2[2];
+        PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
+        PPF_CUDA(cudaStreamSynchronize(R.st));
+        est = e2[0] / e2[1];
+      } else {
+        std::vector<zc> dlt = y;
+        for (size_t i = 0; i < y_prev.size(); ++i) dlt[i] -= y_prev[i];
+        est = nrm(dlt) / nrm(y);
+      }
     }
     y_prev = y;
     if (o->stop == PPF_STOP_TRUE_ERR) {
       R.upload_y(y);
       R.timed(2, double(vb) * (mb + 1), [&] {
-        launch_combine(R.dt, n, R.V(0), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
+        launch_combine(R.dt, n, basis0(), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
       });
       R.timed(2, 2.0 * vb, [&] {
         launch_diffnorm(R.dt, n, R.vec(R.L.T0), o->x_ref, R.scal(S_ERR), R.rs, R.grid_vec, R.st);
@@ -604,7 +690,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
       PPF_CUDA(cudaStreamSynchronize(R.st));
       err = e2[0] / e2[1];
     }
-    if (o->record_history) ctx->hist.push_back({mb, est, err, mvms - (m - mb) * (2LL * q->deg + 1)});
+    if (o->record_history) ctx->hist.push_back({mb, est, err, mvms - (m - mb) * per_step});
     if (mb != m || hsub <= brt * beta0) {
       m = mb;
       term = PPF_BREAKDOWN;
@@ -639,12 +725,40 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     y = dense_y(Hh, m + 1, m, beta0, lanczos);
     t_dense += std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
   }
-  // line 11: f_m = V_m y_m
-  R.upload_y(y);
   void* xo = x_host ? R.vec(R.L.Y) : x;
-  R.timed(2, double(vb) * (m + 1), [&] {
-    launch_combine(R.dt, n, R.V(0), R.L.ldv, m, R.vec(R.L.ybuf), xo, R.st);
-  });
+  long long mv_total = mvms_start + (long long)m * per_step;
+  if (!twopass) {
+    // Alg 1 line 11 / Alg 2 line 11: f_m = V_m y_m or Y_m y_m
+    R.upload_y(y);
+    R.timed(2, double(vb) * (m + 1), [&] {
+      launch_combine(R.dt, n, basis0(), R.L.ldv, m, R.vec(R.L.ybuf), xo, R.st);
+    });
+  } else {
+    // two-pass, pass 2: regenerate v_2..v_m with the pass-1
+    // coefficients (host scalars, no inner products) and accumulate
+    // x~ = V_m y_m; right preconditioning: f_m = q(A) x~.
+    void* acc = R.vec(R.L.XA);  // (xo may be the left path's intermediate buffer L.Y)
+    auto alpha = [&](int jj) { return Hh[size_t(jj) + size_t(jj) * (m + 1)].real(); };
+    auto beta = [&](int jj) { return Hh[size_t(jj + 1) + size_t(jj) * (m + 1)].real(); };
+    PPF_CUDA(cudaMemcpyAsync(R.vsrc(0), R.V(0), vb, cudaMemcpyDeviceToDevice, R.st));
+    R.timed(2, 2.0 * vb, [&] { launch_scale(R.dt, n, R.V(0), acc, nullptr, y[0].real(), R.st); });
+    for (int j = 0; j + 1 < m; ++j) {
+      std::vector<Runner::Call> cs = R.record_step(j);
+      for (auto& c : cs) R.play(c);
+      R.timed(1, double(vb) * (j > 0 ? 6 : 5), [&] {
+        launch_lanczos_regen(R.dt, n, R.vdst(j), R.vsrc(j), R.vprv(j), alpha(j),
+                             j > 0 ? beta(j - 1) : 0.0, 1.0 / beta(j), y[size_t(j + 1)].real(), acc,
+                             R.st);
+      });
+    }
+    mv_total += (long long)(m - 1) * per_step;
+    if (right) {
+      R.apply_q(acc, xo);
+      mv_total += deg;
+    } else {
+      PPF_CUDA(cudaMemcpyAsync(xo, acc, vb, cudaMemcpyDeviceToDevice, R.st));
+    }
+  }
   if (x_host) {
     PPF_CUDA(cudaMemcpyAsync(x_host, xo, vb, cudaMemcpyDeviceToHost, R.st));
     PPF_CUDA(cudaStreamSynchronize(R.st));
@@ -670,12 +784,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   ctx->launches += R.launches;
   rep->iterations = m;
   rep->term = term;
-  rep->mvms = mvms - (o->func == PPF_SQRT ? 0 : 0);
-  {
-    // mvms counted per executed step; recompute for the returned m
-    long long mv = q->deg + (o->func == PPF_SQRT ? 1 : 0) + (long long)m * (2 * q->deg + 1);
-    rep->mvms = mv;
-  }
+  rep->mvms = mv_total;
   rep->inner_products = lanczos ? 2LL * m : (long long)m * m + 2LL * m;
   rep->est = est;
   rep->err = err;
@@ -710,9 +819,9 @@ extern "C" {
 ppf_status ppf_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, const ppf_poly* q,
                                const ppf_opts* o, size_t* bytes) {
   PPF_API_BEGIN
-  PPF_REQUIRE(ctx && A && q && bytes, "NULL argument");
+  PPF_REQUIRE(ctx && A && bytes, "NULL argument");
   check_opts(o);
-  *bytes = ws_layout(A->n_local, A->dtype, o->m_max, ctx->num_sms).total;
+  *bytes = ws_layout(A->n_local, A->dtype, o->m_max, ctx->num_sms, ws_shape(q, o)).total;
   PPF_API_END
 }
 

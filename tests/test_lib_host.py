@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
     assert not missing, missing
     # and the binding declares all of them
     assert names <= set(_lib.SIGNATURES), names - set(_lib.SIGNATURES)
-    assert lib.ppf_abi_version() == 1
+    assert lib.ppf_abi_version() == 2
 
 
 def test_no_batch_memcpy_in_sources():
