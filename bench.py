@@ -38,6 +38,8 @@ WORKLOAD = {
           "Ritz-Newton q deg 16, Arnoldi CGS2, f(z)=z^{-1/2}",
     "C2": "BASELINE configs[1]: 2D convection-diffusion 256^2, Chebyshev q, Arnoldi CGS2, sqrt",
     "C1": "BASELINE configs[0]: 2D Laplacian 32^2, Chebyshev deg 4, Lanczos",
+    "T1": "PAPER.md Table 1 workload (P:418-457): 3D Laplacian 100^3, Chebyshev q, Lanczos, "
+          "f(z)=z^{-1/2}, tol 1e-12 (context, not a BASELINE config)",
 }
 
 
@@ -50,6 +52,13 @@ def parse():
     p.add_argument("--config", default="C4")
     p.add_argument("--deg", type=int, default=None)
     p.add_argument("--fmt", default="sell64", choices=["sell32", "sell64", "csr"])
+    p.add_argument("--precond", default="left", choices=["left", "right"],
+                   help="Algorithm 1 (left) or 2 (right, PAPER.md:155-172)")
+    p.add_argument("--krylov", default=None, choices=["lanczos", "cgs2", "lanczos2p"],
+                   help="override the config's Krylov method (lanczos2p = two-pass)")
+    p.add_argument("--plain", action="store_true", help="no preconditioner (d = 1)")
+    p.add_argument("--check-every", type=int, default=1,
+                   help="k of the stopping check (PAPER.md:424 uses 64/d)")
     p.add_argument("--split", type=int, default=0,
                    help="warps per SELL slice (ppf_mat_set_split; 0 = automatic)")
     p.add_argument("--no-profile", action="store_true",
@@ -265,12 +274,15 @@ def main():
     torch.cuda.synchronize()
 
     def make_q():
+        if args.plain:
+            return None
         if cfg.poly == "chebyshev":
             return pp.Poly.chebyshev(*iv, deg)
         return pp.Poly.ritz_newton(ctx, M, bd, deg)
 
-    run_kw = dict(func=cfg.func, krylov=cfg.krylov, m_max=cfg.m_max, stop="est", tol=cfg.tol,
-                  check_every=1, record_history=False)
+    krylov_m = args.krylov or cfg.krylov
+    run_kw = dict(func=cfg.func, krylov=krylov_m, m_max=cfg.m_max, stop="est", tol=cfg.tol,
+                  check_every=args.check_every, record_history=False, precond=args.precond)
     q0 = make_q()
     opts = api.make_opts(**run_kw)
     work = pp.Workspace(ctx, M, q0, opts)
@@ -279,7 +291,8 @@ def main():
     def one_step():
         q = make_q()
         _, rep = pp.run(ctx, M, q, bd, x, work=work, **run_kw)
-        q.close()
+        if q is not None:
+            q.close()
         return rep
 
     with torch.cuda.stream(stream):
@@ -330,7 +343,7 @@ def main():
     bh = torch.from_numpy(b).pin_memory()
     xh = torch.empty_like(bh).pin_memory()
     e2e_times = []
-    ritz = cfg.poly != "chebyshev"
+    ritz = cfg.poly != "chebyshev" and not args.plain
     for i in range(max(2, min(args.steps, 3)) + 1):
         t0 = time.perf_counter()
         if ritz:  # the Ritz setup starts from b: it needs b on the device
@@ -339,7 +352,8 @@ def main():
             q = make_q()
         _, rep_h = pp.run_host(ctx, M, q, bh, xh, work=work, **run_kw)
         dt = time.perf_counter() - t0
-        q.close()
+        if q is not None:
+            q.close()
         if i > 0:
             e2e_times.append(dt)
     e2e = statistics.median(e2e_times)
@@ -368,9 +382,12 @@ def main():
         "scaling": "strong", "vs_baseline": None,
         "dtype": "c128" if cfg.complex_ else "f64",
         "data": "synthetic (seeded generators in inputs/; no dataset)",
-        "config": {"workload": WORKLOAD.get(name, name), "deg": deg, "format": args.fmt, "sell_split": split,
+        "config": {"workload": WORKLOAD.get(name, name), "deg": None if args.plain else deg,
+                   "precond": "none (plain, d = 1)" if args.plain else args.precond,
+                   "krylov": krylov_m, "check_every": args.check_every, "tol": cfg.tol,
+                   "format": args.fmt, "sell_split": split,
                    "m": m_iter, "mvms": reps[-1].mvms, "n": A.n, "nnz": A.nnz,
-                   "stored_entries": info["stored"], "stop": "estimate <= 1e-8, k = 1 (P:424)",
+                   "stored_entries": info["stored"], "stop": f"estimate <= {cfg.tol:g}, k = {args.check_every} (P:424)",
                    "l2": "inputs larger than L2 (matrix ~1.4 GB/126 MB L2), no flush",
                    "parallelism": f"row slabs x{world} (NCCL halo + allreduce)" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -206,7 +206,7 @@ void ppf_poly_destroy(ppf_poly* q);
  * opts.func / krylov / precond: see enums.  q == NULL selects the plain
  *   (unpreconditioned, d = 1) method: the Krylov space of A from s ("d = 1
  *   corresponds to an unpreconditioned method"); precond is then ignored.
- *   m_max >= 1 (<= 255).  stop:
+ *   m_max >= 1 (<= 1024).  stop:
  *   FIXED_M   run exactly m_max steps (unless breakdown);
  *   EST       stop at the first checkpoint m with the paper's estimate
  *             ||f_m - f_{m-k}|| / ||f_m|| <= tol, k = check_every.

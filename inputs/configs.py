@@ -42,6 +42,10 @@ CONFIGS = {
                  "chebyshev", 1e-8, 60, 104),
     "C5": Config("C5", "wilson", dict(L=16, m0=-1.0, link_seed=205), "invsqrt", (16,), "cgs2", "ritz",
                  1e-8, 30, 105),
+    # PAPER.md Table 1's own workload (§6.1): 3D Laplacian 100^3, tol 1e-12,
+    # right preconditioning, d = deg+1 in {1..64}, k = 64/d (context workload)
+    "T1": Config("T1", "laplacian", dict(N=100, dim=3), "invsqrt", (7,), "lanczos", "chebyshev",
+                 1e-12, 600, 100),
     # scaled-down members of the same families (oracle finishes in seconds)
     "C3s": Config("C3s", "laplacian", dict(N=30, dim=3), "invsqrt", (10, 20), "lanczos", "chebyshev",
                   1e-8, 80, 203),

@@ -110,7 +110,7 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
   for (auto& p : c->prof) p = {0, 0.0, 0.0};
   try {
     PPF_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-    c->h_pinned_bytes = size_t(258) * 256 * 16 + 16384;
+    c->h_pinned_bytes = size_t(66) * 65 * 16 + 2 * 2048;  // grown by ppf_run for larger m_max
     PPF_CUDA(cudaHostAlloc(&c->h_pinned, c->h_pinned_bytes, cudaHostAllocDefault));
     PPF_CUDA(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
     if (nranks > 1 && id128) {

@@ -19,17 +19,33 @@ namespace ppf {
 
 namespace {
 
+// sqrt(a^2 + b^2) without std::hypot's overflow/underflow guards (libm's
+// hypot costs ~40 ns, it dominated the QL sweep); the entries of H_m are
+// bounded by ||A q(A)^2|| (< 1e8 for every config), far from overflow
+inline double fhypot(double a, double b) { return std::sqrt(a * a + b * b); }
+
 inline bool on_branch_cut(zc z) {
   return std::abs(z.imag()) <= 1e-14 * std::max(std::abs(z), 1e-300) && z.real() <= 0.0;
 }
 
 }  // namespace
 
+// The eigenvector matrix is never formed: Z = R_1 R_2 ... R_K is a product of
+// plane rotations on adjacent columns (i, i+1).  Only e_1^T Z is needed for the
+// weights and Z w for the result, so row 0 of Z is tracked through the
+// rotations (O(1) each) and w is pushed back through the logged rotations in
+// reverse order: O(m^2) instead of O(m^3) (m = 576 at Table 1's d = 1).
 void tridiag_invsqrt_e1(int m, const double* dd, const double* ee, double beta0, double* y) {
   std::vector<double> d(dd, dd + m), e(m, 0.0);
   for (int i = 0; i + 1 < m; ++i) e[i] = ee[i];
-  std::vector<double> Z(size_t(m) * m, 0.0);  // column-major, Z(k, i) = Z[k + i*m]
-  for (int i = 0; i < m; ++i) Z[i + size_t(i) * m] = 1.0;
+  struct Rot {
+    int i;
+    double s, c;
+  };
+  std::vector<Rot> log;
+  log.reserve(size_t(8) * m);
+  std::vector<double> z0(m, 0.0);  // row 0 of Z
+  z0[0] = 1.0;
   const double eps = 2.220446049250313e-16;
   for (int l = 0; l < m; ++l) {
     int iter = 0;
@@ -42,7 +58,7 @@ void tridiag_invsqrt_e1(int m, const double* dd, const double* ee, double beta0,
       if (mm != l) {
         if (iter++ == 100) fail(PPF_EDENSE, "tridiagonal QL iteration did not converge");
         double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-        double r = std::hypot(g, 1.0);
+        double r = fhypot(g, 1.0);
         g = d[mm] - d[l] + e[l] / (g + std::copysign(r, g));
         double s = 1.0, c = 1.0, p = 0.0;
         int i;
@@ -50,7 +66,7 @@ void tridiag_invsqrt_e1(int m, const double* dd, const double* ee, double beta0,
         for (i = mm - 1; i >= l; --i) {
           double f = s * e[i];
           const double b = c * e[i];
-          r = std::hypot(f, g);
+          r = fhypot(f, g);
           e[i + 1] = r;
           if (r == 0.0) {
             d[i + 1] -= p;
@@ -65,13 +81,11 @@ void tridiag_invsqrt_e1(int m, const double* dd, const double* ee, double beta0,
           p = s * r;
           d[i + 1] = g + p;
           g = c * r - b;
-          for (int k = 0; k < m; ++k) {
-            double* zi = &Z[size_t(i) * m];
-            double* zi1 = &Z[size_t(i + 1) * m];
-            f = zi1[k];
-            zi1[k] = s * zi[k] + c * f;
-            zi[k] = c * zi[k] - s * f;
-          }
+          // Z <- Z R: Z[:, i+1] = s Z[:, i] + c Z[:, i+1], Z[:, i] = c Z[:, i] - s Z[:, i+1]
+          const double zi = z0[i], zi1 = z0[i + 1];
+          z0[i + 1] = s * zi + c * zi1;
+          z0[i] = c * zi - s * zi1;
+          log.push_back({i, s, c});
         }
         if (early) continue;
         d[l] -= p;
@@ -82,10 +96,13 @@ void tridiag_invsqrt_e1(int m, const double* dd, const double* ee, double beta0,
   }
   for (int i = 0; i < m; ++i)
     if (!(d[i] > 0.0)) fail(PPF_EBRANCH, "eigenvalue of T_m on (-inf, 0]");
-  for (int k = 0; k < m; ++k) y[k] = 0.0;
-  for (int i = 0; i < m; ++i) {
-    const double coef = beta0 * Z[size_t(i) * m] / std::sqrt(d[i]);
-    for (int k = 0; k < m; ++k) y[k] += Z[k + size_t(i) * m] * coef;
+  // y = beta0 Z diag(theta^{-1/2}) Z^T e_1 = Z w, w_i = beta0 z0_i / sqrt(theta_i)
+  for (int i = 0; i < m; ++i) y[i] = beta0 * z0[i] / std::sqrt(d[i]);
+  for (size_t t = log.size(); t-- > 0;) {
+    const Rot& R = log[t];
+    const double a = y[R.i], b = y[R.i + 1];
+    y[R.i] = R.c * a + R.s * b;
+    y[R.i + 1] = -R.s * a + R.c * b;
   }
 }
 

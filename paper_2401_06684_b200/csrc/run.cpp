@@ -196,7 +196,21 @@ struct Runner {
     grid_cgs = std::min(L.max_blocks, c->num_sms);  // persistent CGS kernel: one CTA per SM
     PPF_CUDA(cudaMemsetAsync(w + L.counter, 0, 256, st));
     PPF_CUDA(cudaMemsetAsync(w + L.H, 0, size_t(L.ldh) * (m_max + 1) * sc, st));
+    // pinned host staging: H (and beta0), then two coefficient-vector slots;
+    // grown on demand (the context keeps the largest)
+    stage_h = al256(size_t(L.ldh) * (m_max + 1) * sc + 64);
+    stage_y = al256(size_t(m_max + 2) * 16);
+    const size_t need = stage_h + 2 * stage_y;
+    if (ctx->h_pinned_bytes < need) {
+      PPF_CUDA(cudaStreamSynchronize(st));
+      PPF_CUDA(cudaFreeHost(ctx->h_pinned));
+      ctx->h_pinned = nullptr;
+      ctx->h_pinned_bytes = 0;
+      PPF_CUDA(cudaHostAlloc(&ctx->h_pinned, need, cudaHostAllocDefault));
+      ctx->h_pinned_bytes = need;
+    }
   }
+  size_t stage_h = 0, stage_y = 0;
 
   void* V(int j) { return w + L.V + size_t(j) * al256(size_t(L.ldv) * sc); }
   void* Yb(int j) { return w + L.Yb + size_t(j) * al256(size_t(L.ldv) * sc); }
@@ -467,7 +481,6 @@ struct Runner {
   void fetch_H_async(int cols) {
     char* hp = static_cast<char*>(ctx->h_pinned);
     const size_t bytes = size_t(L.ldh) * cols * sc;
-    if (bytes + 64 > ctx->h_pinned_bytes - 8192) fail(PPF_EINVAL, "m_max too large for staging buffer");
     PPF_CUDA(cudaMemcpyAsync(hp, w + L.H, bytes, cudaMemcpyDeviceToHost, st));
     PPF_CUDA(cudaMemcpyAsync(hp + bytes, scal(S_BETA0), 8, cudaMemcpyDeviceToHost, st));
     PPF_CUDA(cudaEventRecord(ctx->ev, st));
@@ -491,14 +504,14 @@ struct Runner {
 
   void upload_y(const std::vector<zc>& y, size_t dst_off = size_t(-1), int slot = 0) {
     if (dst_off == size_t(-1)) dst_off = L.ybuf;
-    char* hp = static_cast<char*>(ctx->h_pinned) + ctx->h_pinned_bytes - 8192 + slot * 4096;
+    char* hp = static_cast<char*>(ctx->h_pinned) + stage_h + slot * stage_y;
     double* d = reinterpret_cast<double*>(hp);
     const int nd = int(sc / 8);
     for (size_t i = 0; i < y.size(); ++i) {
       d[i * nd] = y[i].real();
       if (nd == 2) d[i * nd + 1] = y[i].imag();
     }
-    if (y.size() * sc > 4096) fail(PPF_EINVAL, "m too large for the coefficient staging buffer");
+    if (y.size() * sc > stage_y) fail(PPF_EINVAL, "m too large for the coefficient staging buffer");
     PPF_CUDA(cudaMemcpyAsync(w + dst_off, hp, y.size() * sc, cudaMemcpyHostToDevice, st));
   }
 };
@@ -534,7 +547,7 @@ void check_opts(const ppf_opts* o) {
                   o->krylov == PPF_LANCZOS_2PASS,
               "bad krylov");
   PPF_REQUIRE(o->precond == PPF_PREC_LEFT || o->precond == PPF_PREC_RIGHT, "bad precond");
-  PPF_REQUIRE(o->m_max >= 1 && o->m_max <= 255, "m_max out of range [1, 255]");
+  PPF_REQUIRE(o->m_max >= 1 && o->m_max <= 1024, "m_max out of range [1, 1024]");
   PPF_REQUIRE(o->stop >= 0 && o->stop <= 2, "bad stop");
   PPF_REQUIRE(o->stop == PPF_STOP_FIXED_M || o->tol > 0.0, "tol must be > 0");
   PPF_REQUIRE(o->check_every >= 1 || o->stop == PPF_STOP_FIXED_M, "check_every >= 1");
