@@ -180,22 +180,39 @@ def haar_su3(rng: np.random.Generator, count: int) -> np.ndarray:
     return Q
 
 
-def wilson_dirac(L: int, m0: float, seed: int | None = None, links: np.ndarray | None = None) -> CSR:
+def wilson_dirac(L: int, m0: float, seed: int | None = None, links: np.ndarray | None = None,
+                 mu: float = 0.0) -> CSR:
     """Wilson-Dirac matrix on a periodic L^4 lattice (12 dof/site, 49 nnz/row).
 
     ``links`` has shape (4, L^4, 3, 3); if None, Haar SU(3) links are drawn from
     ``seed`` in (μ, site) order.  ``links = identity`` gives the free operator.
-    Requires L >= 3 so that the +μ and -μ neighbours are distinct sites.
+    ``mu`` is a chemical potential: the forward time hop
+    (direction 4) carries e^{mu}, the backward one e^{-mu}, which makes
+    Γ5 D non-Hermitian.  Requires L >= 3 so that the +μ and -μ neighbours are
+    distinct sites.
     """
     assert L >= 3
     V = L ** 4
     if links is None:
         rng = np.random.default_rng(seed)
         links = haar_su3(rng, 4 * V).reshape(4, V, 3, 3)
-    return _wilson_assemble(L, m0, links)
+    return _wilson_assemble(L, m0, links, mu)
 
 
-def _wilson_assemble(L: int, m0: float, links: np.ndarray) -> CSR:
+def overlap_kernel(L: int, m_w: float, mu: float = 0.0, seed: int | None = None,
+                   links: np.ndarray | None = None) -> CSR:
+    """Q = Γ5 D_w(m_w, mu), the argument of the sign function in the overlap
+    operator D_ov = I + ρ Γ5 sign(Q).  Γ5 = γ1γ2γ3γ4 =
+    diag(1, 1, -1, -1) on the spins in this chiral basis (the identity on spins
+    1, 2 and minus the identity on spins 3, 4): rows of spin 3, 4
+    of D_w are negated.  Hermitian for mu = 0."""
+    D = wilson_dirac(L, m_w, seed=seed, links=links, mu=mu)
+    rows = np.repeat(np.arange(D.n), np.diff(D.row_ptr))
+    sign = np.where(((rows % 12) // 3) >= 2, -1.0, 1.0)
+    return CSR(D.n, D.row_ptr.copy(), D.col.copy(), D.val * sign)
+
+
+def _wilson_assemble(L: int, m0: float, links: np.ndarray, mu_c: float = 0.0) -> CSR:
     V = L ** 4
     site = np.arange(V, dtype=np.int64)
     coord = [(site // L ** k) % L for k in range(4)]
@@ -218,10 +235,11 @@ def _wilson_assemble(L: int, m0: float, links: np.ndarray) -> CSR:
         for mu in range(4):
             fwd = shift(mu, +1)
             bwd = shift(mu, -1)
-            for nb, P, Cm in ((fwd, I4 - g[mu], links[mu]),
-                              (bwd, I4 + g[mu], np.conj(np.swapaxes(links[mu][bwd], 1, 2)))):
+            ef, eb = (np.exp(mu_c), np.exp(-mu_c)) if mu == 3 else (1.0, 1.0)
+            for nb, P, Cm, ex in ((fwd, I4 - g[mu], links[mu], ef),
+                                  (bwd, I4 + g[mu], np.conj(np.swapaxes(links[mu][bwd], 1, 2)), eb)):
                 for sp in np.nonzero(P[s])[0]:
-                    coef = -0.5 * P[s, sp]
+                    coef = -0.5 * P[s, sp] * ex
                     for b in range(3):
                         cols[:, s, :, e] = (12 * nb + 3 * sp + b)[:, None]
                         vals[:, s, :, e] = coef * Cm[:, :, b]

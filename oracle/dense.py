@@ -47,3 +47,18 @@ def invsqrt_dense(A: np.ndarray) -> np.ndarray:
     lam, X = np.linalg.eig(A)
     _check_branch(lam)
     return X @ np.diag(lam.astype(np.complex128) ** -0.5) @ np.linalg.inv(X)
+
+
+def sign_dense(Q: np.ndarray) -> np.ndarray:
+    """sign(Q) = X diag(sign(Re λ)) X^{-1} from the eigendecomposition
+    (Higham, Functions of Matrices, §5; the definition behind),
+    requiring no eigenvalue on the imaginary axis; Hermitian Q uses eigh."""
+    if np.allclose(Q, Q.conj().T, rtol=0, atol=1e-14 * np.abs(Q).max()):
+        lam, X = np.linalg.eigh(Q)
+        if np.any(lam == 0):
+            raise ValueError("eigenvalue on the imaginary axis")
+        return (X * np.sign(lam)) @ X.conj().T
+    lam, X = np.linalg.eig(Q)
+    if np.any(np.abs(lam.real) <= 1e-14 * np.abs(lam).max()):
+        raise ValueError("eigenvalue on the imaginary axis")
+    return (X * np.sign(lam.real)) @ np.linalg.inv(X)

@@ -38,6 +38,7 @@ import numpy as np
 
 from . import chebyshev, newton
 from .dense import invsqrt_e1
+from .spmv import SquaredOperator
 
 
 @dataclass
@@ -256,6 +257,18 @@ def run_two_pass(op, b: np.ndarray, q, *, func: str = "invsqrt", precond: str = 
         x = apply_q(q, op, x)                                       # f_m = q(A) V_m y_m
     return Result(x=x, m=m, H=H, beta0=beta0, y=y, term=term, mvms=op.mvms - mv0,
                   inner_products=ips, history=hist)
+
+
+def run_sign(op, b: np.ndarray, q, *, krylov: str = "cgs2", **kw) -> Result:
+    """sign(Q) b = Q (Q^2)^{-1/2} b: Algorithm 1 (or 2) for
+    the inverse square root of A = Q^2, applied as two mat-vecs with Q per
+    application (2 mvms each, Table 2's unit), then one more mat-vec with Q.
+    q approximates z^{-1/2} on spec(Q^2) (e.g. Ritz values of Q^2)."""
+    res = run(SquaredOperator(op), b, q, func="invsqrt", krylov=krylov, **kw)
+    res.x_invsqrt_sq = res.x
+    res.x = op.matvec(res.x)
+    res.mvms += 1
+    return res
 
 
 def find_m_star(op, b, q, *, func, krylov, m_max, tol, x_ref) -> Result:

@@ -51,3 +51,23 @@ class Operator:
         return y
 
     __matmul__ = matvec
+
+
+class SquaredOperator:
+    """A = Q^2 applied as two consecutive mat-vecs with Q ("we
+    rather compute A^2 x for a given vector x as two consecutive mvms"); each
+    application counts 2 mvms, the unit of Table 2."""
+
+    def __init__(self, op: Operator):
+        self.op = op
+        self.n = op.n
+        self.dtype = op.dtype
+
+    @property
+    def mvms(self) -> int:
+        return self.op.mvms
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        return self.op.matvec(self.op.matvec(x))
+
+    __matmul__ = matvec

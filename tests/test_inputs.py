@@ -86,3 +86,17 @@ def test_wilson_structure_gamma5():
     assert np.linalg.norm(H, 2) <= 4.0 + 1e-10
     # field of values in C+ for m0 = -1 at this seed: λ_min((D + D^*)/2) > 0
     assert np.linalg.eigvalsh((S + S.conj().T) / 2).min() > 0
+
+
+def test_overlap_kernel_conventions():
+    """Q = Γ5 D_w: Γ5 = diag(1,1,-1,-1) on the spins
+    (P:467); Q is Hermitian at mu = 0 (γ5-hermiticity of D_w) and
+    Q(mu)^H = Q(-mu) with the chemical potential on the time links."""
+    g5 = ops.gamma5()
+    assert np.allclose(g5, np.diag([1, 1, -1, -1]))
+    Q0 = ops.overlap_kernel(3, -1.4, 0.0, seed=2).to_scipy()
+    assert abs(Q0 - Q0.conj().T).max() < 1e-14
+    Qp = ops.overlap_kernel(3, -1.4, 0.3, seed=2).to_scipy()
+    Qm = ops.overlap_kernel(3, -1.4, -0.3, seed=2).to_scipy()
+    assert abs(Qp - Qp.conj().T).max() > 0.1
+    assert abs(Qp.conj().T - Qm).max() < 1e-14

@@ -256,3 +256,30 @@ def test_right_preconditioning_nonhermitian_closed_form():
     left = krylov.run(op, b, q, func="sqrt", krylov="cgs2", m_max=120, stop="true", tol=1e-9,
                       x_ref=xr)
     assert abs(res.m - left.m) <= 2
+
+
+@pytest.mark.parametrize("mu", [0.0, 0.3])
+def test_sign_function_overlap_kernel_dense(mu):
+    """sign(Q)b = Q (Q^2)^{-1/2} b for Q = Γ5 D_w(m_w = -1.4, mu)
+    (Haar links on 3^4): the preconditioned Arnoldi result
+    (Ritz-Newton q of Q^2) against the dense sign from the
+    eigendecomposition, and the invariant sign(Q)^2 = I applied twice."""
+    Qm = ops.overlap_kernel(3, -1.4, mu, seed=31)
+    op = Operator(Qm.to_scipy())
+    rng = np.random.default_rng(4)
+    b = rng.standard_normal(Qm.n) + 1j * rng.standard_normal(Qm.n)
+    S = dense.sign_dense(Qm.to_scipy().toarray())
+    ref = S @ b
+    from oracle.spmv import SquaredOperator
+    q, _, _ = newton.ritz_newton(SquaredOperator(op), b, 7)
+    res = krylov.run_sign(op, b, q, m_max=120, stop="est", tol=1e-12)
+    assert res.term == "converged"
+    assert np.linalg.norm(res.x - ref) <= 1e-9 * np.linalg.norm(ref)
+    # (Q^2)^{-1/2} b itself
+    inv = np.linalg.solve(Qm.to_scipy().toarray(), ref)          # Q^{-1} sign(Q) b
+    assert np.linalg.norm(res.x_invsqrt_sq - inv) <= 1e-9 * np.linalg.norm(inv)
+    twice = krylov.run_sign(op, res.x, q, m_max=120, stop="est", tol=1e-12).x
+    assert np.linalg.norm(twice - b) <= 1e-8 * np.linalg.norm(b)
+    # mvm unit of Table 2 (PAPER.md:495-505): 2 per application of Q^2
+    per = 2 * (2 * q.deg + 1)
+    assert res.mvms == 2 * q.deg + res.m * per + 1
