@@ -38,6 +38,9 @@ WORKLOAD = {
           "Ritz-Newton q deg 16, Arnoldi CGS2, f(z)=z^{-1/2}",
     "C2": "BASELINE configs[1]: 2D convection-diffusion 256^2, Chebyshev q, Arnoldi CGS2, sqrt",
     "C1": "BASELINE configs[0]: 2D Laplacian 32^2, Chebyshev deg 4, Lanczos",
+    "C6": "PAPER.md §6.2 application (P:459-510): sign(Q)b = Q (Q^2)^{-1/2} b for the overlap kernel "
+          "Q = Γ5 D_w(m_w=-1.4, mu=0.3) on a 16^4 Haar lattice (n=786,432) complex128, Q^2 as two SpMVs, "
+          "Ritz-Newton q of Q^2 deg 15 (d=16), Arnoldi CGS2 (context, not a BASELINE config)",
     "T1": "PAPER.md Table 1 workload (P:418-457): 3D Laplacian 100^3, Chebyshev q, Lanczos, "
           "f(z)=z^{-1/2}, tol 1e-12 (context, not a BASELINE config)",
 }
@@ -161,12 +164,17 @@ def cpu_baseline(cfg, A, b, iv, deg, m, mvms_total):
     from oracle.spmv import Operator
     op = Operator(A.to_scipy())
     t0 = time.perf_counter()
+    sq = cfg.func in ("sign", "invsqrt_sq")
     if cfg.poly == "chebyshev":
         q = chebyshev.coefficients(*iv, deg)
         setup_mvms = 0
     else:
-        q, setup_mvms, _ = newton.ritz_newton(op, b, deg)
-    res = krylov.run(op, b, q, func=cfg.func, krylov=cfg.krylov, m_max=1, stop="fixed")
+        from oracle.spmv import SquaredOperator
+        q, setup_mvms, _ = newton.ritz_newton(SquaredOperator(op) if sq else op, b, deg)
+    if sq:
+        res = krylov.run_sign(op, b, q, krylov=cfg.krylov, m_max=1, stop="fixed")
+    else:
+        res = krylov.run(op, b, q, func=cfg.func, krylov=cfg.krylov, m_max=1, stop="fixed")
     t1 = time.perf_counter() - t0
     mv1 = res.mvms + setup_mvms
     per_mvm = t1 / mv1
@@ -188,10 +196,11 @@ def run_reference(args):
     name = args.config
     cfg, A, b, iv = setup_inputs(name)
     deg = args.deg if args.deg is not None else cfg.degs[0]
-    m_assumed = {"C4": 25, "C3": 27, "C5": 3, "C2": 76, "C1": 20}.get(name, 20)
-    mvms_total = deg + (1 if cfg.func == "sqrt" else 0) + m_assumed * (2 * deg + 1)
+    m_assumed = {"C4": 25, "C3": 27, "C5": 3, "C2": 76, "C1": 20, "C6": 10}.get(name, 20)
+    pw = 2 if cfg.func in ("sign", "invsqrt_sq") else 1     # Q^2 = two mvms
+    mvms_total = pw * deg + (1 if cfg.func in ("sqrt", "sign") else 0) + m_assumed * pw * (2 * deg + 1)
     if cfg.poly == "ritz":
-        mvms_total += deg + 1
+        mvms_total += pw * (deg + 1)
     vals = []
     base = None
     for i in range(args.warmup + args.steps):
@@ -278,9 +287,10 @@ def main():
             return None
         if cfg.poly == "chebyshev":
             return pp.Poly.chebyshev(*iv, deg)
-        return pp.Poly.ritz_newton(ctx, M, bd, deg)
+        return pp.Poly.ritz_newton(ctx, M, bd, deg, power=power)
 
     krylov_m = args.krylov or cfg.krylov
+    power = 2 if cfg.func in ("sign", "invsqrt_sq") else 1
     run_kw = dict(func=cfg.func, krylov=krylov_m, m_max=cfg.m_max, stop="est", tol=cfg.tol,
                   check_every=args.check_every, record_history=False, precond=args.precond)
     q0 = make_q()
@@ -347,7 +357,7 @@ def main():
     for i in range(max(2, min(args.steps, 3)) + 1):
         t0 = time.perf_counter()
         if ritz:  # the Ritz setup starts from b: it needs b on the device
-            q = pp.Poly.ritz_newton(ctx, M, bh.to("cuda", non_blocking=True), deg)
+            q = pp.Poly.ritz_newton(ctx, M, bh.to("cuda", non_blocking=True), deg, power=power)
         else:
             q = make_q()
         _, rep_h = pp.run_host(ctx, M, q, bh, xh, work=work, **run_kw)

@@ -57,7 +57,13 @@ typedef enum {
 } ppf_status;
 
 typedef enum { PPF_R64 = 0, PPF_C128 = 1 } ppf_dtype;
-typedef enum { PPF_INVSQRT = 0, PPF_SQRT = 1 } ppf_func;            /* SQRT = A^{-1/2}(A b) */
+typedef enum {
+  PPF_INVSQRT = 0,     /* A^{-1/2} b */
+  PPF_SQRT = 1,        /* A^{1/2} b = A^{-1/2}(A b) */
+  PPF_INVSQRT_SQ = 2,  /* (A^2)^{-1/2} b: the Krylov operator is A^2, applied as two mat-vecs
+                          with the given A; q approximates z^{-1/2} on spec(A^2) */
+  PPF_SIGN = 3         /* sign(A) b = A (A^2)^{-1/2} b */
+} ppf_func;
 typedef enum {
   PPF_LANCZOS = 0,        /* Hermitian A: three-term recurrence, all basis vectors kept (reading Q8) */
   PPF_ARNOLDI_CGS2 = 1,   /* general A: classical Gram-Schmidt with one reorthogonalisation */
@@ -187,6 +193,10 @@ ppf_status ppf_poly_chebyshev(double a, double b, int deg, ppf_poly** out);
 ppf_status ppf_ritz_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, int deg, size_t* bytes);
 ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
                                 void* work, size_t work_bytes, ppf_poly** out);
+/* The same for the Ritz values of A^power (power 1 or 2; power 2 = the operator
+ * of PPF_INVSQRT_SQ / PPF_SIGN, two mat-vecs per Arnoldi step). */
+ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
+                                    int power, void* work, size_t work_bytes, ppf_poly** out);
 ppf_status ppf_poly_import(int kind, int deg, const double* ab, const void* coef,
                            const void* nodes, ppf_poly** out);
 ppf_status ppf_poly_export(const ppf_poly* q, int* kind, int* deg, double* ab,
@@ -215,7 +225,8 @@ void ppf_poly_destroy(ppf_poly* q);
  *             (Y_m is not orthonormal).  Right, two-pass: the
  *             coefficient difference is used as a proxy (DESIGN.md readings);
  *   TRUE_ERR  stop at the first checkpoint with ||f_m - x_ref|| / ||x_ref|| <= tol
- *             (x_ref device, n_local entries; for calibrating m*, reading Q11);
+ *             (x_ref device, n_local entries; for calibrating m*, reading Q11;
+ *             for PPF_SIGN f_m is the (A^2)^{-1/2} b iterate, before the final A);
  *             not available with PPF_LANCZOS_2PASS (PPF_EINVAL).
  * ppf_workspace_bytes: device scratch `work` needed by ppf_run for these
  *   (A, q, opts); it holds V (m_max+1 columns; 4 for PPF_LANCZOS_2PASS), Y
@@ -246,7 +257,9 @@ typedef struct {
 typedef struct {
   int iterations;              /* m of the returned f_m */
   int term;                    /* ppf_term */
-  long long mvms;              /* products with A (P:455 unit), incl. c = q(A)s, A b */
+  long long mvms;              /* products with A (P:455 unit), incl. c = q(A)s, A b; for
+                                  PPF_INVSQRT_SQ / PPF_SIGN 2 per application of A^2 (Table 2's
+                                  unit) plus 1 for the final A f (SIGN) */
   long long inner_products;     /* norms included, ||c|| not */
   double est;                  /* last estimate (NaN if none) */
   double err;                  /* last true error (NaN unless TRUE_ERR) */

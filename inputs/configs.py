@@ -16,9 +16,10 @@ from .vectors import gaussian_vector
 @dataclass(frozen=True)
 class Config:
     name: str
-    family: str                  # "laplacian" | "convdiff" | "wilson"
+    family: str                  # "laplacian" | "convdiff" | "wilson" | "overlap"
     params: dict = field(default_factory=dict)
-    func: str = "invsqrt"        # "invsqrt" | "sqrt"   (sqrt = A^{-1/2}(Ab))
+    func: str = "invsqrt"        # "invsqrt" | "sqrt" (= A^{-1/2}(Ab)) | "sign"
+                                 # (= Q (Q^2)^{-1/2} b)
     degs: tuple = (4,)           # degree of q (deg = d-1 in the paper's notation, reading Q1)
     krylov: str = "lanczos"      # "lanczos" | "cgs2"
     poly: str = "chebyshev"      # "chebyshev" | "ritz"
@@ -28,7 +29,7 @@ class Config:
 
     @property
     def complex_(self) -> bool:
-        return self.family == "wilson"
+        return self.family in ("wilson", "overlap")
 
 
 CONFIGS = {
@@ -42,6 +43,12 @@ CONFIGS = {
                  "chebyshev", 1e-8, 60, 104),
     "C5": Config("C5", "wilson", dict(L=16, m0=-1.0, link_seed=205), "invsqrt", (16,), "cgs2", "ritz",
                  1e-8, 30, 105),
+    # the paper's headline application (§6.2): sign(Q)b for the
+    # overlap kernel Q = Γ5 D_w(m_w = -1.4, mu = 0.3) (P:473 values) on a 16^4 Haar
+    # lattice (the SFB-TRR55 ensemble is not available), Ritz-Newton q of Q^2
+    # (P:475), d = 16 (Table 2 row), Arnoldi CGS2 (context workload, not a BASELINE config)
+    "C6": Config("C6", "overlap", dict(L=16, m_w=-1.4, mu=0.3, link_seed=206), "sign", (15,),
+                 "cgs2", "ritz", 1e-8, 60, 106),
     # PAPER.md Table 1's own workload (§6.1): 3D Laplacian 100^3, tol 1e-12,
     # right preconditioning, d = deg+1 in {1..64}, k = 64/d (context workload)
     "T1": Config("T1", "laplacian", dict(N=100, dim=3), "invsqrt", (7,), "lanczos", "chebyshev",
@@ -51,6 +58,8 @@ CONFIGS = {
                   1e-8, 80, 203),
     "C4s": Config("C4s", "convdiff", dict(N=32, dim=3, beta=(10.0, 10.0, 10.0)), "sqrt", (20, 5), "cgs2",
                   "chebyshev", 1e-8, 60, 204),
+    "C6s": Config("C6s", "overlap", dict(L=4, m_w=-1.4, mu=0.3, link_seed=306), "sign", (15, 7),
+                  "cgs2", "ritz", 1e-8, 60, 206),
     "C5s": Config("C5s", "wilson", dict(L=4, m0=-1.0, link_seed=305), "invsqrt", (16, 4), "cgs2", "ritz",
                   1e-8, 30, 205),
 }
@@ -65,6 +74,8 @@ def operator(cfg: Config):
                 ops.convdiff_interval(p["N"], p["dim"], p["beta"]))
     if cfg.family == "wilson":
         return ops.wilson_dirac(p["L"], p["m0"], seed=p["link_seed"]), None
+    if cfg.family == "overlap":
+        return ops.overlap_kernel(p["L"], p["m_w"], p["mu"], seed=p["link_seed"]), None
     raise ValueError(cfg.family)
 
 

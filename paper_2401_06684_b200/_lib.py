@@ -15,7 +15,7 @@ PPF_OK = 0
 STATUS = {0: "PPF_OK", 1: "PPF_EINVAL", 2: "PPF_ECUDA", 3: "PPF_ENCCL", 4: "PPF_EWORKSPACE",
           5: "PPF_EBRANCH", 6: "PPF_EDENSE", 7: "PPF_ESTATE"}
 R64, C128 = 0, 1
-INVSQRT, SQRT = 0, 1
+INVSQRT, SQRT, INVSQRT_SQ, SIGN = 0, 1, 2, 3
 LANCZOS, ARNOLDI_CGS2, LANCZOS_2PASS = 0, 1, 2
 PREC_LEFT, PREC_RIGHT = 0, 1
 STOP_FIXED_M, STOP_EST, STOP_TRUE_ERR = 0, 1, 2
@@ -68,6 +68,8 @@ SIGNATURES = {
     "ppf_poly_chebyshev": (C.c_int, [C.c_double, C.c_double, C.c_int, C.POINTER(vp)]),
     "ppf_ritz_workspace_bytes": (C.c_int, [vp, vp, C.c_int, C.POINTER(C.c_size_t)]),
     "ppf_poly_ritz_newton": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_size_t, C.POINTER(vp)]),
+    "ppf_poly_ritz_newton_pow": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp, C.c_size_t,
+                                           C.POINTER(vp)]),
     "ppf_poly_import": (C.c_int, [C.c_int, C.c_int, dblp, vp, vp, C.POINTER(vp)]),
     "ppf_poly_export": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), dblp, vp, vp]),
     "ppf_poly_eval": (C.c_int, [vp, C.c_int, dblp, dblp]),

@@ -189,15 +189,17 @@ class Poly:
         return cls(h)
 
     @classmethod
-    def ritz_newton(cls, ctx: Context, A: Matrix, start, deg: int) -> "Poly":
-        """Ritz values of deg+1 device Arnoldi steps from ``start``."""
+    def ritz_newton(cls, ctx: Context, A: Matrix, start, deg: int, power: int = 1) -> "Poly":
+        """Ritz values of deg+1 device Arnoldi steps with A^power
+        (power 2: the operator of func "invsqrt_sq" / "sign") from ``start``."""
         torch = _torch()
         nb = C.c_size_t()
         check(_lib().ppf_ritz_workspace_bytes(ctx.h, A.h, deg, C.byref(nb)))
         work = torch.empty(nb.value, dtype=torch.uint8, device=start.device)
         h = C.c_void_p()
-        check(_lib().ppf_poly_ritz_newton(ctx.h, A.h, C.c_void_p(start.data_ptr()), deg,
-                                          C.c_void_p(work.data_ptr()), nb.value, C.byref(h)))
+        check(_lib().ppf_poly_ritz_newton_pow(ctx.h, A.h, C.c_void_p(start.data_ptr()), deg,
+                                              int(power), C.c_void_p(work.data_ptr()), nb.value,
+                                              C.byref(h)))
         return cls(h)
 
     @classmethod
@@ -282,7 +284,7 @@ class RunReport:
 
 
 _TERM = {L.CONVERGED: "converged", L.MAX_ITER: "max_iter", L.BREAKDOWN: "breakdown"}
-_FUNC = {"invsqrt": L.INVSQRT, "sqrt": L.SQRT}
+_FUNC = {"invsqrt": L.INVSQRT, "sqrt": L.SQRT, "invsqrt_sq": L.INVSQRT_SQ, "sign": L.SIGN}
 _KRY = {"lanczos": L.LANCZOS, "cgs2": L.ARNOLDI_CGS2, "lanczos2p": L.LANCZOS_2PASS}
 _PREC = {"left": L.PREC_LEFT, "right": L.PREC_RIGHT}
 _STOP = {"fixed": L.STOP_FIXED_M, "est": L.STOP_EST, "true": L.STOP_TRUE_ERR}

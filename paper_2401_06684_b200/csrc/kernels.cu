@@ -25,9 +25,10 @@ template <typename T> struct EpiT {
   T s_ax, s_x, s_z, s_u;
   const T* z;
   const T* u;
+  const T* xe;  // vector of the s_x term: the SpMV input, or Epi::xe (squared operator)
 };
 
-template <typename T> EpiT<T> to_epi(const Epi& e) {
+template <typename T> EpiT<T> to_epi(const Epi& e, const void* x) {
   EpiT<T> r;
   r.s_ax = s_from<T>(e.s_ax[0], e.s_ax[1]);
   r.s_x = s_from<T>(e.s_x[0], e.s_x[1]);
@@ -35,6 +36,7 @@ template <typename T> EpiT<T> to_epi(const Epi& e) {
   r.s_u = s_from<T>(e.s_u[0], e.s_u[1]);
   r.z = static_cast<const T*>(e.z);
   r.u = static_cast<const T*>(e.u);
+  r.xe = static_cast<const T*>(e.xe ? e.xe : x);
   return r;
 }
 
@@ -83,7 +85,7 @@ template <typename T>
 __device__ __forceinline__ T epilogue(const EpiT<T>& e, T ax, const T* __restrict__ x, int64_t row,
                                       bool has_x) {
   T r = s_mul(e.s_ax, ax);
-  if (has_x) r = s_fma(e.s_x, ldg(x + row), r);
+  if (has_x) r = s_fma(e.s_x, ldg(e.xe + row), r);
   if (e.z) r = s_fma(e.s_z, ldg(e.z + row), r);
   if (e.u) r = s_fma(e.s_u, ldg(e.u + row), r);
   return r;
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
     r.x = e.s_ax * a0;
     r.y = e.s_ax * a1;
     if (has_x) {
-      const double2 xv = __ldg(reinterpret_cast<const double2*>(x + r0));
+      const double2 xv = __ldg(reinterpret_cast<const double2*>(e.xe + r0));
       r.x = fma(e.s_x, xv.x, r.x);
       r.y = fma(e.s_x, xv.y, r.y);
     }
@@ -841,7 +843,7 @@ void post_launch(const char* what) { cuda_check(cudaGetLastError(), what); }
 // ---------------------------------------------------------------------------
 template <typename T>
 static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st) {
-  const EpiT<T> et = to_epi<T>(e);
+  const EpiT<T> et = to_epi<T>(e, x);
   const bool has_x = (e.s_x[0] != 0.0 || e.s_x[1] != 0.0);
   const T* xt = static_cast<const T*>(x);
   T* ot = static_cast<T*>(out);

@@ -221,10 +221,11 @@ std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& nodes);
 // ---------------------------------------------------------------------------
 // Device kernels (kernels.cu): host-side launchers
 // ---------------------------------------------------------------------------
-struct Epi {          // out = s_ax*(A x) + s_x*x + s_z*z + s_u*u
+struct Epi {          // out = s_ax*(A x) + s_x*xe + s_z*z + s_u*u
   double s_ax[2], s_x[2], s_z[2], s_u[2];
   const void* z;      // may be null (s_z ignored)
   const void* u;      // may be null (s_u ignored)
+  const void* xe = nullptr;  // null: xe = x (the SpMV input); set for A = Q^2 chains
 };
 
 int auto_sell_ks(const ppf_mat* m, int num_sms);

@@ -28,14 +28,15 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Workspace shape: which bases the run keeps.
 enum { WS_RIGHT = 1,     // right preconditioning, one-pass: Y_m (m_max columns)
-       WS_TWOPASS = 2 }; // two-pass Lanczos: V = {v_1, ring of 3}, + accumulator XA
+       WS_TWOPASS = 2,   // two-pass Lanczos: V = {v_1, ring of 3}, + accumulator XA
+       WS_SQUARE = 4 };  // operator A = Q^2: + the intermediate Q x (TSQ)
 
 struct WsLayout {
   int64_t ldv;       // leading dimension of V and vector length (padded)
   int ldh;           // leading dimension of H
   int vcols;         // columns of V
-  size_t V, Yb, U, Y, T0, T1, T2, XA, H, hbuf, gbuf, ybuf, ybuf2, scal, partials, counter, raw,
-      total;
+  size_t V, Yb, U, Y, T0, T1, T2, XA, TSQ, H, hbuf, gbuf, ybuf, ybuf2, scal, partials, counter,
+      raw, total;
   int max_blocks;
   int max_vals;
 };
@@ -66,6 +67,8 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms, int shape = 
   o += vec;
   L.XA = o;
   if (shape & WS_TWOPASS) o += vec;
+  L.TSQ = o;
+  if (shape & WS_SQUARE) o += vec;
   L.H = o;
   o += al256(size_t(L.ldh) * (m_max + 1) * sc);
   L.hbuf = o;
@@ -88,8 +91,10 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms, int shape = 
   return L;
 }
 
+bool squared(const ppf_opts* o) { return o->func == PPF_INVSQRT_SQ || o->func == PPF_SIGN; }
+
 int ws_shape(const ppf_poly* q, const ppf_opts* o) {
-  int s = 0;
+  int s = squared(o) ? WS_SQUARE : 0;
   if (o->krylov == PPF_LANCZOS_2PASS) s |= WS_TWOPASS;
   else if (q && o->precond == PPF_PREC_RIGHT) s |= WS_RIGHT;
   return s;
@@ -249,7 +254,21 @@ struct Runner {
   }
 
   // ----- SpMV with halo exchange (nranks > 1) -----
+  // A x with its fused epilogue.  power == 2 (A = Q^2): two
+  // launches, t = Q x, then out = s_ax Q t + s_x x + s_z z + s_u u -- the
+  // epilogue's x term reads the chain vector x, not the launch input t.
+  int power = 1;
   void spmv(const void* x, void* out, const Epi& e) {
+    if (power == 2) {
+      spmv1(x, vec(L.TSQ), epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
+      Epi e2 = e;
+      if (!e2.xe) e2.xe = x;
+      spmv1(vec(L.TSQ), out, e2);
+      return;
+    }
+    spmv1(x, out, e);
+  }
+  void spmv1(const void* x, void* out, const Epi& e) {
     if (rec) {
       rec->push_back({x, out, e, false, 0.0});
       return;
@@ -542,7 +561,9 @@ double nrm(const std::vector<zc>& v) {
 
 void check_opts(const ppf_opts* o) {
   PPF_REQUIRE(o, "opts is NULL");
-  PPF_REQUIRE(o->func == PPF_INVSQRT || o->func == PPF_SQRT, "bad func");
+  PPF_REQUIRE(o->func == PPF_INVSQRT || o->func == PPF_SQRT || o->func == PPF_INVSQRT_SQ ||
+                  o->func == PPF_SIGN,
+              "bad func");
   PPF_REQUIRE(o->krylov == PPF_LANCZOS || o->krylov == PPF_ARNOLDI_CGS2 ||
                   o->krylov == PPF_LANCZOS_2PASS,
               "bad krylov");
@@ -569,11 +590,14 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   const bool lanczos = o->krylov != PPF_ARNOLDI_CGS2;
   const bool right = q && o->precond == PPF_PREC_RIGHT;
   const int deg = q ? q->deg : 0;
-  const long long per_step = q ? 2LL * deg + 1 : 1;   // mvms per preconditioned step
+  const int power = squared(o) ? 2 : 1;  // A = Q^2 for INVSQRT_SQ / SIGN
+  // mvms per preconditioned step (2 per application of Q^2)
+  const long long per_step = power * (q ? 2LL * deg + 1 : 1);
   const int m_max = o->m_max;
   const int k = std::max(1, o->check_every);
   const double brt = o->breakdown_rtol > 0.0 ? o->breakdown_rtol : 1e-14;
   Runner R(ctx, A, q, m_max, work, bytes, ws_shape(q, o), right);
+  R.power = power;
   const int64_t n = R.n;
   const size_t vb = size_t(n) * R.sc;
   double t_dense = 0.0;
@@ -599,7 +623,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
       PPF_CUDA(cudaMemcpyAsync(R.V(0), s_vec, vb, cudaMemcpyDeviceToDevice, R.st));
   } else {
     R.apply_q(s_vec, R.V(0));
-    mvms += deg;
+    mvms += (long long)deg * power;
   }
   R.normalise_start();
   if (twopass) PPF_CUDA(cudaMemcpyAsync(R.vsrc(0), R.V(0), vb, cudaMemcpyDeviceToDevice, R.st));
@@ -739,12 +763,14 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     t_dense += std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
   }
   void* xo = x_host ? R.vec(R.L.Y) : x;
+  // sign(Q) b = Q f: f goes to U (free once the steps are done), then one SpMV
+  void* fo = o->func == PPF_SIGN ? R.vec(R.L.U) : xo;
   long long mv_total = mvms_start + (long long)m * per_step;
   if (!twopass) {
     // Alg 1 line 11 / Alg 2 line 11: f_m = V_m y_m or Y_m y_m
     R.upload_y(y);
     R.timed(2, double(vb) * (m + 1), [&] {
-      launch_combine(R.dt, n, basis0(), R.L.ldv, m, R.vec(R.L.ybuf), xo, R.st);
+      launch_combine(R.dt, n, basis0(), R.L.ldv, m, R.vec(R.L.ybuf), fo, R.st);
     });
   } else {
     // two-pass, pass 2: regenerate v_2..v_m with the pass-1
@@ -766,11 +792,16 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     }
     mv_total += (long long)(m - 1) * per_step;
     if (right) {
-      R.apply_q(acc, xo);
-      mv_total += deg;
+      R.apply_q(acc, fo);
+      mv_total += (long long)deg * power;
     } else {
-      PPF_CUDA(cudaMemcpyAsync(xo, acc, vb, cudaMemcpyDeviceToDevice, R.st));
+      PPF_CUDA(cudaMemcpyAsync(fo, acc, vb, cudaMemcpyDeviceToDevice, R.st));
     }
+  }
+  if (o->func == PPF_SIGN) {
+    R.power = 1;
+    R.spmv(fo, xo, Runner::epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
+    mv_total += 1;
   }
   if (x_host) {
     PPF_CUDA(cudaMemcpyAsync(x_host, xo, vb, cudaMemcpyDeviceToHost, R.st));
@@ -891,20 +922,22 @@ ppf_status ppf_hessenberg(ppf_ctx* ctx, int ld, void* H, int* m, double* beta0) 
 ppf_status ppf_ritz_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, int deg, size_t* bytes) {
   PPF_API_BEGIN
   PPF_REQUIRE(ctx && A && bytes && deg >= 0 && deg < 255, "bad arguments");
-  *bytes = ws_layout(A->n_local, A->dtype, deg + 1, ctx->num_sms).total;
+  *bytes = ws_layout(A->n_local, A->dtype, deg + 1, ctx->num_sms, WS_SQUARE).total;
   PPF_API_END
 }
 
-// Ritz values of H_d from d = deg+1 Arnoldi steps with A, Leja order,
-// divided differences.
-ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg, void* work,
-                                size_t bytes, ppf_poly** out) {
+// Ritz values of H_d from d = deg+1 Arnoldi steps with A^power,
+// Leja order, divided differences.
+ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
+                                    int power, void* work, size_t bytes, ppf_poly** out) {
   PPF_API_BEGIN
   PPF_REQUIRE(ctx && A && start && out, "NULL argument");
   PPF_REQUIRE(deg >= 0 && deg < 255, "deg out of range");
+  PPF_REQUIRE(power == 1 || power == 2, "power must be 1 or 2");
   PPF_REQUIRE(A->dtype == PPF_C128, "Ritz-Newton polynomials need a complex operator");
   const int d = deg + 1;
-  Runner R(ctx, A, nullptr, d, work, bytes);
+  Runner R(ctx, A, nullptr, d, work, bytes, WS_SQUARE);
+  R.power = power;
   PPF_CUDA(cudaMemcpyAsync(R.V(0), start, size_t(R.n) * R.sc, cudaMemcpyDeviceToDevice, R.st));
   R.normalise_start();
   for (int j = 0; j < d; ++j) {
@@ -931,6 +964,11 @@ ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int
   q->dd = divided_differences_invsqrt(q->nodes);
   *out = q;
   PPF_API_END
+}
+
+ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg, void* work,
+                                size_t bytes, ppf_poly** out) {
+  return ppf_poly_ritz_newton_pow(ctx, A, start, deg, 1, work, bytes, out);
 }
 
 }  // extern "C"
