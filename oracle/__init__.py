@@ -16,6 +16,7 @@ Modules (each function cites the passage it follows):
   spmv       O9  row-chunked SciPy CSR mat-vec
   chebyshev  O1, O3  Chebyshev interpolant of z^{-1/2}, forward three-term apply
   newton     O2, O3  Ritz values, Lejà order, divided differences, Newton apply
+  contour_ls §5.3    least-squares q on a discretised contour, Arnoldi-like apply
   dense      O6  y = beta0 * H^{-1/2} e_1 by eigendecomposition
   krylov     O4, O5, O7, O8  Algorithm 1 (Lanczos / CGS2 Arnoldi), history, m*
   reference  R1-R4  closed-form / reference f(A)b

@@ -36,7 +36,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import chebyshev, newton
+from . import chebyshev, contour_ls, newton
 from .dense import invsqrt_e1
 from .spmv import SquaredOperator
 
@@ -59,6 +59,8 @@ def apply_q(q, op, v):
         return v
     if isinstance(q, chebyshev.ChebPoly):
         return chebyshev.apply(q, op, v)
+    if isinstance(q, contour_ls.LSPoly):
+        return contour_ls.apply(q, op, v)
     return newton.apply(q, op, v)
 
 
@@ -74,7 +76,7 @@ def run(op, b: np.ndarray, q, *, func: str = "invsqrt", krylov: str = "cgs2",
     right = precond == "right" and q is not None
     mv0 = op.mvms
     dt = np.result_type(b.dtype, op.dtype, np.float64)
-    if isinstance(q, newton.NewtonPoly):
+    if isinstance(q, (newton.NewtonPoly, contour_ls.LSPoly)):
         dt = np.complex128
     s = op.matvec(b) if func == "sqrt" else b
     if right:

@@ -6,8 +6,9 @@ import os
 import numpy as np
 import pytest
 
+from inputs import configs
 from inputs import operators as ops
-from oracle import chebyshev, newton, reference
+from oracle import chebyshev, krylov, newton, reference
 from oracle.spmv import Operator
 
 from .conftest import GOLDEN
@@ -154,3 +155,61 @@ def test_ritz_values_are_eigs_of_hessenberg_and_branch_check():
     assert np.abs(th - ev).max() < 1e-8                               # full space: Ritz = eig
     with pytest.raises(newton.BranchError):
         newton.ritz_values(np.diag([1.0, -2.0]))
+
+
+# ---------------------------------------------------------------------------
+# contour least-squares polynomial (§5.3)
+# ---------------------------------------------------------------------------
+def test_contour_ls_circle_equals_taylor_series():
+    """On N equispaced points of a circle |z - c| = r the orthonormal basis is
+    ((z - c)/r)^k / sqrt(N) and the least-squares fit of z^{-1/2} is the
+    truncated Taylor series Σ binom(-1/2, k) c^{-1/2-k} (z - c)^k up to
+    aliasing of order (r/c)^(N-d) (closed form)."""
+    from scipy.special import binom
+    from oracle import contour_ls
+    c, r, N, deg = 3.0, 2.2, 128, 16
+    q = contour_ls.construct(contour_ls.circle(c, r, N), deg)
+    k = np.arange(deg + 1)
+    t = binom(-0.5, k) * c ** (-0.5 - k)
+    zz = c + 1.9 * np.exp(1j * np.linspace(0, 2 * np.pi, 37)) * np.linspace(0.1, 1, 37)
+    taylor = np.polynomial.polynomial.polyval(zz - c, t)
+    assert np.abs(contour_ls.evaluate(q, zz) - taylor).max() < 1e-12 * np.abs(taylor).max()
+    assert contour_ls.certify(q) > 0
+
+
+def test_contour_ls_normal_equations_and_lstsq():
+    """General contour (an ellipse offset from 0): the residual z^{-1/2} - q is
+    orthogonal to P_{d-1} in ⟨.,.⟩_ω (eq. polynomial_inner_product), and the fit
+    values agree with numpy's least squares on a scaled monomial basis."""
+    from oracle import contour_ls
+    t = 2 * np.pi * np.arange(200) / 200
+    z = 4.0 + 3.0 * np.cos(t) + 1.5j * np.sin(t)
+    deg = 9
+    q = contour_ls.construct(z, deg)
+    f = z ** -0.5
+    qz = contour_ls.evaluate(q, z)
+    V = np.vander((z - 4.0) / 3.0, deg + 1, increasing=True)
+    assert np.abs(V.conj().T @ (f - qz)).max() < 1e-12 * np.abs(f).sum()
+    coef, *_ = np.linalg.lstsq(V, f, rcond=None)
+    assert np.abs(V @ coef - qz).max() < 1e-12
+    # q(A) v for A = diag(z) (the Arnoldi-like matrix process, P:398) equals
+    # the fitted values
+    import scipy.sparse as sp
+    from oracle.spmv import Operator
+    op = Operator(sp.diags(z).tocsr())
+    assert np.abs(contour_ls.apply(q, op, np.ones(len(z))) - qz).max() < 1e-12
+    assert op.mvms == deg
+
+
+def test_contour_ls_wilson_converges():
+    """The C5 family (Wilson-Dirac 4^4, m0 = -1.0) with the circle
+    |z - (4 + m0)| = 2.2: left-preconditioned CGS2 reaches the
+    R4 reference to 1e-8."""
+    from oracle import contour_ls
+    A, b, _ = configs.build("C5s")
+    op = Operator(A.to_scipy())
+    xr = reference.arnoldi_reference(op, b).x
+    q = contour_ls.construct(contour_ls.circle(3.0, 2.2, 128), 16)
+    res = krylov.run(op, b, q, func="invsqrt", krylov="cgs2", m_max=30, stop="true", tol=1e-8,
+                     x_ref=xr)
+    assert res.term == "converged" and res.m <= 6
