@@ -60,6 +60,9 @@ def parse():
     p.add_argument("--krylov", default=None, choices=["lanczos", "cgs2", "lanczos2p"],
                    help="override the config's Krylov method (lanczos2p = two-pass)")
     p.add_argument("--plain", action="store_true", help="no preconditioner (d = 1)")
+    p.add_argument("--poly", default="config", choices=["config", "contour"],
+                   help="contour: least-squares q on the circle |z - (4+m0)| = 2.2 (P:359-404; "
+                        "Wilson configs)")
     p.add_argument("--check-every", type=int, default=1,
                    help="k of the stopping check (PAPER.md:424 uses 64/d)")
     p.add_argument("--split", type=int, default=0,
@@ -285,6 +288,9 @@ def main():
     def make_q():
         if args.plain:
             return None
+        if args.poly == "contour":
+            c = 4.0 + cfg.params["m0"]
+            return pp.Poly.contour_ls(c + 2.2 * np.exp(2j * np.pi * np.arange(128) / 128), deg)
         if cfg.poly == "chebyshev":
             return pp.Poly.chebyshev(*iv, deg)
         return pp.Poly.ritz_newton(ctx, M, bd, deg, power=power)
@@ -353,7 +359,7 @@ def main():
     bh = torch.from_numpy(b).pin_memory()
     xh = torch.empty_like(bh).pin_memory()
     e2e_times = []
-    ritz = cfg.poly != "chebyshev" and not args.plain
+    ritz = cfg.poly != "chebyshev" and not args.plain and args.poly == "config"
     for i in range(max(2, min(args.steps, 3)) + 1):
         t0 = time.perf_counter()
         if ritz:  # the Ritz setup starts from b: it needs b on the device
@@ -394,6 +400,8 @@ def main():
         "data": "synthetic (seeded generators in inputs/; no dataset)",
         "config": {"workload": WORKLOAD.get(name, name), "deg": None if args.plain else deg,
                    "precond": "none (plain, d = 1)" if args.plain else args.precond,
+                   "poly": "contour-LS circle |z-(4+m0)|=2.2, N=128" if args.poly == "contour"
+                   else cfg.poly,
                    "krylov": krylov_m, "check_every": args.check_every, "tol": cfg.tol,
                    "format": args.fmt, "sell_split": split,
                    "m": m_iter, "mvms": reps[-1].mvms, "n": A.n, "nnz": A.nnz,

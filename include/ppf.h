@@ -197,6 +197,16 @@ ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int
  * of PPF_INVSQRT_SQ / PPF_SIGN, two mat-vecs per Arnoldi step). */
 ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
                                     int power, void* work, size_t work_bytes, ppf_poly** out);
+/* ppf_poly_contour_ls (§5.3): the least-squares polynomial of degree
+ *   deg for z^{-1/2} on the discretised contour `points` (npts complex, host,
+ *   interleaved; npts > deg + 1; no point on (-inf, 0]): Arnoldi on
+ *   diag(points) from ones/sqrt(npts), alpha = P^H z^{-1/2}.  Stored in Newton
+ *   form on deg+1 Leja-ordered contour points (the interpolant of a degree-deg
+ *   polynomial is the polynomial), applied by the fused Newton-Horner chain.
+ *   min_re_q (may be NULL) = min Re q over the points; <= 0 gives PPF_EBRANCH
+ *   (the certificate of P:401-403). */
+ppf_status ppf_poly_contour_ls(const double* points, int npts, int deg, double* min_re_q,
+                               ppf_poly** out);
 ppf_status ppf_poly_import(int kind, int deg, const double* ab, const void* coef,
                            const void* nodes, ppf_poly** out);
 ppf_status ppf_poly_export(const ppf_poly* q, int* kind, int* deg, double* ab,

@@ -203,6 +203,18 @@ class Poly:
         return cls(h)
 
     @classmethod
+    def contour_ls(cls, points, deg: int) -> "Poly":
+        """least-squares q on the contour points (complex array)."""
+        z = np.ascontiguousarray(np.asarray(points, dtype=np.complex128))
+        h = C.c_void_p()
+        mr = C.c_double()
+        check(_lib().ppf_poly_contour_ls(_ptr(z.view(np.float64), C.c_double), len(z), int(deg),
+                                         C.byref(mr), C.byref(h)))
+        p = cls(h)
+        p.min_re = mr.value
+        return p
+
+    @classmethod
     def newton(cls, nodes, dd) -> "Poly":
         nodes = np.ascontiguousarray(nodes, dtype=np.complex128)
         dd = np.ascontiguousarray(dd, dtype=np.complex128)

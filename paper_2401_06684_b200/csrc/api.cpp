@@ -592,6 +592,38 @@ ppf_status ppf_poly_eval(const ppf_poly* q, int npts, const double* z, double* o
   PPF_API_END
 }
 
+ppf_status ppf_poly_contour_ls(const double* points, int npts, int deg, double* min_re_q,
+                               ppf_poly** out) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(points && out, "NULL argument");
+  PPF_REQUIRE(deg >= 0 && deg <= 256 && npts > deg + 1, "need 0 <= deg <= 256 and npts > deg + 1");
+  std::vector<zc> z(npts);
+  for (int i = 0; i < npts; ++i) {
+    z[i] = zc(points[2 * i], points[2 * i + 1]);
+    PPF_REQUIRE(std::isfinite(z[i].real()) && std::isfinite(z[i].imag()), "non-finite point");
+    if (std::abs(z[i].imag()) <= 1e-14 * std::abs(z[i]) && z[i].real() <= 0.0)
+      fail(PPF_EBRANCH, "contour point on the branch cut (-inf, 0]");
+  }
+  auto* q = new ppf_poly();
+  double mr = 0.0;
+  try {
+    contour_ls_newton(z, deg, q->nodes, q->dd, mr);
+  } catch (...) {
+    delete q;
+    throw;
+  }
+  if (min_re_q) *min_re_q = mr;
+  if (!(mr > 0.0)) {
+    delete q;
+    fail(PPF_EBRANCH, "Re q <= 0 at a contour point (certificate of P:401-403)");
+  }
+  q->kind = PPF_POLY_NEWTON;
+  q->deg = deg;
+  q->a = q->b = 0.0;
+  *out = q;
+  PPF_API_END
+}
+
 void ppf_poly_destroy(ppf_poly* q) { delete q; }
 
 // ---------------------------------------------------------------------------

@@ -94,6 +94,87 @@ std::vector<zc> leja_order(const std::vector<zc>& nodes) {
   return out;
 }
 
+// Least-squares q on a discretised contour: Arnoldi on
+// diag(z_1..z_N) from [1..1]/sqrt(N) gives the orthonormal basis polynomials
+// as the columns of P; alpha = P^H z^{-1/2}; the fit's
+// values at the contour points are P alpha.  The device applies q in Newton
+// form: q has degree deg, so its interpolant at deg+1 Leja-ordered contour
+// points is q itself (divided differences of the fitted values), evaluated by
+// the same fused Newton-Horner chain as the Ritz polynomials.  Returns
+// min Re q(z_i) (the certificate of P:401-403) through min_re.
+void contour_ls_newton(const std::vector<zc>& z, int deg, std::vector<zc>& nodes,
+                       std::vector<zc>& dd, double& min_re) {
+  const int N = int(z.size()), d = deg + 1;
+  std::vector<zc> P(size_t(N) * d, zc(0.0, 0.0));  // column-major N x d
+  auto col = [&](int k) { return &P[size_t(k) * N]; };
+  for (int i = 0; i < N; ++i) col(0)[i] = 1.0 / std::sqrt(double(N));
+  std::vector<zc> w(N), h(d);
+  for (int k = 1; k < d; ++k) {
+    for (int i = 0; i < N; ++i) w[i] = z[i] * col(k - 1)[i];
+    for (int pass = 0; pass < 2; ++pass) {  // CGS with one reorthogonalisation
+      for (int j = 0; j < k; ++j) {
+        zc s(0.0, 0.0);
+        for (int i = 0; i < N; ++i) s += std::conj(col(j)[i]) * w[i];
+        h[j] = s;
+      }
+      for (int j = 0; j < k; ++j)
+        for (int i = 0; i < N; ++i) w[i] -= h[j] * col(j)[i];
+    }
+    double nr = 0.0;
+    for (int i = 0; i < N; ++i) nr += std::norm(w[i]);
+    nr = std::sqrt(nr);
+    if (!(nr > 0.0)) fail(PPF_EINVAL, "contour points do not support degree deg (need deg + 1 distinct points)");
+    for (int i = 0; i < N; ++i) col(k)[i] = w[i] / nr;
+  }
+  std::vector<zc> alpha(d);
+  for (int j = 0; j < d; ++j) {
+    zc s(0.0, 0.0);
+    for (int i = 0; i < N; ++i) s += std::conj(col(j)[i]) * (1.0 / std::sqrt(z[i]));
+    alpha[j] = s;
+  }
+  std::vector<zc> qz(N, zc(0.0, 0.0));
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i < N; ++i) qz[i] += alpha[j] * col(j)[i];
+  min_re = HUGE_VAL;
+  for (int i = 0; i < N; ++i) min_re = std::min(min_re, qz[i].real());
+  // deg+1 nodes in Leja order among the contour points (same rule as
+  // leja_order: max modulus first, then greedy max sum log distance, ties to
+  // the smaller index after sorting by (Re, Im))
+  std::vector<int> idx(N);
+  for (int i = 0; i < N; ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+    if (z[a].real() != z[b].real()) return z[a].real() < z[b].real();
+    return z[a].imag() < z[b].imag();
+  });
+  std::vector<char> used(N, 0);
+  std::vector<double> score(N, 0.0);
+  std::vector<int> chosen;
+  int first = 0;
+  for (int t = 1; t < N; ++t)
+    if (std::abs(z[idx[t]]) > std::abs(z[idx[first]])) first = t;
+  chosen.push_back(first);
+  used[first] = 1;
+  while (int(chosen.size()) < d) {
+    const int last = chosen.back();
+    int best = -1;
+    for (int t = 0; t < N; ++t) {
+      if (used[t]) continue;
+      score[t] += std::log(std::abs(z[idx[t]] - z[idx[last]]));
+      if (best < 0 || score[t] > score[best]) best = t;
+    }
+    chosen.push_back(best);
+    used[best] = 1;
+  }
+  nodes.resize(d);
+  dd.resize(d);
+  for (int j = 0; j < d; ++j) {
+    nodes[j] = z[idx[chosen[j]]];
+    dd[j] = qz[idx[chosen[j]]];
+  }
+  for (int k = 1; k < d; ++k)
+    for (int i = d - 1; i >= k; --i) dd[i] = (dd[i] - dd[i - 1]) / (nodes[i] - nodes[i - k]);
+}
+
 std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& x) {
   const int n = int(x.size());
   std::vector<zc> dd(n);

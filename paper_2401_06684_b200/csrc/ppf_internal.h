@@ -217,6 +217,8 @@ double chebyshev_eval(const ppf_poly& q, double z);
 zc poly_eval(const ppf_poly& q, zc z);
 std::vector<zc> leja_order(const std::vector<zc>& nodes);
 std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& nodes);
+void contour_ls_newton(const std::vector<zc>& z, int deg, std::vector<zc>& nodes,
+                       std::vector<zc>& dd, double& min_re);
 
 // ---------------------------------------------------------------------------
 // Device kernels (kernels.cu): host-side launchers

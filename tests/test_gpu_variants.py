@@ -219,3 +219,27 @@ def test_sign_function_hermitian_lanczos(ctx):
     xg, rep = pp.run(ctx, M, pp.Poly.chebyshev(a, bb, 6), dev(b), func="sign", krylov="lanczos",
                      m_max=20, stop="fixed")
     _check(ctx, res_o, xg, rep, complex_=True, h_tol=1e-10)
+
+
+# ---------------------------------------------------------------------------
+# contour least-squares polynomial
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("stop", ["fixed", "true"])
+def test_contour_ls_wilson(ctx, stop):
+    """C5 family (Wilson-Dirac 4^4) with the least-squares q on the circle
+    |z - (4 + m0)| = 2.2: the library's q (Newton form on Leja
+    contour points) against the oracle's (Arnoldi-like recurrence), same m*."""
+    from oracle import contour_ls
+    cfg = configs.CONFIGS["C5s"]
+    A, b, _ = configs.build("C5s")
+    op = Operator(A.to_scipy())
+    z = contour_ls.circle(3.0, 2.2, 128)
+    qo = contour_ls.construct(z, 16)
+    kw = dict(m_max=8) if stop == "fixed" else dict(m_max=cfg.m_max)
+    xr = reference.arnoldi_reference(op, b).x if stop == "true" else None
+    res_o = krylov.run(op, b, qo, func="invsqrt", krylov="cgs2", stop=stop, tol=cfg.tol,
+                       x_ref=xr, **kw)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A))
+    xg, rep = pp.run(ctx, M, pp.Poly.contour_ls(z, 16), dev(b), func="invsqrt", krylov="cgs2",
+                     stop=stop, tol=cfg.tol, x_ref=None if xr is None else dev(xr), **kw)
+    _check(ctx, res_o, xg, rep, complex_=True, h_tol=1e-10)

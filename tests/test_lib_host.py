@@ -11,7 +11,7 @@ import scipy.linalg as sla
 
 from inputs import configs
 from inputs import operators as ops
-from oracle import chebyshev, dense, newton
+from oracle import chebyshev, contour_ls, dense, newton
 
 from .conftest import ROOT
 
@@ -85,6 +85,31 @@ def test_newton_import_eval_matches_oracle():
     assert np.abs(q.eval(qo.nodes) - qo.nodes ** -0.5).max() < 1e-10
     ex = q.export()
     assert np.array_equal(ex["nodes"], qo.nodes) and np.array_equal(ex["dd"], qo.dd)
+
+
+@pytest.mark.parametrize("contour", ["circle", "ellipse"])
+@pytest.mark.parametrize("deg", [0, 4, 16])
+def test_contour_ls_matches_oracle(contour, deg):
+    """ppf_poly_contour_ls (host, Newton form on Leja contour points) vs the
+    oracle's least-squares polynomial (Arnoldi-like recurrence) at
+    points inside and on the contour; the certificate min Re q."""
+    if contour == "circle":
+        z = contour_ls.circle(3.0, 2.2, 128)
+    else:
+        t = 2 * np.pi * np.arange(150) / 150
+        z = 4.0 + 3.0 * np.cos(t) + 1.5j * np.sin(t)
+    qo = contour_ls.construct(z, deg)
+    q = Poly.contour_ls(z, deg)
+    zz = np.concatenate([z, 0.5 * z + 0.5 * z.mean()])
+    ref = contour_ls.evaluate(qo, zz)
+    assert np.abs(q.eval(zz) - ref).max() < 1e-11 * np.abs(ref).max()
+    assert q.min_re == pytest.approx(contour_ls.certify(qo), rel=1e-10)
+
+
+def test_contour_ls_rejects_branch_cut():
+    # a circle around 0: the contour meets (-inf, 0]
+    with pytest.raises(_lib.PPFError):
+        Poly.contour_ls(contour_ls.circle(0.0, 1.0, 64), 4)
 
 
 @pytest.mark.parametrize("m", [1, 2, 7, 25, 60])
