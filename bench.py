@@ -41,6 +41,10 @@ WORKLOAD = {
     "C6": "PAPER.md §6.2 application (P:459-510): sign(Q)b = Q (Q^2)^{-1/2} b for the overlap kernel "
           "Q = Γ5 D_w(m_w=-1.4, mu=0.3) on a 16^4 Haar lattice (n=786,432) complex128, Q^2 as two SpMVs, "
           "Ritz-Newton q of Q^2 deg 15 (d=16), Arnoldi CGS2 (context, not a BASELINE config)",
+    "C7": "PAPER.md Ex. 6.3 setting (P:518-566): L^{1/2}b for the in-degree Laplacian of a synthetic "
+          "web-like directed graph (n=281,903, ~2.6M nnz; stands in for Kamvar/Stanford), sqrt via "
+          "L^{-1/2}(Lb) with implicit desingularisation, Ritz-Newton q from Lb, Arnoldi CGS2, tol 1e-7 "
+          "(context, not a BASELINE config)",
     "T1": "PAPER.md Table 1 workload (P:418-457): 3D Laplacian 100^3, Chebyshev q, Lanczos, "
           "f(z)=z^{-1/2}, tol 1e-12 (context, not a BASELINE config)",
 }
@@ -54,7 +58,10 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C4")
     p.add_argument("--deg", type=int, default=None)
-    p.add_argument("--fmt", default="sell64", choices=["sell32", "sell64", "csr"])
+    p.add_argument("--fmt", default=None, choices=["sell32", "sell64", "csr"],
+                   help="default: sell64 (fp64 stencils), sell32 (complex, graph)")
+    p.add_argument("--sigma", type=int, default=0,
+                   help="SELL-C-sigma sorting window (0: 1, or a global sort for the power-law graph)")
     p.add_argument("--precond", default="left", choices=["left", "right"],
                    help="Algorithm 1 (left) or 2 (right, PAPER.md:155-172)")
     p.add_argument("--krylov", default=None, choices=["lanczos", "cgs2", "lanczos2p"],
@@ -173,7 +180,8 @@ def cpu_baseline(cfg, A, b, iv, deg, m, mvms_total):
         setup_mvms = 0
     else:
         from oracle.spmv import SquaredOperator
-        q, setup_mvms, _ = newton.ritz_newton(SquaredOperator(op) if sq else op, b, deg)
+        start = op.matvec(b) if cfg.params.get("ritz_start") == "Ab" else b
+        q, setup_mvms, _ = newton.ritz_newton(SquaredOperator(op) if sq else op, start, deg)
     if sq:
         res = krylov.run_sign(op, b, q, krylov=cfg.krylov, m_max=1, stop="fixed")
     else:
@@ -251,9 +259,16 @@ def main():
     name = args.config
     cfg, A, b, iv = setup_inputs(name)
     deg = args.deg if args.deg is not None else cfg.degs[0]
+    if args.fmt is None:
+        args.fmt = "sell32" if (cfg.complex_ or cfg.family == "graph") else "sell64"
     fmt = {"sell32": ("sell", 32), "sell64": ("sell", 64), "csr": ("csr", 32)}[args.fmt]
     if cfg.complex_ and fmt == ("sell", 64):
         fmt = ("sell", 32)
+    sigma = args.sigma
+    if sigma == 0:
+        # power-law row lengths: sort rows globally by length (0.14% padding
+        # for C7 instead of 7x with sigma = 1)
+        sigma = 32 * ((A.n + 31) // 32) if (cfg.family == "graph" and fmt == ("sell", 32)) else 1
     stream = torch.cuda.Stream()
     if world > 1:
         # row-slab sharding: contiguous slabs of whole grid planes /
@@ -264,7 +279,7 @@ def main():
         rp = A.row_ptr[lo:hi + 1] - A.row_ptr[lo]
         sl = slice(int(A.row_ptr[lo]), int(A.row_ptr[hi]))
         plan = pp.Plan(rp, A.col[sl], A.val[sl], row_bounds=bounds, rank=rank, fmt=fmt[0],
-                       C_=fmt[1])
+                       C_=fmt[1], sigma=sigma)
         needs = {p: plan.halo_recv(p) for p in range(world)}
         all_needs = [None] * world
         dist.all_gather_object(all_needs, needs)
@@ -276,13 +291,14 @@ def main():
         b = b[lo:hi].copy()
     else:
         bounds = [0, A.n]
-        plan = pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1])
+        plan = pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1], sigma=sigma)
         ctx = pp.Context(local, stream=stream)
     info = plan.info()
     M = pp.Matrix(ctx, plan)
     split = M.set_split(args.split)
     plan.close()
     bd = torch.from_numpy(b).cuda()
+    ritz_buf = torch.empty_like(bd)
     torch.cuda.synchronize()
 
     def make_q():
@@ -293,6 +309,11 @@ def main():
             return pp.Poly.contour_ls(c + 2.2 * np.exp(2j * np.pi * np.arange(128) / 128), deg)
         if cfg.poly == "chebyshev":
             return pp.Poly.chebyshev(*iv, deg)
+        if cfg.params.get("ritz_start") == "Ab":
+            # singular A (Thm 4.1): the Ritz values from A b, whose null-space
+            # component is deflated (implicit desingularisation)
+            M.spmv(bd, ritz_buf)
+            return pp.Poly.ritz_newton(ctx, M, ritz_buf, deg, power=power)
         return pp.Poly.ritz_newton(ctx, M, bd, deg, power=power)
 
     krylov_m = args.krylov or cfg.krylov
@@ -363,7 +384,8 @@ def main():
     for i in range(max(2, min(args.steps, 3)) + 1):
         t0 = time.perf_counter()
         if ritz:  # the Ritz setup starts from b: it needs b on the device
-            q = pp.Poly.ritz_newton(ctx, M, bh.to("cuda", non_blocking=True), deg, power=power)
+            bd.copy_(bh, non_blocking=True)
+            q = make_q()
         else:
             q = make_q()
         _, rep_h = pp.run_host(ctx, M, q, bh, xh, work=work, **run_kw)
@@ -403,7 +425,7 @@ def main():
                    "poly": "contour-LS circle |z-(4+m0)|=2.2, N=128" if args.poly == "contour"
                    else cfg.poly,
                    "krylov": krylov_m, "check_every": args.check_every, "tol": cfg.tol,
-                   "format": args.fmt, "sell_split": split,
+                   "format": args.fmt, "sell_sigma": sigma, "sell_split": split,
                    "m": m_iter, "mvms": reps[-1].mvms, "n": A.n, "nnz": A.nnz,
                    "stored_entries": info["stored"], "stop": f"estimate <= {cfg.tol:g}, k = {args.check_every} (P:424)",
                    "l2": "inputs larger than L2 (matrix ~1.4 GB/126 MB L2), no flush",

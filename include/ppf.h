@@ -181,10 +181,15 @@ ppf_status ppf_spmv_local(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
  *   (-inf, 0] (PPF_EBRANCH), Leja-orders them (max modulus first, then
  *   greedy max sum log|theta - chosen|, ties to the smaller index after sorting
  *   by (Re, Im)) and forms the divided differences of z^{-1/2}.  `work` is
- *   device scratch of at least ppf_ritz_workspace_bytes.  Always complex.
+ *   device scratch of at least ppf_ritz_workspace_bytes.  Complex operators:
+ *   any nodes off (-inf, 0]; real operators: real nodes only.
  * ppf_poly_import: kind CHEBYSHEV: ab = {a, b}, coef = deg+1 doubles, nodes
  *   ignored.  kind NEWTON: coef = deg+1 complex divided differences, nodes =
  *   deg+1 complex Leja-ordered nodes, ab ignored.  No certificate is applied.
+ *   A Newton polynomial is applied to a PPF_R64 operator only if all its nodes
+ *   and divided differences are real (exactly zero imaginary parts); the Ritz
+ *   construction on a PPF_R64 operator returns PPF_EINVAL for complex Ritz
+ *   values (use a PPF_C128 plan of the same matrix).
  * ppf_poly_export: the same layout (caller buffers of deg+1 entries; query deg
  *   first with coef = nodes = NULL).
  * ppf_poly_eval: q at `npts` complex points (host, interleaved) -> host out.

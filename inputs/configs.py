@@ -16,7 +16,7 @@ from .vectors import gaussian_vector
 @dataclass(frozen=True)
 class Config:
     name: str
-    family: str                  # "laplacian" | "convdiff" | "wilson" | "overlap"
+    family: str                  # "laplacian" | "convdiff" | "wilson" | "overlap" | "graph"
     params: dict = field(default_factory=dict)
     func: str = "invsqrt"        # "invsqrt" | "sqrt" (= A^{-1/2}(Ab)) | "sign"
                                  # (= Q (Q^2)^{-1/2} b)
@@ -49,6 +49,13 @@ CONFIGS = {
     # (P:475), d = 16 (Table 2 row), Arnoldi CGS2 (context workload, not a BASELINE config)
     "C6": Config("C6", "overlap", dict(L=16, m_w=-1.4, mu=0.3, link_seed=206), "sign", (15,),
                  "cgs2", "ritz", 1e-8, 60, 106),
+    # Ex. 6.3's setting: L^{1/2} b for the in-degree Laplacian of a
+    # directed graph, a seeded synthetic web-like graph standing in for Kamvar/Stanford
+    # (n = 281,903, ~2.59M nnz; the dataset is not available), Ritz-Newton q from
+    # L b (implicit desingularisation, Thm 4.1), Arnoldi with reorthogonalisation,
+    # tol 1e-7, k = 32/d (context workload, not a BASELINE config)
+    "C7": Config("C7", "graph", dict(n=281903, avg_deg=8.97, graph_seed=207, ritz_start="Ab"),
+                 "sqrt", (15, 7), "cgs2", "ritz", 1e-7, 200, 107),
     # PAPER.md Table 1's own workload (§6.1): 3D Laplacian 100^3, tol 1e-12,
     # right preconditioning, d = deg+1 in {1..64}, k = 64/d (context workload)
     "T1": Config("T1", "laplacian", dict(N=100, dim=3), "invsqrt", (7,), "lanczos", "chebyshev",
@@ -60,6 +67,8 @@ CONFIGS = {
                   "chebyshev", 1e-8, 60, 204),
     "C6s": Config("C6s", "overlap", dict(L=4, m_w=-1.4, mu=0.3, link_seed=306), "sign", (15, 7),
                   "cgs2", "ritz", 1e-8, 60, 206),
+    "C7s": Config("C7s", "graph", dict(n=2000, avg_deg=8.97, graph_seed=307, ritz_start="Ab"),
+                  "sqrt", (7, 3), "cgs2", "ritz", 1e-7, 200, 207),
     "C5s": Config("C5s", "wilson", dict(L=4, m0=-1.0, link_seed=305), "invsqrt", (16, 4), "cgs2", "ritz",
                   1e-8, 30, 205),
 }
@@ -74,6 +83,8 @@ def operator(cfg: Config):
                 ops.convdiff_interval(p["N"], p["dim"], p["beta"]))
     if cfg.family == "wilson":
         return ops.wilson_dirac(p["L"], p["m0"], seed=p["link_seed"]), None
+    if cfg.family == "graph":
+        return ops.directed_graph_laplacian(p["n"], p["avg_deg"], p["graph_seed"]), None
     if cfg.family == "overlap":
         return ops.overlap_kernel(p["L"], p["m_w"], p["mu"], seed=p["link_seed"]), None
     raise ValueError(cfg.family)

@@ -254,3 +254,49 @@ def _wilson_assemble(L: int, m0: float, links: np.ndarray, mu_c: float = 0.0) ->
     assert np.all(np.diff(cols, axis=1) > 0), "duplicate columns (L too small?)"
     row_ptr = np.arange(0, n * K + 1, K, dtype=np.int64)
     return CSR(n, row_ptr, cols.reshape(-1), vals.reshape(-1))
+
+
+# ----------------------------------------------------------------------------
+# In-degree graph Laplacian of a directed graph (Ex. 6.3)
+# ----------------------------------------------------------------------------
+def directed_graph_laplacian(n: int, avg_deg: float, seed: int, alpha: float = 2.1,
+                             max_out: int = 255) -> CSR:
+    """L = D_in - A for a seeded synthetic directed graph (it
+    stands in for SuiteSparse Kamvar/Stanford, which is not available and is
+    not reproduced).  A_ij = 1 for an edge i -> j; D_in = diag(column sums of
+    A), so every column of L sums to zero and L is singular.
+
+    Web-crawl-like degree structure: out-degrees (the row lengths of L) follow
+    a power law truncated at ``max_out`` (crawlers cap the links followed per
+    page), in-degrees are heavy-tailed (targets drawn with weights
+    w_k ∝ k^{-1/(alpha-1)}); self loops dropped, duplicates merged; plus the
+    cycle i -> i+1 (mod n), so the graph is strongly connected and the
+    eigenvalue 0 of L is simple (hence semi-simple, the hypothesis of
+    Theorem 4.1)."""
+    rng = np.random.default_rng(seed)
+    # out-degrees: P(d) ∝ d^{-2.2} on 1..max_out, rescaled to the mean avg_deg - 1
+    d = np.arange(1, max_out + 1, dtype=np.float64)
+    pd = d ** -2.2
+    pd /= pd.sum()
+    outdeg = rng.choice(np.arange(1, max_out + 1), size=n, p=pd).astype(np.float64)
+    outdeg = np.clip(np.round(outdeg * (avg_deg - 1.0) / outdeg.mean()), 0, max_out).astype(np.int64)
+    k = np.arange(1, n + 1, dtype=np.float64)
+    win = k ** (-1.0 / (alpha - 1.0))
+    rng.shuffle(win)
+    src = np.repeat(np.arange(n, dtype=np.int64), outdeg)
+    dst = rng.choice(n, size=len(src), p=win / win.sum())
+    keep = src != dst
+    src = np.concatenate([src[keep], np.arange(n)])
+    dst = np.concatenate([dst[keep], (np.arange(n) + 1) % n])
+    key = np.unique(src * n + dst)
+    src, dst = key // n, key % n
+    din = np.bincount(dst, minlength=n).astype(np.float64)
+    # rows of L: diagonal din[i] and -1 at (i, j) for every edge i -> j
+    rows = np.concatenate([np.arange(n), src])
+    cols = np.concatenate([np.arange(n), dst])
+    vals = np.concatenate([din, -np.ones(len(src))])
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
+    return CSR(n, row_ptr, cols.astype(np.int64), vals)

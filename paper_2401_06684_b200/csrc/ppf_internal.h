@@ -236,6 +236,7 @@ void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
 void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st);
 // run.cpp: the sharded SpMV with communication/compute overlap
 void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e);
+bool poly_fits(const ppf_poly* q, ppf_dtype dt);
 
 struct RedScratch {   // reduction scratch (device)
   double* partials;   // [max_blocks * max_vals * 2]

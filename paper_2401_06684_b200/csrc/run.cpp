@@ -91,6 +91,19 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms, int shape = 
   return L;
 }
 
+}  // namespace
+
+// a polynomial the operator's arithmetic can apply: Chebyshev always, Newton on
+// a real operator only with real nodes and divided differences
+bool poly_fits(const ppf_poly* q, ppf_dtype dt) {
+  if (q->kind == PPF_POLY_CHEBYSHEV || dt == PPF_C128) return true;
+  for (size_t i = 0; i < q->nodes.size(); ++i)
+    if (q->nodes[i].imag() != 0.0 || q->dd[i].imag() != 0.0) return false;
+  return true;
+}
+
+namespace {
+
 bool squared(const ppf_opts* o) { return o->func == PPF_INVSQRT_SQ || o->func == PPF_SIGN; }
 
 int ws_shape(const ppf_poly* q, const ppf_opts* o) {
@@ -584,8 +597,8 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   PPF_REQUIRE(ctx && A && rep, "NULL argument");
   PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
   check_opts(o);
-  PPF_REQUIRE(!q || q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
-              "a Newton (complex) polynomial needs a complex operator");
+  PPF_REQUIRE(!q || poly_fits(q, A->dtype),
+              "a Newton polynomial with complex nodes needs a complex operator");
   const bool twopass = o->krylov == PPF_LANCZOS_2PASS;
   const bool lanczos = o->krylov != PPF_ARNOLDI_CGS2;
   const bool right = q && o->precond == PPF_PREC_RIGHT;
@@ -934,7 +947,6 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
   PPF_REQUIRE(ctx && A && start && out, "NULL argument");
   PPF_REQUIRE(deg >= 0 && deg < 255, "deg out of range");
   PPF_REQUIRE(power == 1 || power == 2, "power must be 1 or 2");
-  PPF_REQUIRE(A->dtype == PPF_C128, "Ritz-Newton polynomials need a complex operator");
   const int d = deg + 1;
   Runner R(ctx, A, nullptr, d, work, bytes, WS_SQUARE);
   R.power = power;
@@ -953,6 +965,16 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
   for (int j = 0; j < d; ++j)
     for (int i = 0; i < d; ++i) Hd[size_t(i) + size_t(j) * d] = Hh[size_t(i) + size_t(j) * (d + 1)];
   std::vector<zc> theta = eigenvalues(d, Hd);
+  if (A->dtype == PPF_R64) {
+    // a real operator runs the chain in real arithmetic: the Ritz values must
+    // be real (they are for the graph Laplacians of P:561-563); complex pairs
+    // need a complex (PPF_C128) plan of the same matrix
+    for (auto& t : theta) {
+      if (std::abs(t.imag()) > 1e-12 * std::abs(t))
+        fail(PPF_EINVAL, "complex Ritz values of a real operator: use a PPF_C128 plan");
+      t = zc(t.real(), 0.0);
+    }
+  }
   for (auto& t : theta)
     if (std::abs(t.imag()) <= 1e-13 * std::max(std::abs(t), 1e-300) && t.real() <= 0.0)
       fail(PPF_EBRANCH, "Ritz value on the branch cut (-inf, 0]");
@@ -1013,8 +1035,8 @@ extern "C" ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q
     PPF_REQUIRE(ctx && A && q && x && y, "NULL argument");
     PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
     PPF_REQUIRE(x != y, "x and y must be distinct");
-    PPF_REQUIRE(q->kind == PPF_POLY_CHEBYSHEV || A->dtype == PPF_C128,
-                "a Newton (complex) polynomial needs a complex operator");
+    PPF_REQUIRE(ppf::poly_fits(q, A->dtype),
+                "a Newton polynomial with complex nodes needs a complex operator");
     ppf::Runner R(ctx, A, q, 1, work, bytes);
     R.apply_q(x, y);
     if (ctx->profile) {

@@ -243,3 +243,60 @@ def test_contour_ls_wilson(ctx, stop):
     xg, rep = pp.run(ctx, M, pp.Poly.contour_ls(z, 16), dev(b), func="invsqrt", krylov="cgs2",
                      stop=stop, tol=cfg.tol, x_ref=None if xr is None else dev(xr), **kw)
     _check(ctx, res_o, xg, rep, complex_=True, h_tol=1e-10)
+
+
+# ---------------------------------------------------------------------------
+# sqrt of a singular in-degree graph Laplacian (Thm 4.1)
+# ---------------------------------------------------------------------------
+def _horner_np(q, op, v):
+    """Test-local Newton-Horner evaluation of a Newton q: a rounding
+    perturbation of the oracle's forward Newton basis, same mathematics."""
+    w = q.dd[q.deg] * v
+    for j in range(q.deg - 1, -1, -1):
+        w = op.matvec(w) - q.nodes[j] * w + q.dd[j] * v
+    return w
+
+
+def _newton_h_tolerance(op, b, q, **kw):
+    """H-parity bar for strongly non-normal operators (the graph Laplacian):
+    1e-11, raised to 10x the measured gap between two oracle runs that differ
+    only in the rounding of q(A)v (forward Newton basis vs Horner) -- the
+    Arnoldi process itself amplifies rounding there (cf. test_gpu_parity's
+    h_tolerance for the Chebyshev case)."""
+    r1 = krylov.run(op, b, q, func="sqrt", krylov="cgs2", stop="fixed", **kw)
+    orig = krylov.apply_q
+    try:
+        krylov.apply_q = _horner_np
+        r2 = krylov.run(op, b, q, func="sqrt", krylov="cgs2", stop="fixed", **kw)
+    finally:
+        krylov.apply_q = orig
+    gap = np.abs(r1.H - r2.H).max() / np.abs(r1.H).max()
+    return max(H_TOL, 10 * gap)
+
+
+@pytest.mark.parametrize("fmt,C_,sig", [("sell", 32, 256), ("sell", 32, 1), ("csr", 32, 1)])
+def test_graph_laplacian_sqrt(ctx, fmt, C_, sig):
+    """C7s (synthetic web-like digraph, n = 2000): real-arithmetic Newton chain
+    with the oracle's Ritz q from L b imported; x, H_m, m and mvms at the
+    estimate stop; the library's own real Ritz construction from L b agrees."""
+    from oracle import newton
+    cfg = configs.CONFIGS["C7s"]
+    A, b, _ = configs.build("C7s")
+    op = Operator(A.to_scipy())
+    qo, _, _ = newton.ritz_newton(op, op.matvec(b), 7)
+    res_o = krylov.run(op, b, qo, func="sqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                       tol=cfg.tol, check_every=4)
+    res_o.x = res_o.x.real
+    h_tol = _newton_h_tolerance(op, b, qo, m_max=res_o.m)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt=fmt, C_=C_, sigma=sig))
+    q = pp.Poly.newton(qo.nodes.real.astype(np.complex128), qo.dd.real.astype(np.complex128))
+    xg, rep = pp.run(ctx, M, q, dev(b), func="sqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                     tol=cfg.tol, check_every=4)
+    _check(ctx, res_o, xg, rep, h_tol=h_tol)
+    bd = dev(b)
+    Lb = torch.empty_like(bd)
+    M.spmv(bd, Lb)
+    ql = pp.Poly.ritz_newton(ctx, M, Lb, 7)
+    nodes = ql.export()["nodes"]
+    assert np.abs(nodes.imag).max() == 0.0
+    assert np.abs(np.sort(nodes.real) - np.sort(qo.nodes.real)).max() <= 1e-8 * qo.nodes.real.max()

@@ -283,3 +283,25 @@ def test_sign_function_overlap_kernel_dense(mu):
     # mvm unit of Table 2: 2 per application of Q^2
     per = 2 * (2 * q.deg + 1)
     assert res.mvms == 2 * q.deg + res.m * per + 1
+
+
+def test_graph_laplacian_sqrt_implicit_desingularisation():
+    """Ex. 6.3 setting: L = D_in - A is singular (zero column
+    sums) with a simple eigenvalue 0; L^{1/2} b = L^{-1/2}(L b) with the
+    Ritz-Newton q from L b works unchanged (Theorem 4.1): against
+    the dense Schur square root (scipy.linalg.sqrtm) and the invariant
+    L^{1/2}(L^{1/2} b) = L b."""
+    A, b, _ = configs.build("C7s")
+    S = A.to_scipy()
+    assert abs(np.asarray(S.sum(axis=0))).max() == 0.0
+    op = Operator(S)
+    q, _, _ = newton.ritz_newton(op, op.matvec(b), 7)
+    assert np.abs(q.nodes.imag).max() == 0.0 and q.nodes.real.min() > 0
+    res = krylov.run(op, b, q, func="sqrt", krylov="cgs2", m_max=200, stop="est", tol=1e-11)
+    assert res.term == "converged"
+    ref = sla.sqrtm(S.toarray()) @ b
+    assert np.linalg.norm(res.x - ref) <= 1e-8 * np.linalg.norm(ref)
+    twice = krylov.run(op, res.x.real, q, func="sqrt", krylov="cgs2", m_max=200, stop="est",
+                       tol=1e-11).x
+    Lb = op.matvec(b)
+    assert np.linalg.norm(twice - Lb) <= 1e-8 * np.linalg.norm(Lb)
