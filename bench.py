@@ -67,6 +67,9 @@ def parse():
     p.add_argument("--krylov", default=None, choices=["lanczos", "cgs2", "lanczos2p"],
                    help="override the config's Krylov method (lanczos2p = two-pass)")
     p.add_argument("--plain", action="store_true", help="no preconditioner (d = 1)")
+    p.add_argument("--newton-eval", default=None, choices=["horner", "basis"],
+                   help="Newton-form q on the device: Horner (P:354) or the forward basis "
+                        "(default: basis for the graph Laplacian, horner otherwise)")
     p.add_argument("--poly", default="config", choices=["config", "contour"],
                    help="contour: least-squares q on the circle |z - (4+m0)| = 2.2 (P:359-404; "
                         "Wilson configs)")
@@ -313,11 +316,14 @@ def main():
             # singular A (Thm 4.1): the Ritz values from A b, whose null-space
             # component is deflated (implicit desingularisation)
             M.spmv(bd, ritz_buf)
-            return pp.Poly.ritz_newton(ctx, M, ritz_buf, deg, power=power)
-        return pp.Poly.ritz_newton(ctx, M, bd, deg, power=power)
+            q = pp.Poly.ritz_newton(ctx, M, ritz_buf, deg, power=power)
+        else:
+            q = pp.Poly.ritz_newton(ctx, M, bd, deg, power=power)
+        return q.set_newton_eval(newton_eval)
 
     krylov_m = args.krylov or cfg.krylov
     power = 2 if cfg.func in ("sign", "invsqrt_sq") else 1
+    newton_eval = args.newton_eval or ("basis" if cfg.family == "graph" else "horner")
     run_kw = dict(func=cfg.func, krylov=krylov_m, m_max=cfg.m_max, stop="est", tol=cfg.tol,
                   check_every=args.check_every, record_history=False, precond=args.precond)
     q0 = make_q()
@@ -424,6 +430,7 @@ def main():
                    "precond": "none (plain, d = 1)" if args.plain else args.precond,
                    "poly": "contour-LS circle |z-(4+m0)|=2.2, N=128" if args.poly == "contour"
                    else cfg.poly,
+                   "newton_eval": newton_eval if cfg.poly == "ritz" else None,
                    "krylov": krylov_m, "check_every": args.check_every, "tol": cfg.tol,
                    "format": args.fmt, "sell_sigma": sigma, "sell_split": split,
                    "m": m_iter, "mvms": reps[-1].mvms, "n": A.n, "nnz": A.nnz,

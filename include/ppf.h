@@ -223,6 +223,13 @@ ppf_status ppf_poly_eval(const ppf_poly* q, int npts, const double* z, double* o
 ppf_status ppf_poly_apply_bytes(ppf_ctx* ctx, const ppf_mat* A, size_t* bytes);
 ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const void* x, void* y,
                           void* work, size_t work_bytes);
+/* ppf_poly_set_newton_eval: how the device applies a Newton-form q.
+ *   mode 0 (default): Horner, w = (A - theta_j) w + dd_j v (the paper's "Horner-type
+ *   scheme"); mode 1: the forward Newton basis p_{j+1} = (A - theta_j) p_j with
+ *   sum dd_j p_j accumulated as a second output of each SpMV (one more vector
+ *   stream per launch), numerically preferable when spec(A) extends far beyond
+ *   the nodes (Q28).  Same deg SpMV launches.  Chebyshev: ignored. */
+ppf_status ppf_poly_set_newton_eval(ppf_poly* q, int mode);
 void ppf_poly_destroy(ppf_poly* q);
 
 /* ----------------------------------------------------------------------------

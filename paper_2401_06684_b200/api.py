@@ -202,6 +202,11 @@ class Poly:
                                               C.byref(h)))
         return cls(h)
 
+    def set_newton_eval(self, mode: str) -> "Poly":
+        """ppf_poly_set_newton_eval: "horner" (P:354, default) or "basis"."""
+        check(_lib().ppf_poly_set_newton_eval(self.h, {"horner": 0, "basis": 1}[mode]))
+        return self
+
     @classmethod
     def contour_ls(cls, points, deg: int) -> "Poly":
         """least-squares q on the contour points (complex array)."""

@@ -624,6 +624,14 @@ ppf_status ppf_poly_contour_ls(const double* points, int npts, int deg, double* 
   PPF_API_END
 }
 
+ppf_status ppf_poly_set_newton_eval(ppf_poly* q, int mode) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(q, "NULL polynomial");
+  PPF_REQUIRE(mode == 0 || mode == 1, "mode must be 0 (Horner) or 1 (forward Newton basis)");
+  q->newton_eval = mode;
+  PPF_API_END
+}
+
 void ppf_poly_destroy(ppf_poly* q) { delete q; }
 
 // ---------------------------------------------------------------------------

@@ -26,6 +26,9 @@ template <typename T> struct EpiT {
   const T* z;
   const T* u;
   const T* xe;  // vector of the s_x term: the SpMV input, or Epi::xe (squared operator)
+  T* acc;       // second output (ACC kernels): acc = (acc_init ? s_acc0 xe : acc) + s_acc out
+  T s_acc, s_acc0;
+  bool acc_init;
 };
 
 template <typename T> EpiT<T> to_epi(const Epi& e, const void* x) {
@@ -37,6 +40,10 @@ template <typename T> EpiT<T> to_epi(const Epi& e, const void* x) {
   r.z = static_cast<const T*>(e.z);
   r.u = static_cast<const T*>(e.u);
   r.xe = static_cast<const T*>(e.xe ? e.xe : x);
+  r.acc = static_cast<T*>(e.acc);
+  r.s_acc = s_from<T>(e.s_acc[0], e.s_acc[1]);
+  r.s_acc0 = s_from<T>(e.s_acc0[0], e.s_acc0[1]);
+  r.acc_init = e.acc_init;
   return r;
 }
 
@@ -91,6 +98,13 @@ __device__ __forceinline__ T epilogue(const EpiT<T>& e, T ax, const T* __restric
   return r;
 }
 
+// second output of the forward-Newton-basis chain: acc += s_acc * r
+template <typename T>
+__device__ __forceinline__ void acc_update(const EpiT<T>& e, int64_t row, T r) {
+  const T base = e.acc_init ? s_mul(e.s_acc0, ldg(e.xe + row)) : e.acc[row];
+  e.acc[row] = s_fma(e.s_acc, r, base);
+}
+
 // ---------------------------------------------------------------------------
 // SELL-C-sigma SpMV + fused epilogue.  KS warps per slice, one row per lane.
 //
@@ -110,7 +124,7 @@ __device__ __forceinline__ T epilogue(const EpiT<T>& e, T ax, const T* __restric
 // latency-bound at 5.2 TB/s (ncu: 36% "mem busy", 60 warps/SM active) instead
 // of 6.5 TB/s.
 // ---------------------------------------------------------------------------
-template <typename T, int KS, bool PERM>
+template <typename T, int KS, bool PERM, bool ACC = false>
 __global__ void __launch_bounds__(256, 3) sell1_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
@@ -160,13 +174,15 @@ __global__ void __launch_bounds__(256, 3) sell1_kernel(int64_t nslices, int64_t 
   const int64_t pos = slice * 32 + lane;
   if (pos < n) {
     const int64_t row = PERM ? int64_t(perm[pos]) : pos;
-    out[row] = epilogue(e, acc, x, row, has_x);
+    const T r = epilogue(e, acc, x, row, has_x);
+    out[row] = r;
+    if constexpr (ACC) acc_update(e, row, r);
   }
 }
 
 // two rows per lane, 128-bit loads of (val, val) and (col, col); C = 64, fp64;
 // KS warps per slice as in sell1_kernel
-template <int KS>
+template <int KS, bool ACC = false>
 __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
@@ -230,15 +246,21 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
       r.y = fma(e.s_u, uv.y, r.y);
     }
     *reinterpret_cast<double2*>(out + r0) = r;
+    if constexpr (ACC) {
+      acc_update(e, r0, r.x);
+      acc_update(e, r0 + 1, r.y);
+    }
   } else if (r0 < n) {
-    out[r0] = epilogue(e, a0, x, r0, has_x);
+    const double r = epilogue(e, a0, x, r0, has_x);
+    out[r0] = r;
+    if constexpr (ACC) acc_update(e, r0, r);
   }
 }
 
 // ---------------------------------------------------------------------------
 // CSR SpMV + fused epilogue, G lanes per row.
 // ---------------------------------------------------------------------------
-template <typename T, int G>
+template <typename T, int G, bool ACC = false>
 __global__ void __launch_bounds__(256) csr_kernel(int64_t n, const int64_t* __restrict__ rp,
                                                   const int32_t* __restrict__ col,
                                                   const T* __restrict__ val,
@@ -264,7 +286,11 @@ __global__ void __launch_bounds__(256) csr_kernel(int64_t n, const int64_t* __re
       acc = s_add(acc, reinterpret_cast<T&>(t));
     }
   }
-  if (lg == 0) out[row] = epilogue(e, acc, x, row, has_x);
+  if (lg == 0) {
+    const T r = epilogue(e, acc, x, row, has_x);
+    out[row] = r;
+    if constexpr (ACC) acc_update(e, row, r);
+  }
 }
 
 // halo: out[rows[i]] += s_ax * sum val * recv[col]
@@ -827,6 +853,15 @@ __global__ void __launch_bounds__(256) lanczos_regen_kernel(int64_t n, T* __rest
   }
 }
 
+// acc = (acc_init ? s_acc0 xe : acc) + s_acc out, as a separate sweep (the
+// sharded SpMV completes `out` only after its halo block)
+template <typename T>
+__global__ void __launch_bounds__(256) acc_kernel(int64_t n, const T* __restrict__ out, EpiT<T> e) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    acc_update(e, i, ldg(out + i));
+}
+
 int blocks_for(int64_t n, int threads, int cap) {
   int64_t b = (n + threads - 1) / threads;
   if (b > cap) b = cap;
@@ -848,6 +883,44 @@ static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStrea
   const T* xt = static_cast<const T*>(x);
   T* ot = static_cast<T*>(out);
   const T* val = static_cast<const T*>(A->d_val);
+  if (e.acc) {
+    // forward-Newton-basis chain step: KS = 1, second output acc
+    if (A->fmt == PPF_FMT_SELL) {
+      const int blocks = int((A->nslices + 7) / 8);
+      if (blocks == 0) return;
+      if constexpr (sizeof(T) == 8) {
+        if (A->C == 64) {
+          sell2_kernel<1, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
+                                                        reinterpret_cast<const double*>(val), xt, ot,
+                                                        et, has_x);
+          post_launch("sell2_kernel");
+          return;
+        }
+      }
+      if (A->d_perm)
+        sell1_kernel<T, 1, true, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr,
+                                                               A->d_col, val, xt, ot, et, has_x,
+                                                               A->d_perm);
+      else
+        sell1_kernel<T, 1, false, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr,
+                                                                A->d_col, val, xt, ot, et, has_x,
+                                                                nullptr);
+      post_launch("sell1_kernel");
+    } else {
+      const int G = A->csr_group;
+      const int blocks = int((A->n_local * G + 255) / 256);
+      if (blocks == 0) return;
+      switch (G) {
+        case 2: csr_kernel<T, 2, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
+        case 4: csr_kernel<T, 4, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
+        case 8: csr_kernel<T, 8, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
+        case 16: csr_kernel<T, 16, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
+        default: csr_kernel<T, 32, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
+      }
+      post_launch("csr_kernel");
+    }
+    return;
+  }
   if (A->fmt == PPF_FMT_SELL) {
     const int KS = A->sell_ks;
     const int64_t spb = 8 / KS;  // slices per 256-thread block
@@ -915,6 +988,17 @@ void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_
     spmv_t<double>(A, x, out, e, st);
   else
     spmv_t<cplx>(A, x, out, e, st);
+}
+
+void launch_acc(ppf_mat* A, const void* x, const void* out, const Epi& e, cudaStream_t st) {
+  const int blocks = blocks_for(A->n_local, 256, 148 * 8);
+  if (A->dtype == PPF_R64)
+    acc_kernel<double><<<blocks, 256, 0, st>>>(A->n_local, static_cast<const double*>(out),
+                                               to_epi<double>(e, x));
+  else
+    acc_kernel<cplx><<<blocks, 256, 0, st>>>(A->n_local, static_cast<const cplx*>(out),
+                                             to_epi<cplx>(e, x));
+  post_launch("acc_kernel");
 }
 
 void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st) {

@@ -153,6 +153,7 @@ struct ppf_poly {
   double a, b;                      // Chebyshev interval
   std::vector<double> c;            // Chebyshev coefficients c_0..c_deg
   std::vector<ppf::zc> nodes, dd;   // Newton form (Leja order)
+  int newton_eval = 0;              // 0: Horner, 1: forward Newton basis
 };
 
 namespace ppf {
@@ -228,11 +229,18 @@ struct Epi {          // out = s_ax*(A x) + s_x*xe + s_z*z + s_u*u
   const void* z;      // may be null (s_z ignored)
   const void* u;      // may be null (s_u ignored)
   const void* xe = nullptr;  // null: xe = x (the SpMV input); set for A = Q^2 chains
+  // optional second output (forward Newton basis, Newton-eval mode 1):
+  //   acc = (acc_init ? s_acc0*xe : acc) + s_acc*out
+  void* acc = nullptr;
+  double s_acc[2] = {0.0, 0.0}, s_acc0[2] = {0.0, 0.0};
+  bool acc_init = false;
 };
 
 int auto_sell_ks(const ppf_mat* m, int num_sms);
 void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st);
 void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
+// the second output of an Epi with acc set, from a completed `out` (x: the SpMV input)
+void launch_acc(ppf_mat* A, const void* x, const void* out, const Epi& e, cudaStream_t st);
 void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st);
 // run.cpp: the sharded SpMV with communication/compute overlap
 void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e);

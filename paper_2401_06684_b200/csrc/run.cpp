@@ -156,9 +156,12 @@ void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e)
     halo_sendrecv(ctx, A, ctx->comm_stream);
     PPF_CUDA(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
   }
-  launch_spmv(A, x, out, e, st);
+  Epi ed = e;
+  ed.acc = nullptr;  // the second output needs the complete out: after the halo block
+  launch_spmv(A, x, out, ed, st);
   if (A->send_total || A->halo_total) PPF_CUDA(cudaStreamWaitEvent(st, ctx->ev_halo, 0));
   if (A->halo_rows) launch_halo_apply(A, out, e.s_ax, st);
+  if (e.acc) launch_acc(A, x, out, e, st);
 }
 
 namespace {
@@ -369,6 +372,33 @@ struct Runner {
         spmv(T[cur], out, epi(alpha, beta, 0.0, nullptr, c[0] - c[d], in));
       else
         spmv(T[cur], out, epi(alpha, beta, -1.0, T[prev], c[0], in));
+    } else if (q->newton_eval == 1) {
+      // forward Newton basis: p_0 = v, p_{j+1} = (A - theta_j) p_j,
+      // out = sum_j dd_j p_j accumulated by the SpMV's second output (the
+      // first step initialises out = dd_0 v + dd_1 p_1); the basis is
+      // numerically preferable to Horner when spec(A) reaches far beyond the
+      // nodes (the graph Laplacian, Q28)
+      const auto& dd = q->dd;
+      const auto& th = q->nodes;
+      if (d == 0) {
+        lincomb(in, out, dd[0]);
+        return;
+      }
+      const void* src = in;
+      for (int j = 0; j < d; ++j) {
+        void* dst = T[j % 2];
+        Epi e = epi(1.0, -th[j], 0.0, nullptr, 0.0, nullptr);
+        e.acc = out;
+        e.s_acc[0] = dd[j + 1].real();
+        e.s_acc[1] = dd[j + 1].imag();
+        if (j == 0) {
+          e.acc_init = true;
+          e.s_acc0[0] = dd[0].real();
+          e.s_acc0[1] = dd[0].imag();
+        }
+        spmv(src, dst, e);
+        src = dst;
+      }
     } else {
       // Horner on the Newton form: w = dd_d v; w = (A - theta_j) w + dd_j v, j = d-1..0
       const auto& dd = q->dd;

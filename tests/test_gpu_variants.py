@@ -300,3 +300,72 @@ def test_graph_laplacian_sqrt(ctx, fmt, C_, sig):
     nodes = ql.export()["nodes"]
     assert np.abs(nodes.imag).max() == 0.0
     assert np.abs(np.sort(nodes.real) - np.sort(qo.nodes.real)).max() <= 1e-8 * qo.nodes.real.max()
+
+
+@pytest.mark.parametrize("deg", [1, 2, 7, 16])
+@pytest.mark.parametrize("which", ["wilson", "graph"])
+def test_newton_forward_basis_chain(ctx, deg, which):
+    """Newton-eval mode "basis" (the forward Newton basis with the sum carried
+    as the SpMV's second output) against the oracle's forward Newton basis
+    (P:354 form, same arithmetic order), complex and real operators."""
+    from oracle import newton
+    rng = np.random.default_rng(deg)
+    if which == "wilson":
+        A = ops.wilson_dirac(3, -1.0, seed=9)
+        th = 3.0 + 1.5 * rng.random(deg + 1) * np.exp(2j * np.pi * rng.random(deg + 1))
+        v = rng.standard_normal(A.n) + 1j * rng.standard_normal(A.n)
+    else:
+        A, _, _ = configs.build("C7s")
+        th = np.sort(50 + 500 * rng.random(deg + 1)).astype(np.complex128)
+        v = rng.standard_normal(A.n)
+    qo = newton.from_nodes(th)
+    if which == "graph":
+        qo.nodes, qo.dd = qo.nodes.real.astype(np.complex128), qo.dd.real.astype(np.complex128)
+    q = pp.Poly.newton(qo.nodes, qo.dd).set_newton_eval("basis")
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A))
+    got = host(q.apply(ctx, M, dev(v)))
+    ref = newton.apply(qo, Operator(A.to_scipy()), v)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_graph_laplacian_forward_basis_run(ctx):
+    """C7s with the forward-basis Newton chain (the oracle's scheme): x and m
+    exact, H within 10x the oracle's own sensitivity to SpMV summation order."""
+    from oracle import newton
+    cfg = configs.CONFIGS["C7s"]
+    A, b, _ = configs.build("C7s")
+    op = Operator(A.to_scipy())
+    qo, _, _ = newton.ritz_newton(op, op.matvec(b), 7)
+    res_o = krylov.run(op, b, qo, func="sqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                       tol=cfg.tol, check_every=4)
+    res_o.x = res_o.x.real
+    # H bar: 1e-11, raised to 10x the gap between two oracle runs that differ
+    # only in the summation order inside each mat-vec (entries of every row
+    # reversed): this operator's Arnoldi process amplifies SpMV rounding
+    import scipy.sparse as sp
+    S = A.to_scipy()
+    rows = np.repeat(np.arange(A.n), np.diff(S.indptr))
+    k = np.arange(S.nnz) - S.indptr[rows]
+    rp = S.indptr[rows + 1] - 1 - k                       # each row's entries reversed
+    Srev = sp.csr_matrix((S.data[rp], S.indices[rp], S.indptr), shape=S.shape)
+    op_rev = Operator(Srev)
+    assert np.abs(op_rev.matvec(b) - op.matvec(b)).max() <= 1e-12 * np.abs(op.matvec(b)).max()
+
+    class _Rev:
+        mvms = 0
+        dtype = op.dtype
+        n = op.n
+
+        def matvec(self, x):
+            _Rev.mvms += 1
+            return op_rev.matvec(x)
+    r2 = krylov.run(_Rev(), b, qo, func="sqrt", krylov="cgs2", m_max=res_o.m, stop="fixed")
+    gap = np.abs(r2.H - res_o.H).max() / np.abs(res_o.H).max()
+    h_tol = max(H_TOL, 10 * gap)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32, sigma=2016))
+    q = pp.Poly.newton(qo.nodes.real.astype(np.complex128), qo.dd.real.astype(np.complex128))
+    q.set_newton_eval("basis")
+    xg, rep = pp.run(ctx, M, q, dev(b), func="sqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                     tol=cfg.tol, check_every=4)
+    _check(ctx, res_o, xg, rep, h_tol=h_tol)
+    assert h_tol < 1e-8          # the same scheme as the oracle: far tighter than Horner's
