@@ -653,6 +653,10 @@ ppf_status ppf_dense_invsqrt_e1(ppf_dtype dtype, int m, const void* H, int ld, d
       yo[i * ND] = yy[i];
       if (ND == 2) yo[i * ND + 1] = 0.0;
     }
+  } else if (ND == 1) {  // real Hessenberg: the real Schur route
+    std::vector<double> yy(m);
+    real_invsqrt_e1(m, h, ld, beta0, yy.data());
+    for (int i = 0; i < m; ++i) yo[i] = yy[i];
   } else {
     std::vector<zc> A(size_t(m) * m), yy;
     for (int j = 0; j < m; ++j)

@@ -207,6 +207,9 @@ void tridiag_invsqrt_e1(int m, const double* d, const double* e, double beta0, d
 void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q);
 // y = beta0 * H^{-1/2} e1 via Schur -> triangular sqrt -> solve.
 void general_invsqrt_e1(int m, const std::vector<zc>& H, double beta0, std::vector<zc>& y);
+// y = beta0 * H^{-1/2} e1 for a REAL upper Hessenberg H (column-major, ld ldh):
+// real Schur (Francis double shift) -> quasi-triangular square root -> solve.
+void real_invsqrt_e1(int m, const double* H, int ldh, double beta0, double* y);
 // Eigenvalues of a general complex m x m matrix (column-major).
 std::vector<zc> eigenvalues(int m, std::vector<zc> H);
 

@@ -588,6 +588,21 @@ std::vector<zc> dense_y(const std::vector<zc>& Hh, int rows, int m, double beta0
     tridiag_invsqrt_e1(m, d.data(), e.data(), beta0, yy.data());
     for (int i = 0; i < m; ++i) y[i] = yy[i];
   } else {
+    bool real = true;
+    for (int jj = 0; jj < m && real; ++jj)
+      for (int i = 0; i < m; ++i)
+        if (Hh[size_t(i) + size_t(jj) * rows].imag() != 0.0) {
+          real = false;
+          break;
+        }
+    if (real) {  // a real operator's Arnoldi matrix: real Schur route (dense.cpp)
+      std::vector<double> Hr(size_t(m) * m), yy(m);
+      for (int jj = 0; jj < m; ++jj)
+        for (int i = 0; i < m; ++i) Hr[size_t(i) + size_t(jj) * m] = Hh[size_t(i) + size_t(jj) * rows].real();
+      real_invsqrt_e1(m, Hr.data(), m, beta0, yy.data());
+      for (int i = 0; i < m; ++i) y[i] = yy[i];
+      return y;
+    }
     std::vector<zc> Hm(size_t(m) * m);
     for (int jj = 0; jj < m; ++jj)
       for (int i = 0; i < m; ++i) Hm[size_t(i) + size_t(jj) * m] = Hh[size_t(i) + size_t(jj) * rows];

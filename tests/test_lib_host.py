@@ -136,6 +136,53 @@ def test_dense_schur_matches_oracle(m):
     assert np.linalg.norm(yc - refc) <= 1e-11 * np.linalg.norm(refc)
 
 
+@pytest.mark.parametrize("m", [2, 3, 7, 25, 60, 130])
+@pytest.mark.parametrize("kind", ["real_eigs", "complex_pairs", "stiff"])
+def test_dense_real_schur_matches_oracle(m, kind):
+    """Real Hessenberg H (a real operator's Arnoldi matrix): the library's real
+    Schur route (Francis double shift, quasi-triangular square root) against
+    the oracle's eigendecomposition, with real eigenvalues, complex pairs and a
+    wide spectrum; and against the complex Schur route of the same matrix."""
+    rng = np.random.default_rng(7 * m + len(kind))
+    H = np.triu(rng.standard_normal((m, m)), -1)
+    if kind == "real_eigs":
+        H = np.triu(rng.random((m, m)), -1) * 0.2 + np.diag(np.linspace(0.5, 3.0, m))
+    elif kind == "complex_pairs":
+        H += np.diag(np.full(m, 2.0 * np.sqrt(m)))
+    else:
+        H = (np.triu(rng.random((m, m)), 1) * 0.3 + np.diag(rng.random(m - 1) * 0.01, -1)
+             + np.diag(np.geomspace(0.05, 5e3, m)))
+    ev = np.linalg.eigvals(H)
+    assert not np.any((np.abs(ev.imag) < 1e-12) & (ev.real <= 0))
+    y = dense_invsqrt_e1(H, 0.7, hermitian=False)
+    ref = dense.invsqrt_e1(H.astype(np.complex128), 0.7, hermitian=False)
+    assert np.linalg.norm(y - ref) <= 1e-11 * np.linalg.norm(ref)
+    yc = dense_invsqrt_e1(H.astype(np.complex128), 0.7, hermitian=False)
+    assert np.linalg.norm(y - yc) <= 1e-11 * np.linalg.norm(yc)
+
+
+@pytest.mark.parametrize("m", [30, 60])
+def test_dense_real_schur_nearly_symmetric(m):
+    """CGS2-Arnoldi matrix of a symmetric operator (C1, plain method): a real
+    Hessenberg with converged 2x2 blocks whose off-diagonals are ~1e-15 --
+    the case that needs the cancellation-free 2x2 standardisation."""
+    from oracle import krylov
+    from oracle.spmv import Operator
+    A, b, iv = configs.build("C1")
+    r = krylov.run(Operator(A.to_scipy()), b, chebyshev.coefficients(*iv, 0), krylov="cgs2",
+                   m_max=m)
+    H = r.H[:m, :m].real.copy()
+    y = dense_invsqrt_e1(H, r.beta0, hermitian=False)
+    assert np.linalg.norm(y - r.y) <= 1e-12 * np.linalg.norm(r.y)
+
+
+def test_dense_real_schur_branch_cut():
+    H = np.array([[1.0, 2.0, 0.0], [1.0, -3.0, 1.0], [0.0, 0.5, 2.0]])
+    assert np.any(np.linalg.eigvals(H).real < 0)
+    with pytest.raises(_lib.PPFError):
+        dense_invsqrt_e1(H, 1.0, hermitian=False)
+
+
 def test_dense_branch_cut_rejected():
     with pytest.raises(_lib.PPFError) as e:
         dense_invsqrt_e1(np.diag([1.0, -2.0]), 1.0, hermitian=True)
