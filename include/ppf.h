@@ -102,6 +102,24 @@ int ppf_abi_version(void);
  *   ppf_spmv then return PPF_ESTATE.  nranks == 1 ignores id128.
  * ------------------------------------------------------------------------- */
 ppf_status ppf_nccl_unique_id(void* out128);
+/* Host transport (nranks > 1 without NCCL): the caller moves the halo and sums
+ * the reductions itself, e.g. over torch.distributed/gloo -- used to verify the
+ * sharded algorithm with several processes on one device.  The library stages
+ * through pinned host memory and synchronises the stream around each call:
+ *   exchange(user, send, send_counts, recv, recv_counts): send holds this
+ *     rank's packed boundary entries, per-peer segments in peer order,
+ *     send_counts[p] doubles each (complex: 2 per entry); fill recv likewise
+ *     (recv_counts[p] doubles from peer p, peer order);
+ *   allreduce_sum(user, buf, count): in-place sum over all ranks.
+ * Both return 0 on success (anything else -> PPF_ENCCL).  The function
+ * pointers must stay valid for the context's lifetime; NULL clears. */
+typedef struct {
+  void* user;
+  int (*exchange)(void* user, const double* send, const int64_t* send_counts, double* recv,
+                  const int64_t* recv_counts);
+  int (*allreduce_sum)(void* user, double* buf, int64_t count);
+} ppf_transport;
+ppf_status ppf_ctx_set_transport(ppf_ctx* ctx, const ppf_transport* transport);
 ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128,
                           void* cuda_stream, ppf_ctx** out);
 void ppf_ctx_destroy(ppf_ctx* ctx);

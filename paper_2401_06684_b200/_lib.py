@@ -35,6 +35,15 @@ class Opts(C.Structure):
                 ("precond", C.c_int)]
 
 
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                          C.POINTER(C.c_double), C.POINTER(C.c_int64))
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+
+
+class Transport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("exchange", EXCHANGE_FN), ("allreduce_sum", ALLREDUCE_FN)]
+
+
 class Report(C.Structure):
     _fields_ = [("iterations", C.c_int), ("term", C.c_int), ("mvms", C.c_longlong),
                 ("inner_products", C.c_longlong), ("est", C.c_double), ("err", C.c_double),
@@ -61,6 +70,7 @@ SIGNATURES = {
     "ppf_mat_create": (C.c_int, [vp, vp, vp, C.c_size_t, C.POINTER(vp)]),
     "ppf_spmv": (C.c_int, [vp, vp, vp, vp]),
     "ppf_mat_set_split": (C.c_int, [vp, C.c_int, C.POINTER(C.c_int)]),
+    "ppf_ctx_set_transport": (C.c_int, [vp, C.POINTER(Transport)]),
     "ppf_mat_destroy": (None, [vp]),
     "ppf_halo_pack": (C.c_int, [vp, vp, vp]),
     "ppf_halo_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),

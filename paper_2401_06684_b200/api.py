@@ -49,6 +49,40 @@ class Context:
         check(_lib().ppf_ctx_create(device, rank, nranks, idbuf, _stream_handle(self.stream),
                                     C.byref(h)))
         self.h = h
+        self.rank, self.nranks = rank, nranks
+
+    def set_transport(self, exchange, allreduce_sum):
+        """ppf_ctx_set_transport: host-side halo exchange / sum over ranks.
+
+        exchange(send: ndarray, send_counts: list, recv: ndarray, recv_counts: list)
+        fills ``recv`` (float64, per-peer segments in peer order); allreduce_sum(buf)
+        sums ``buf`` (float64) over all ranks in place.  Exceptions -> nonzero."""
+        nr = self.nranks
+
+        def _ex(user, send, sc, recv, rc):
+            try:
+                scount = [int(sc[p]) for p in range(nr)]
+                rcount = [int(rc[p]) for p in range(nr)]
+                s_arr = np.ctypeslib.as_array(send, shape=(max(1, sum(scount)),))[: sum(scount)]
+                r_arr = np.ctypeslib.as_array(recv, shape=(max(1, sum(rcount)),))[: sum(rcount)]
+                exchange(s_arr, scount, r_arr, rcount)
+                return 0
+            except Exception:  # pragma: no cover - reported as PPF_ENCCL
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def _ar(user, buf, count):
+            try:
+                allreduce_sum(np.ctypeslib.as_array(buf, shape=(int(count),)))
+                return 0
+            except Exception:  # pragma: no cover
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._transport = L.Transport(None, L.EXCHANGE_FN(_ex), L.ALLREDUCE_FN(_ar))
+        check(_lib().ppf_ctx_set_transport(self.h, C.byref(self._transport)))
 
     def close(self):
         if self.h:

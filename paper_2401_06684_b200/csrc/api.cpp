@@ -132,6 +132,21 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
   PPF_API_END
 }
 
+ppf_status ppf_ctx_set_transport(ppf_ctx* c, const ppf_transport* t) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(c, "NULL ctx");
+  if (!t) {
+    c->has_transport = false;
+    return PPF_OK;
+  }
+  PPF_REQUIRE(c->nranks > 1, "a transport needs nranks > 1");
+  PPF_REQUIRE(!c->nccl_comm, "context already has an NCCL communicator");
+  PPF_REQUIRE(t->exchange && t->allreduce_sum, "NULL transport function");
+  c->transport = *t;
+  c->has_transport = true;
+  PPF_API_END
+}
+
 ppf_status ppf_profile_enable(ppf_ctx* c, int on) {
   PPF_API_BEGIN
   PPF_REQUIRE(c, "NULL ctx");
@@ -154,6 +169,7 @@ void ppf_ctx_destroy(ppf_ctx* c) {
   for (auto e : c->prof_pool) cudaEventDestroy(e);
   if (c->nccl_comm) ncclCommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->t_host) cudaFreeHost(c->t_host);
   if (c->ev) cudaEventDestroy(c->ev);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);

@@ -175,6 +175,11 @@ struct ppf_ctx {
   // `stream`; ev_pack / ev_halo order the two streams
   cudaStream_t comm_stream;
   cudaEvent_t ev_pack, ev_halo;
+  // host transport (ppf_ctx_set_transport) instead of NCCL
+  bool has_transport = false;
+  ppf_transport transport{};
+  void* t_host = nullptr;      // pinned staging for halo send + recv / reductions
+  size_t t_host_bytes = 0;
   int num_sms;
   // pinned host staging for H columns and y
   void* h_pinned;

@@ -146,8 +146,54 @@ void halo_sendrecv(ppf_ctx* ctx, ppf_mat* A, cudaStream_t cs) {
 // The halo block adds s_ax * A_offdiag x_halo to out (the epilogue is linear
 // in A x, so the split is exact).  Buffer reuse is ordered by the streams:
 // the next pack (stream) follows this halo block, which followed ev_halo.
+// pinned host staging of the host transport, grown on demand
+static double* transport_stage(ppf_ctx* ctx, size_t bytes) {
+  if (ctx->t_host_bytes < bytes) {
+    PPF_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->t_host) PPF_CUDA(cudaFreeHost(ctx->t_host));
+    ctx->t_host = nullptr;
+    ctx->t_host_bytes = 0;
+    PPF_CUDA(cudaHostAlloc(&ctx->t_host, bytes, cudaHostAllocDefault));
+    ctx->t_host_bytes = bytes;
+  }
+  return static_cast<double*>(ctx->t_host);
+}
+
+// the halo exchange through the caller's host transport (no overlap: a
+// verification path, see ppf_ctx_set_transport)
+static void halo_transport(ppf_ctx* ctx, ppf_mat* A, const void* x) {
+  cudaStream_t st = ctx->stream;
+  const size_t sc = A->dtype == PPF_R64 ? 8 : 16;
+  const int nd = int(sc / 8);
+  launch_halo_pack(A, x, st);
+  double* hs = transport_stage(ctx, size_t(A->send_total + A->halo_total) * sc + 64);
+  double* hr = hs + size_t(A->send_total) * nd;
+  if (A->send_total)
+    PPF_CUDA(cudaMemcpyAsync(hs, A->d_send, size_t(A->send_total) * sc, cudaMemcpyDeviceToHost, st));
+  PPF_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> scount(A->nranks), rcount(A->nranks);
+  for (int p = 0; p < A->nranks; ++p) {
+    scount[p] = A->send_count[p] * nd;
+    rcount[p] = A->recv_count[p] * nd;
+  }
+  if (ctx->transport.exchange(ctx->transport.user, hs, scount.data(), hr, rcount.data()) != 0)
+    fail(PPF_ENCCL, "transport exchange failed");
+  if (A->halo_total)
+    PPF_CUDA(cudaMemcpyAsync(A->d_recv, hr, size_t(A->halo_total) * sc, cudaMemcpyHostToDevice, st));
+  PPF_CUDA(cudaStreamSynchronize(st));  // the staging is reused by the next call
+}
+
 void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e) {
   cudaStream_t st = ctx->stream;
+  if (ctx->has_transport) {
+    halo_transport(ctx, A, x);
+    Epi ed = e;
+    ed.acc = nullptr;
+    launch_spmv(A, x, out, ed, st);
+    if (A->halo_rows) launch_halo_apply(A, out, e.s_ax, st);
+    if (e.acc) launch_acc(A, x, out, e, st);
+    return;
+  }
   if (A->send_total || A->halo_total) {
     if (!ctx->comm_stream) fail(PPF_ESTATE, "nranks > 1 needs a context with an NCCL communicator");
     launch_halo_pack(A, x, st);
@@ -185,9 +231,18 @@ struct Runner {
   // then finalise them (sqrt, H entries, 1/norm) on the device; no-op on 1 rank.
   void reduce_fin(int op, int nv, void* o0, void* o1, void* o2, const void* ci) {
     if (!dist) return;
-    if (ncclAllReduce(rs.raw, rs.raw, size_t(nv), ncclDouble, ncclSum,
-                      static_cast<ncclComm_t>(ctx->nccl_comm), st) != ncclSuccess)
+    if (ctx->has_transport) {
+      double* hb = transport_stage(ctx, size_t(nv) * 8 + 64);
+      PPF_CUDA(cudaMemcpyAsync(hb, rs.raw, size_t(nv) * 8, cudaMemcpyDeviceToHost, st));
+      PPF_CUDA(cudaStreamSynchronize(st));
+      if (ctx->transport.allreduce_sum(ctx->transport.user, hb, nv) != 0)
+        fail(PPF_ENCCL, "transport allreduce failed");
+      PPF_CUDA(cudaMemcpyAsync(rs.raw, hb, size_t(nv) * 8, cudaMemcpyHostToDevice, st));
+      PPF_CUDA(cudaStreamSynchronize(st));
+    } else if (ncclAllReduce(rs.raw, rs.raw, size_t(nv), ncclDouble, ncclSum,
+                             static_cast<ncclComm_t>(ctx->nccl_comm), st) != ncclSuccess) {
       fail(PPF_ENCCL, "ncclAllReduce");
+    }
     timed(2, 0.0, [&] { launch_finalize(op, nv, int(sc / 8), rs.raw, o0, o1, o2, ci, st); });
   }
 
@@ -210,7 +265,8 @@ struct Runner {
     rs.max_blocks = L.max_blocks;
     dist = A->nranks > 1;
     if (dist) {
-      if (!c->nccl_comm) fail(PPF_ESTATE, "nranks > 1 needs a context with an NCCL communicator");
+      if (!c->nccl_comm && !c->has_transport)
+        fail(PPF_ESTATE, "nranks > 1 needs a context with an NCCL communicator or a transport");
       rs.raw = reinterpret_cast<double*>(w + L.raw);
     }
     grid_vec = std::min(L.max_blocks, 4 * c->num_sms);
