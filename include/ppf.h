@@ -120,6 +120,11 @@ typedef struct {
   int (*allreduce_sum)(void* user, double* buf, int64_t count);
 } ppf_transport;
 ppf_status ppf_ctx_set_transport(ppf_ctx* ctx, const ppf_transport* transport);
+/* ppf_ctx_set_graphs: with left preconditioning (one-pass, one rank, profiling
+ * off) ppf_run captures the step's q(A)q(A) chain -- its 2 deg fused SpMV
+ * launches between fixed buffers -- once as a CUDA graph and replays it every
+ * step (default on).  Results are bitwise identical either way. */
+ppf_status ppf_ctx_set_graphs(ppf_ctx* ctx, int on);
 ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128,
                           void* cuda_stream, ppf_ctx** out);
 void ppf_ctx_destroy(ppf_ctx* ctx);

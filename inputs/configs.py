@@ -63,6 +63,9 @@ CONFIGS = {
     # scaled-down members of the same families (oracle finishes in seconds)
     "C3s": Config("C3s", "laplacian", dict(N=30, dim=3), "invsqrt", (10, 20), "lanczos", "chebyshev",
                   1e-8, 80, 203),
+    # L2-resident member of the C4 family (micro-benchmarks of the SpMV chain)
+    "C4m": Config("C4m", "convdiff", dict(N=80, dim=3, beta=(10.0, 10.0, 10.0)), "sqrt", (20,), "cgs2",
+                  "chebyshev", 1e-8, 60, 404),
     "C4s": Config("C4s", "convdiff", dict(N=32, dim=3, beta=(10.0, 10.0, 10.0)), "sqrt", (20, 5), "cgs2",
                   "chebyshev", 1e-8, 60, 204),
     "C6s": Config("C6s", "overlap", dict(L=4, m_w=-1.4, mu=0.3, link_seed=306), "sign", (15, 7),

@@ -71,6 +71,7 @@ SIGNATURES = {
     "ppf_spmv": (C.c_int, [vp, vp, vp, vp]),
     "ppf_mat_set_split": (C.c_int, [vp, C.c_int, C.POINTER(C.c_int)]),
     "ppf_ctx_set_transport": (C.c_int, [vp, C.POINTER(Transport)]),
+    "ppf_ctx_set_graphs": (C.c_int, [vp, C.c_int]),
     "ppf_mat_destroy": (None, [vp]),
     "ppf_halo_pack": (C.c_int, [vp, vp, vp]),
     "ppf_halo_buffers": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),

@@ -51,6 +51,10 @@ class Context:
         self.h = h
         self.rank, self.nranks = rank, nranks
 
+    def set_graphs(self, on: bool):
+        """ppf_ctx_set_graphs: CUDA-graph replay of the step's q(A)q(A) chain."""
+        check(_lib().ppf_ctx_set_graphs(self.h, int(bool(on))))
+
     def set_transport(self, exchange, allreduce_sum):
         """ppf_ctx_set_transport: host-side halo exchange / sum over ranks.
 

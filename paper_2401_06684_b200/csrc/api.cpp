@@ -147,6 +147,13 @@ ppf_status ppf_ctx_set_transport(ppf_ctx* c, const ppf_transport* t) {
   PPF_API_END
 }
 
+ppf_status ppf_ctx_set_graphs(ppf_ctx* c, int on) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(c, "NULL ctx");
+  c->use_graphs = on ? 1 : 0;
+  PPF_API_END
+}
+
 ppf_status ppf_profile_enable(ppf_ctx* c, int on) {
   PPF_API_BEGIN
   PPF_REQUIRE(c, "NULL ctx");
@@ -174,6 +181,7 @@ void ppf_ctx_destroy(ppf_ctx* c) {
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
 }
 

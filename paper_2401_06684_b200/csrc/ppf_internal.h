@@ -194,6 +194,8 @@ struct ppf_ctx {
   long long launches;
   // optional per-kernel-class timing with CUDA events on the context stream
   int profile;
+  int use_graphs = 1;         // CUDA-graph replay of the step's q(A)q(A) chain (ppf_ctx_set_graphs)
+  cudaStream_t cap_stream = nullptr;  // private stream the chain is captured on
   std::vector<cudaEvent_t> prof_pool;
   struct ProfAcc {
     long long launches;

@@ -29,14 +29,15 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 // Workspace shape: which bases the run keeps.
 enum { WS_RIGHT = 1,     // right preconditioning, one-pass: Y_m (m_max columns)
        WS_TWOPASS = 2,   // two-pass Lanczos: V = {v_1, ring of 3}, + accumulator XA
-       WS_SQUARE = 4 };  // operator A = Q^2: + the intermediate Q x (TSQ)
+       WS_SQUARE = 4,    // operator A = Q^2: + the intermediate Q x (TSQ)
+       WS_GRAPH = 8 };   // CUDA-graph step: + the fixed output W2 of the captured q(A)q(A) chain
 
 struct WsLayout {
   int64_t ldv;       // leading dimension of V and vector length (padded)
   int ldh;           // leading dimension of H
   int vcols;         // columns of V
-  size_t V, Yb, U, Y, T0, T1, T2, XA, TSQ, H, hbuf, gbuf, ybuf, ybuf2, scal, partials, counter,
-      raw, total;
+  size_t V, Yb, U, Y, T0, T1, T2, XA, TSQ, W2, H, hbuf, gbuf, ybuf, ybuf2, scal, partials,
+      counter, raw, total;
   int max_blocks;
   int max_vals;
 };
@@ -69,6 +70,8 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms, int shape = 
   if (shape & WS_TWOPASS) o += vec;
   L.TSQ = o;
   if (shape & WS_SQUARE) o += vec;
+  L.W2 = o;
+  if (shape & WS_GRAPH) o += vec;
   L.H = o;
   o += al256(size_t(L.ldh) * (m_max + 1) * sc);
   L.hbuf = o;
@@ -110,6 +113,9 @@ int ws_shape(const ppf_poly* q, const ppf_opts* o) {
   int s = squared(o) ? WS_SQUARE : 0;
   if (o->krylov == PPF_LANCZOS_2PASS) s |= WS_TWOPASS;
   else if (q && o->precond == PPF_PREC_RIGHT) s |= WS_RIGHT;
+  // left-preconditioned one-pass steps can replay their q(A)q(A) chain as a CUDA graph
+  if (q && q->deg >= 1 && o->precond == PPF_PREC_LEFT && o->krylov != PPF_LANCZOS_2PASS)
+    s |= WS_GRAPH;
   return s;
 }
 
@@ -306,10 +312,15 @@ struct Runner {
     Epi e;
     bool scale;   // out = c * x (degree-0 polynomial) instead of an SpMV
     double c;
+    bool graph = false;  // replay the captured q(A)q(A) chain (U -> W2)
   };
   std::vector<Call>* rec = nullptr;
 
   void play(const Call& c) {
+    if (c.graph) {
+      run_graph();
+      return;
+    }
     if (c.scale)
       timed(2, 2.0 * n * sc, [&] { launch_scale(dt, n, c.x, c.out, nullptr, c.c, st); });
     else
@@ -490,6 +501,12 @@ struct Runner {
       apply_q(vsrc(j), yj);
       apply_q(yj, vec(L.U));
       spmv(vec(L.U), vdst(j), plain);
+    } else if (use_graph) {
+      spmv(vsrc(j), vec(L.U), plain);
+      if (rec)
+        rec->push_back({nullptr, nullptr, Epi{}, false, 0.0, true});
+      else
+        run_graph();
     } else {
       spmv(vsrc(j), vec(L.U), plain);
       apply_q(vec(L.U), vec(L.Y));
@@ -497,17 +514,61 @@ struct Runner {
     }
   }
 
+  // ----- CUDA graph of the step's q(A) q(A) chain (left preconditioning) -----
+  // Its 2 deg (x power) SpMV launches always read U and write W2 through the
+  // same buffers, so one capture serves every step: each step is then one
+  // plain SpMV (v_j -> U), one graph launch and the orthogonalisation, which
+  // takes w from W2 and writes v_{j+1}.  Launch-bound steps (C1, C2, small
+  // n) lose most of their per-kernel host cost and inter-kernel gaps.
+  bool use_graph = false;
+  cudaGraphExec_t gexec = nullptr;
+  long long graph_kernels = 0;
+  void run_graph() {
+    if (!gexec) {
+      // capture on the context's private stream (the caller's may be the
+      // legacy default stream, which cannot capture); replay on the caller's
+      if (!ctx->cap_stream) PPF_CUDA(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+      const long long before = launches;
+      cudaStream_t user = st;
+      cudaGraph_t g = nullptr;
+      st = ctx->cap_stream;
+      PPF_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        apply_q(vec(L.U), vec(L.Y));
+        apply_q(vec(L.Y), vec(L.W2));
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        st = user;
+        throw;
+      }
+      PPF_CUDA(cudaStreamEndCapture(st, &g));
+      st = user;
+      PPF_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+      PPF_CUDA(cudaGraphDestroy(g));
+      graph_kernels = launches - before;
+      launches = before;
+    }
+    PPF_CUDA(cudaGraphLaunch(gexec, st));
+    launches += graph_kernels;
+  }
+  ~Runner() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+  }
+  // where step j's w = Op v_j lands: W2 with the graph, else v_{j+1} itself
+  void* wbuf(int j) { return use_graph ? vec(L.W2) : vdst(j); }
+
   void orthogonalise(int j, bool lanczos) {
     const double vb = double(n) * double(sc);
     if (lanczos) {
       const double* bprev = j > 0 ? reinterpret_cast<const double*>(Hp(j, j - 1)) : nullptr;
       timed(1, vb * (j > 0 ? 4 : 3), [&] {
-        launch_lanczos(dt, 1, n, vsrc(j), vprv(j), bprev, vdst(j), Hp(j, j), nullptr, nullptr,
+        launch_lanczos(dt, 1, n, vsrc(j), vprv(j), bprev, wbuf(j), Hp(j, j), nullptr, nullptr,
                        nullptr, rs, grid_vec, st);
       });
       reduce_fin(FIN_LZ1, int(sc / 8), Hp(j, j), nullptr, nullptr, nullptr);
       timed(1, vb * 3, [&] {
-        launch_lanczos(dt, 2, n, vsrc(j), nullptr, nullptr, vdst(j), Hp(j, j), Hp(j + 1, j),
+        launch_lanczos(dt, 2, n, vsrc(j), nullptr, nullptr, wbuf(j), Hp(j, j), Hp(j + 1, j),
                        Hp(j, j + 1), scal(S_INV), rs, grid_vec, st);
       });
       reduce_fin(FIN_LZ2, 1, Hp(j + 1, j), Hp(j, j + 1), scal(S_INV), nullptr);
@@ -517,22 +578,22 @@ struct Runner {
       // launch_cgs returns the number of kernels it issued (column tiles of 32)
       const int nv = (j + 1) * int(sc / 8);
       timed(1, vb * (j + 2), [&] {
-        launches += launch_cgs(dt, 0, n, V(0), L.ldv, j + 1, V(j + 1), nullptr, hb, nullptr,
+        launches += launch_cgs(dt, 0, n, V(0), L.ldv, j + 1, wbuf(j), nullptr, hb, nullptr,
                                nullptr, nullptr, rs, grid_cgs, st) - 1;
       });
       reduce_fin(FIN_COEF, nv, hb, nullptr, nullptr, nullptr);
       timed(1, vb * (j + 3), [&] {
-        launches += launch_cgs(dt, 1, n, V(0), L.ldv, j + 1, V(j + 1), hb, gb, Hp(0, j), nullptr,
+        launches += launch_cgs(dt, 1, n, V(0), L.ldv, j + 1, wbuf(j), hb, gb, Hp(0, j), nullptr,
                                nullptr, rs, grid_cgs, st) - 1;
       });
       reduce_fin(FIN_COEF, nv, gb, Hp(0, j), nullptr, hb);
       timed(1, vb * (j + 3), [&] {
-        launches += launch_cgs(dt, 2, n, V(0), L.ldv, j + 1, V(j + 1), gb, nullptr, nullptr,
+        launches += launch_cgs(dt, 2, n, V(0), L.ldv, j + 1, wbuf(j), gb, nullptr, nullptr,
                                Hp(j + 1, j), scal(S_INV), rs, grid_cgs, st) - 1;
       });
       reduce_fin(FIN_SUBNORM, 1, Hp(j + 1, j), nullptr, scal(S_INV), nullptr);
     }
-    timed(1, vb * 2, [&] { launch_scale(dt, n, vdst(j), vdst(j), scal(S_INV), 0.0, st); });
+    timed(1, vb * 2, [&] { launch_scale(dt, n, wbuf(j), vdst(j), scal(S_INV), 0.0, st); });
   }
 
   // start: V0 = s/||s||  (||s|| -> scal(S_BETA0))
@@ -712,6 +773,10 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   const double brt = o->breakdown_rtol > 0.0 ? o->breakdown_rtol : 1e-14;
   Runner R(ctx, A, q, m_max, work, bytes, ws_shape(q, o), right);
   R.power = power;
+  // graphs pay where launches dominate: matrices of < 256 MB (L2-scale: C1,
+  // C2, the graph Laplacian, Table 1's 100^3); at C3-C5 one SpMV is 0.1-0.3 ms
+  R.use_graph = (ws_shape(q, o) & WS_GRAPH) && ctx->use_graphs && !ctx->profile &&
+                A->nranks == 1 && double(A->stored) * double(R.sc + 4) < 256e6;
   const int64_t n = R.n;
   const size_t vb = size_t(n) * R.sc;
   double t_dense = 0.0;

@@ -359,3 +359,27 @@ def test_branch_errors(ctx):
     with pytest.raises(api.L.PPFError) as e:
         pp.Poly.ritz_newton(ctx, M, dev(np.ones(n, dtype=complex)), 3)
     assert e.value.status == 5
+
+
+@pytest.mark.parametrize("name,deg,kry", [("C2", 10, "cgs2"), ("C1", 4, "lanczos"), ("C4s", 5, "cgs2")])
+def test_graph_replay_bitwise(ctx, name, deg, kry):
+    """The CUDA-graph replay of the step's q(A)q(A) chain (ppf_ctx_set_graphs)
+    launches the same kernels in the same order: x and H bitwise equal to the
+    direct launches, and equal to the oracle within the usual bars."""
+    cfg = configs.CONFIGS[name]
+    A, b, iv = configs.build(name)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A))
+    q = pp.Poly.chebyshev(*iv, deg)
+    out = {}
+    for on in (True, False):
+        ctx.set_graphs(on)
+        x, rep = pp.run(ctx, M, q, dev(b), func=cfg.func, krylov=kry, m_max=cfg.m_max, stop="est",
+                        tol=cfg.tol)
+        out[on] = (host(x), pp.hessenberg(ctx, False)[0], rep)
+    ctx.set_graphs(True)
+    assert np.array_equal(out[True][0], out[False][0])
+    assert np.array_equal(out[True][1], out[False][1])
+    assert out[True][2].iterations == out[False][2].iterations
+    # (launch counts differ only by the look-ahead at the final checkpoint: the
+    # graph mode runs the next step's whole chain ahead, 2 deg - 1 more kernels)
+    assert out[True][2].kernel_launches - out[False][2].kernel_launches == 2 * deg - 1
