@@ -1145,7 +1145,7 @@ static void cgs_nc(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* c
   else if (nct <= 16)
     cgs_go<T, 16, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
   else if constexpr (cgs_tile<T>() > 16)
-    cgs_go<T, 32, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
+    cgs_go<T, 24, FL>(n, V, ldv, nct, w, ci, co, hc, hs, inv, rs, raw, grid, st);
   else
     fail(PPF_EINVAL, "CGS column tile too wide");
 }
