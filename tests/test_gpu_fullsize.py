@@ -90,3 +90,48 @@ def test_c5_fullsize_invariant(ctx):
     res = A.to_scipy() @ x2.cpu().numpy() - b
     assert np.linalg.norm(res) / np.linalg.norm(b) <= 1e-9
     assert rep1.iterations <= 8
+
+
+def test_c6_fullsize_sign_involution(ctx):
+    """sign(Q)b for the 16^4 overlap kernel (bench C6): sign(Q)(sign(Q) b) = b
+    (sign(Q)^2 = I) in the bench's launch configuration, Ritz values of Q^2 off
+    the branch cut, and the (Q^2)^{-1/2} b iterate satisfies Q^2 f ~ ... via
+    sign: Q f = sign(Q) b."""
+    cfg = configs.CONFIGS["C6"]
+    A, b, _ = configs.build("C6")
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32))
+    _sampled_spmv(ctx, A, M, np.random.default_rng(6))
+    bd = torch.from_numpy(b).cuda()
+    q = pp.Poly.ritz_newton(ctx, M, bd, 15, power=2)
+    nodes = q.export()["nodes"]
+    assert not np.any((np.abs(nodes.imag) < 1e-12 * np.abs(nodes)) & (nodes.real <= 0))
+    s1, r1 = pp.run(ctx, M, q, bd, func="sign", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                    tol=1e-12)
+    s2, r2 = pp.run(ctx, M, q, s1.clone(), func="sign", krylov="cgs2", m_max=cfg.m_max,
+                    stop="est", tol=1e-12)
+    assert r1.term == "converged" and r2.term == "converged"
+    torch.cuda.synchronize()
+    assert np.linalg.norm(s2.cpu().numpy() - b) <= 1e-9 * np.linalg.norm(b)
+
+
+def test_c7_fullsize_sqrt_invariant(ctx):
+    """L^{1/2} b for the synthetic 281,903-node graph Laplacian (bench C7, global
+    SELL-32 sorting, forward-basis Newton chain): L^{1/2}(L^{1/2} b) = L b
+    (Theorem 4.1's setting) with the Ritz q from L b."""
+    cfg = configs.CONFIGS["C7"]
+    A, b, _ = configs.build("C7")
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32, sigma=32 * ((A.n + 31) // 32)))
+    _sampled_spmv(ctx, A, M, np.random.default_rng(7))
+    bd = torch.from_numpy(b).cuda()
+    Lb = torch.empty_like(bd)
+    M.spmv(bd, Lb)
+    q = pp.Poly.ritz_newton(ctx, M, Lb, 15).set_newton_eval("basis")
+    assert np.all(q.export()["nodes"].real > 0)
+    x1, r1 = pp.run(ctx, M, q, bd, func="sqrt", krylov="cgs2", m_max=250, stop="est", tol=1e-10,
+                    check_every=2)
+    x2, r2 = pp.run(ctx, M, q, x1.clone(), func="sqrt", krylov="cgs2", m_max=250, stop="est",
+                    tol=1e-10, check_every=2)
+    assert r1.term == "converged" and r2.term == "converged"
+    torch.cuda.synchronize()
+    Lbh = Lb.cpu().numpy()
+    assert np.linalg.norm(x2.cpu().numpy() - Lbh) <= 1e-7 * np.linalg.norm(Lbh)
