@@ -383,3 +383,35 @@ def test_graph_replay_bitwise(ctx, name, deg, kry):
     # (launch counts differ only by the look-ahead at the final checkpoint: the
     # graph mode runs the next step's whole chain ahead, 2 deg - 1 more kernels)
     assert out[True][2].kernel_launches - out[False][2].kernel_launches == 2 * deg - 1
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 65, 257])
+@pytest.mark.parametrize("kry", ["lanczos", "cgs2"])
+def test_tiny_and_ragged_sizes(ctx, n, kry):
+    """Sizes below one SELL slice (64 rows), one CGS2 chunk (256 rows) and
+    ragged tails just past them: the run must match the oracle, including the
+    bulk-copy tail of the CGS2 sweeps (one padding element for odd n)."""
+    rng = np.random.default_rng(n)
+    main = 2.0 + rng.random(n)
+    off = 0.3 * rng.random(max(n - 1, 0))
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        for j, v in ((i - 1, off[i - 1] if i > 0 else 0), (i, main[i]), (i + 1, off[i] if i + 1 < n else 0)):
+            if 0 <= j < n:
+                rows.append(i)
+                cols.append(j)
+                vals.append(v)
+    import scipy.sparse as sp
+    S = sp.csr_matrix((vals, (rows, cols)), shape=(n, n))
+    A = CSR(n, S.indptr.astype(np.int64), S.indices.astype(np.int64), S.data.astype(np.float64))
+    lam = np.linalg.eigvalsh(S.toarray())
+    a, bb = 0.9 * lam.min(), 1.1 * lam.max()
+    b = rng.standard_normal(n)
+    m = min(n, 6)
+    qo = chebyshev.coefficients(a, bb, 3)
+    res_o = krylov.run(Operator(S), b, qo, krylov=kry, m_max=m)
+    for fmt, C_ in (("sell", 64), ("sell", 32), ("csr", 32)):
+        M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt=fmt, C_=C_))
+        xg, rep = pp.run(ctx, M, pp.Poly.chebyshev(a, bb, 3), dev(b), krylov=kry, m_max=m)
+        assert rep.iterations == res_o.m
+        assert np.linalg.norm(host(xg) - res_o.x) <= X_TOL * np.linalg.norm(res_o.x)
