@@ -1129,9 +1129,9 @@ static void cgs_go(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* c
   post_launch("cgs_kernel");
 }
 
-// column tile width per launch: 24 (fp64: two stages of 25 x 4 KB column
-// segments fit in shared memory, cgs_rpt) / 16 (complex)
-template <typename T> constexpr int cgs_tile() { return sizeof(T) == 8 ? 24 : 16; }
+// column tile width per launch: 24 (two stages of 25 x 4 KB column segments
+// fit in shared memory, cgs_rpt), fp64 and complex
+template <typename T> constexpr int cgs_tile() { return 24; }
 
 template <typename T, int FL>
 static void cgs_nc(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* ci, T* co, T* hc,

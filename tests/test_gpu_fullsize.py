@@ -134,4 +134,9 @@ def test_c7_fullsize_sqrt_invariant(ctx):
     assert r1.term == "converged" and r2.term == "converged"
     torch.cuda.synchronize()
     Lbh = Lb.cpu().numpy()
-    assert np.linalg.norm(x2.cpu().numpy() - Lbh) <= 1e-7 * np.linalg.norm(Lbh)
+    # bar: 10x what the oracle itself reaches with this stopping rule (estimate
+    # 1e-10 at k = 2): 9.0e-5 at full size (m = 186 / 148), because on this
+    # strongly non-normal operator the paper's estimate is optimistic (at
+    # n = 20000 the oracle's est 1e-10 is a true error of 4e-8) and the
+    # composition doubles it; a wrong result would be O(1) off
+    assert np.linalg.norm(x2.cpu().numpy() - Lbh) <= 9e-4 * np.linalg.norm(Lbh)
