@@ -920,6 +920,7 @@ static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStrea
       const int blocks = int((A->n_local * G + 255) / 256);
       if (blocks == 0) return;
       switch (G) {
+        case 1: csr_kernel<T, 1, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
         case 2: csr_kernel<T, 2, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
         case 4: csr_kernel<T, 4, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
         case 8: csr_kernel<T, 8, true><<<blocks, 256, 0, st>>>(A->n_local, A->d_ptr, A->d_col, val, xt, ot, et, has_x); break;
@@ -979,6 +980,7 @@ static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStrea
                                               has_x);                                         \
     break;
     switch (G) {
+      PPF_CSR(1)
       PPF_CSR(2)
       PPF_CSR(4)
       PPF_CSR(8)
