@@ -70,6 +70,8 @@ def parse():
     p.add_argument("--newton-eval", default=None, choices=["horner", "basis"],
                    help="Newton-form q on the device: Horner (P:354) or the forward basis "
                         "(default: basis for the graph Laplacian, horner otherwise)")
+    p.add_argument("--harmonic", action="store_true",
+                   help="Ritz configs: harmonic Ritz values as nodes (P:357-367)")
     p.add_argument("--poly", default="config", choices=["config", "contour"],
                    help="contour: least-squares q on the circle |z - (4+m0)| = 2.2 (P:359-404; "
                         "Wilson configs)")
@@ -316,9 +318,9 @@ def main():
             # singular A (Thm 4.1): the Ritz values from A b, whose null-space
             # component is deflated (implicit desingularisation)
             M.spmv(bd, ritz_buf)
-            q = pp.Poly.ritz_newton(ctx, M, ritz_buf, deg, power=power)
+            q = pp.Poly.ritz_newton(ctx, M, ritz_buf, deg, power=power, harmonic=args.harmonic)
         else:
-            q = pp.Poly.ritz_newton(ctx, M, bd, deg, power=power)
+            q = pp.Poly.ritz_newton(ctx, M, bd, deg, power=power, harmonic=args.harmonic)
         return q.set_newton_eval(newton_eval)
 
     krylov_m = args.krylov or cfg.krylov

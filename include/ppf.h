@@ -222,9 +222,12 @@ ppf_status ppf_ritz_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, int deg, siz
 ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
                                 void* work, size_t work_bytes, ppf_poly** out);
 /* The same for the Ritz values of A^power (power 1 or 2; power 2 = the operator
- * of PPF_INVSQRT_SQ / PPF_SIGN, two mat-vecs per Arnoldi step). */
+ * of PPF_INVSQRT_SQ / PPF_SIGN, two mat-vecs per Arnoldi step); with
+ * harmonic != 0 the nodes are the harmonic Ritz values, the eigenvalues of
+ * H_d + h_{d+1,d}^2 H_d^{-*} e_d e_d^* (P:357-367). */
 ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
-                                    int power, void* work, size_t work_bytes, ppf_poly** out);
+                                    int power, int harmonic, void* work, size_t work_bytes,
+                                    ppf_poly** out);
 /* ppf_poly_contour_ls (§5.3): the least-squares polynomial of degree
  *   deg for z^{-1/2} on the discretised contour `points` (npts complex, host,
  *   interleaved; npts > deg + 1; no point on (-inf, 0]): Arnoldi on

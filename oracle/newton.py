@@ -66,6 +66,20 @@ def ritz_values(H_square: np.ndarray) -> np.ndarray:
     return theta
 
 
+def harmonic_ritz_values(H: np.ndarray) -> np.ndarray:
+    """Harmonic Ritz values: the eigenvalues of
+    H~_d = H_d + h_{d+1,d}^2 H_d^{-*} e_d e_d^*, from the (d+1) x d Arnoldi
+    Hessenberg H.  Rejects any value on (-inf, 0]."""
+    d = H.shape[1]
+    Hd = H[:d, :d].astype(np.complex128)
+    h = H[d, d - 1]
+    ed = np.zeros(d, dtype=np.complex128)
+    ed[-1] = 1.0
+    f = np.linalg.solve(Hd.conj().T, ed)          # H_d^{-*} e_d
+    Ht = Hd + (abs(h) ** 2) * np.outer(f, ed.conj())
+    return ritz_values(Ht)
+
+
 def leja_order(theta: np.ndarray) -> np.ndarray:
     """Lejà ordering: max modulus first, then argmax Σ log|θ - θ_i|."""
     theta = np.asarray(theta, dtype=np.complex128)
@@ -103,13 +117,14 @@ def from_nodes(nodes) -> NewtonPoly:
     return NewtonPoly(ordered, divided_differences(ordered))
 
 
-def ritz_newton(op, b: np.ndarray, deg: int):
-    """Full O2 construction: deg+1 Arnoldi steps from b, Ritz values, Lejà, dd.
+def ritz_newton(op, b: np.ndarray, deg: int, harmonic: bool = False):
+    """Full O2 construction: deg+1 Arnoldi steps from b, Ritz values (or
+    harmonic Ritz values), Lejà, dd.
     Returns (NewtonPoly, mvms, inner_products)."""
     d = deg + 1
     m0 = op.mvms
     H, ips = arnoldi_plain(op, b, d)
-    theta = ritz_values(H[:d, :d])
+    theta = harmonic_ritz_values(H) if harmonic else ritz_values(H[:d, :d])
     return from_nodes(theta), op.mvms - m0, ips
 
 

@@ -227,7 +227,8 @@ class Poly:
         return cls(h)
 
     @classmethod
-    def ritz_newton(cls, ctx: Context, A: Matrix, start, deg: int, power: int = 1) -> "Poly":
+    def ritz_newton(cls, ctx: Context, A: Matrix, start, deg: int, power: int = 1,
+                    harmonic: bool = False) -> "Poly":
         """Ritz values of deg+1 device Arnoldi steps with A^power
         (power 2: the operator of func "invsqrt_sq" / "sign") from ``start``."""
         torch = _torch()
@@ -236,8 +237,8 @@ class Poly:
         work = torch.empty(nb.value, dtype=torch.uint8, device=start.device)
         h = C.c_void_p()
         check(_lib().ppf_poly_ritz_newton_pow(ctx.h, A.h, C.c_void_p(start.data_ptr()), deg,
-                                              int(power), C.c_void_p(work.data_ptr()), nb.value,
-                                              C.byref(h)))
+                                              int(power), int(bool(harmonic)),
+                                              C.c_void_p(work.data_ptr()), nb.value, C.byref(h)))
         return cls(h)
 
     def set_newton_eval(self, mode: str) -> "Poly":

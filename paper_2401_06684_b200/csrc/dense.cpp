@@ -188,6 +188,36 @@ void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q) {
     for (int i = j + 1; i < m; ++i) h(i, j) = 0.0;
 }
 
+// f with H^H f = e_{m-1} (the last unit vector), Gaussian elimination with
+// partial pivoting on the m x m adjoint (column-major H)
+std::vector<zc> solve_dense_adjoint_ed(int m, const std::vector<zc>& H) {
+  std::vector<zc> M(size_t(m) * m), f(m, zc(0.0, 0.0));
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) M[size_t(i) * m + j] = std::conj(H[size_t(j) + size_t(i) * m]);  // row-major H^H
+  f[m - 1] = 1.0;
+  for (int c = 0; c < m; ++c) {
+    int p = c;
+    for (int r = c + 1; r < m; ++r)
+      if (std::abs(M[size_t(r) * m + c]) > std::abs(M[size_t(p) * m + c])) p = r;
+    if (std::abs(M[size_t(p) * m + c]) == 0.0) fail(PPF_EDENSE, "singular H_d in the harmonic Ritz construction");
+    if (p != c) {
+      for (int j = 0; j < m; ++j) std::swap(M[size_t(c) * m + j], M[size_t(p) * m + j]);
+      std::swap(f[c], f[p]);
+    }
+    for (int r = c + 1; r < m; ++r) {
+      const zc t = M[size_t(r) * m + c] / M[size_t(c) * m + c];
+      for (int j = c; j < m; ++j) M[size_t(r) * m + j] -= t * M[size_t(c) * m + j];
+      f[r] -= t * f[c];
+    }
+  }
+  for (int c = m - 1; c >= 0; --c) {
+    zc t = f[c];
+    for (int j = c + 1; j < m; ++j) t -= M[size_t(c) * m + j] * f[j];
+    f[c] = t / M[size_t(c) * m + c];
+  }
+  return f;
+}
+
 std::vector<zc> eigenvalues(int m, std::vector<zc> H) {
   std::vector<zc> Q;
   complex_schur(m, H, Q);

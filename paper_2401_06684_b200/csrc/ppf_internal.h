@@ -217,6 +217,8 @@ void general_invsqrt_e1(int m, const std::vector<zc>& H, double beta0, std::vect
 // y = beta0 * H^{-1/2} e1 for a REAL upper Hessenberg H (column-major, ld ldh):
 // real Schur (Francis double shift) -> quasi-triangular square root -> solve.
 void real_invsqrt_e1(int m, const double* H, int ldh, double beta0, double* y);
+// f with H^H f = e_{m-1} (harmonic Ritz values)
+std::vector<zc> solve_dense_adjoint_ed(int m, const std::vector<zc>& H);
 // Eigenvalues of a general complex m x m matrix (column-major).
 std::vector<zc> eigenvalues(int m, std::vector<zc> H);
 

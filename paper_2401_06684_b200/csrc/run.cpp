@@ -1108,7 +1108,8 @@ ppf_status ppf_ritz_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, int deg, siz
 // Ritz values of H_d from d = deg+1 Arnoldi steps with A^power,
 // Leja order, divided differences.
 ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg,
-                                    int power, void* work, size_t bytes, ppf_poly** out) {
+                                    int power, int harmonic, void* work, size_t bytes,
+                                    ppf_poly** out) {
   PPF_API_BEGIN
   PPF_REQUIRE(ctx && A && start && out, "NULL argument");
   PPF_REQUIRE(deg >= 0 && deg < 255, "deg out of range");
@@ -1130,6 +1131,12 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
   std::vector<zc> Hd(size_t(d) * d);
   for (int j = 0; j < d; ++j)
     for (int i = 0; i < d; ++i) Hd[size_t(i) + size_t(j) * d] = Hh[size_t(i) + size_t(j) * (d + 1)];
+  if (harmonic) {
+    // H~_d = H_d + |h_{d+1,d}|^2 f e_d^T with H_d^H f = e_d
+    const zc hs = Hh[size_t(d) + size_t(d - 1) * (d + 1)];
+    std::vector<zc> f = solve_dense_adjoint_ed(d, Hd);
+    for (int i = 0; i < d; ++i) Hd[size_t(i) + size_t(d - 1) * d] += std::norm(hs) * f[i];
+  }
   std::vector<zc> theta = eigenvalues(d, Hd);
   if (A->dtype == PPF_R64) {
     // a real operator runs the chain in real arithmetic: the Ritz values must
@@ -1156,7 +1163,7 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
 
 ppf_status ppf_poly_ritz_newton(ppf_ctx* ctx, ppf_mat* A, const void* start, int deg, void* work,
                                 size_t bytes, ppf_poly** out) {
-  return ppf_poly_ritz_newton_pow(ctx, A, start, deg, 1, work, bytes, out);
+  return ppf_poly_ritz_newton_pow(ctx, A, start, deg, 1, 0, work, bytes, out);
 }
 
 }  // extern "C"

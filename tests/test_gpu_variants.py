@@ -369,3 +369,23 @@ def test_graph_laplacian_forward_basis_run(ctx):
                      tol=cfg.tol, check_every=4)
     _check(ctx, res_o, xg, rep, h_tol=h_tol)
     assert h_tol < 1e-8          # the same scheme as the oracle: far tighter than Horner's
+
+
+def test_harmonic_ritz_wilson(ctx):
+    """Harmonic Ritz nodes from the device Arnoldi run
+    against the oracle's (multisets, parity unpinned at ~1e-10 like the Ritz
+    nodes, F6), and the run with the oracle's harmonic q imported."""
+    from oracle import newton
+    cfg = configs.CONFIGS["C5s"]
+    A, b, _ = configs.build("C5s")
+    op = Operator(A.to_scipy())
+    qo, _, _ = newton.ritz_newton(op, b, 16, harmonic=True)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A))
+    ql = pp.Poly.ritz_newton(ctx, M, dev(b), 16, harmonic=True)
+    nodes = ql.export()["nodes"]
+    assert np.abs(np.sort_complex(nodes) - np.sort_complex(qo.nodes)).max() < 1e-8
+    res_o = krylov.run(op, b, qo, func="invsqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                       tol=cfg.tol)
+    xg, rep = pp.run(ctx, M, pp.Poly.newton(qo.nodes, qo.dd), dev(b), func="invsqrt",
+                     krylov="cgs2", m_max=cfg.m_max, stop="est", tol=cfg.tol)
+    _check(ctx, res_o, xg, rep, complex_=True, h_tol=1e-10)

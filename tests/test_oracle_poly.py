@@ -213,3 +213,42 @@ def test_contour_ls_wilson_converges():
     res = krylov.run(op, b, q, func="invsqrt", krylov="cgs2", m_max=30, stop="true", tol=1e-8,
                      x_ref=xr)
     assert res.term == "converged" and res.m <= 6
+
+
+def test_harmonic_ritz_values_closed_forms():
+    """Harmonic Ritz values: (i) they are the reciprocals of
+    the Ritz values of A^{-1} on A K_d(A, b), i.e. the eigenvalues of the
+    d x d pencil (V^H A^H A V, V^H A^H V) -- checked against that definition
+    with scipy's generalized eigensolver; (ii) for HPD A they are real and lie in
+    [lambda_min, lambda_max] (bounded away from 0)."""
+    import scipy.linalg as sla
+    import scipy.sparse as sp
+    from oracle import newton
+    rng = np.random.default_rng(3)
+    n = 40
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.linspace(0.3, 9.0, n)
+    M = (Q * lam) @ Q.T + 0.3 * np.triu(rng.standard_normal((n, n)), 1)   # non-normal
+    op = Operator(sp.csr_matrix(M))
+    b = rng.standard_normal(n)
+    d = 7
+    H, _ = newton.arnoldi_plain(op, b, d)
+    mu = newton.harmonic_ritz_values(H)
+    # basis of K_d from the same Arnoldi process (oracle-independent rebuild)
+    V = np.zeros((n, d))
+    V[:, 0] = b / np.linalg.norm(b)
+    for j in range(1, d):
+        w = M @ V[:, j - 1]
+        for _ in range(2):
+            w -= V[:, :j] @ (V[:, :j].T @ w)
+        V[:, j] = w / np.linalg.norm(w)
+    AV = M @ V
+    ref = sla.eigvals(AV.T @ AV, AV.T @ V)
+    assert np.abs(np.sort_complex(mu) - np.sort_complex(ref)).max() < 1e-8 * np.abs(ref).max()
+    # (ii) a symmetric positive definite A
+    S = (Q * lam) @ Q.T
+    ops = Operator(sp.csr_matrix(S))
+    Hs, _ = newton.arnoldi_plain(ops, b, 9)
+    mus = newton.harmonic_ritz_values(Hs)
+    assert np.all(mus.real >= lam[0] - 1e-10) and np.all(mus.real <= lam[-1] + 1e-10)
+    assert np.abs(mus.imag).max() < 1e-8
