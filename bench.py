@@ -72,9 +72,10 @@ def parse():
                         "(default: basis for the graph Laplacian, horner otherwise)")
     p.add_argument("--harmonic", action="store_true",
                    help="Ritz configs: harmonic Ritz values as nodes (P:357-367)")
-    p.add_argument("--poly", default="config", choices=["config", "contour"],
+    p.add_argument("--poly", default="config", choices=["config", "contour", "contour-ritz"],
                    help="contour: least-squares q on the circle |z - (4+m0)| = 2.2 (P:359-404; "
-                        "Wilson configs)")
+                        "Wilson configs); contour-ritz: least squares on the polygon of 60 Ritz "
+                        "values (P:562-563; complex arithmetic, as the paper notes)")
     p.add_argument("--check-every", type=int, default=1,
                    help="k of the stopping check (PAPER.md:424 uses 64/d)")
     p.add_argument("--split", type=int, default=0,
@@ -264,10 +265,17 @@ def main():
     name = args.config
     cfg, A, b, iv = setup_inputs(name)
     deg = args.deg if args.deg is not None else cfg.degs[0]
+    if args.poly == "contour-ritz" and not cfg.complex_:
+        # the least-squares q is complex: run the real operator in complex128
+        # ("necessitate complex arithmetic even though L and b are real")
+        from inputs.operators import CSR
+        A = CSR(A.n, A.row_ptr, A.col, A.val.astype(np.complex128))
+        b = b.astype(np.complex128)
+    cplx_run = cfg.complex_ or args.poly == "contour-ritz"
     if args.fmt is None:
-        args.fmt = "sell32" if (cfg.complex_ or cfg.family == "graph") else "sell64"
+        args.fmt = "sell32" if (cplx_run or cfg.family == "graph") else "sell64"
     fmt = {"sell32": ("sell", 32), "sell64": ("sell", 64), "csr": ("csr", 32)}[args.fmt]
-    if cfg.complex_ and fmt == ("sell", 64):
+    if cplx_run and fmt == ("sell", 64):
         fmt = ("sell", 32)
     sigma = args.sigma
     if sigma == 0:
@@ -312,6 +320,17 @@ def main():
         if args.poly == "contour":
             c = 4.0 + cfg.params["m0"]
             return pp.Poly.contour_ls(c + 2.2 * np.exp(2j * np.pi * np.arange(128) / 128), deg)
+        if args.poly == "contour-ritz":
+            # 60 Arnoldi steps -> Ritz values -> polygon with minimum
+            # distance 0.1 -> ~2000 points -> least-squares q of degree deg
+            start = bd
+            if cfg.params.get("ritz_start") == "Ab":
+                M.spmv(bd, ritz_buf)
+                start = ritz_buf
+            theta = pp.Poly.ritz_newton(ctx, M, start, 59).export()["nodes"]
+            span = (theta.real.max() - theta.real.min()) + (theta.imag.max() - theta.imag.min())
+            pts = api.contour_from_ritz(theta, 0.1, max(2.0 * span / 2000, 1e-6))
+            return pp.Poly.contour_ls(pts, deg)
         if cfg.poly == "chebyshev":
             return pp.Poly.chebyshev(*iv, deg)
         if cfg.params.get("ritz_start") == "Ab":
@@ -388,7 +407,7 @@ def main():
     bh = torch.from_numpy(b).pin_memory()
     xh = torch.empty_like(bh).pin_memory()
     e2e_times = []
-    ritz = cfg.poly != "chebyshev" and not args.plain and args.poly == "config"
+    ritz = cfg.poly != "chebyshev" and not args.plain and args.poly in ("config", "contour-ritz")
     for i in range(max(2, min(args.steps, 3)) + 1):
         t0 = time.perf_counter()
         if ritz:  # the Ritz setup starts from b: it needs b on the device
@@ -420,18 +439,19 @@ def main():
     except Exception:
         traffic_note = None
     m_iter = reps[-1].iterations
-    n_bytes = len(b) * (16 if cfg.complex_ else 8)   # this rank's slab of b and x
+    n_bytes = len(b) * (16 if cplx_run else 8)   # this rank's slab of b and x
     line = {
         "metric": "f(A)b time-to-1e-8 rel. error (s) & Krylov-step HBM GB/s vs B200 peak",
         "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "c128" if cfg.complex_ else "f64",
+        "dtype": "c128" if cplx_run else "f64",
         "data": "synthetic (seeded generators in inputs/; no dataset)",
         "config": {"workload": WORKLOAD.get(name, name), "deg": None if args.plain else deg,
                    "precond": "none (plain, d = 1)" if args.plain else args.precond,
-                   "poly": "contour-LS circle |z-(4+m0)|=2.2, N=128" if args.poly == "contour"
-                   else cfg.poly,
+                   "poly": {"contour": "contour-LS circle |z-(4+m0)|=2.2, N=128",
+                            "contour-ritz": "contour-LS on the polygon of 60 Ritz values, r_min 0.1, "
+                                            "~2000 points (complex arithmetic)"}.get(args.poly, cfg.poly),
                    "newton_eval": newton_eval if cfg.poly == "ritz" else None,
                    "krylov": krylov_m, "check_every": args.check_every, "tol": cfg.tol,
                    "format": args.fmt, "sell_sigma": sigma, "sell_split": split,
@@ -456,7 +476,8 @@ def main():
                           "note": "same K steps with per-launch CUDA events; roofline and "
                                   "breakdown come from this pass"},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.poly == "config" \
+            and not args.plain and args.precond == "left" and args.krylov is None:
         line["cpu_baseline"] = cpu_baseline(cfg, A, b, iv, deg, m_iter, reps[-1].mvms)
     if rank == 0:
         print(json.dumps(line), flush=True)

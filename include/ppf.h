@@ -238,6 +238,15 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
  *   (the certificate of P:401-403). */
 ppf_status ppf_poly_contour_ls(const double* points, int npts, int deg, double* min_re_q,
                                ppf_poly** out);
+/* ppf_contour_from_ritz (Q29): a contour
+ *   for ppf_poly_contour_ls from Ritz values theta (ntheta complex, host,
+ *   interleaved): their convex hull (collinear values: the segment there and
+ *   back), densified in steps <= step, the parts closer to 0 than r_min
+ *   replaced by the arc |z| = r_min (then resampled uniformly).  Writes *npts
+ *   points to `points` (cap complex entries; query with points = NULL).
+ *   PPF_EBRANCH if the hull surrounds 0. */
+ppf_status ppf_contour_from_ritz(const double* theta, int ntheta, double r_min, double step,
+                                 int cap, double* points, int* npts);
 ppf_status ppf_poly_import(int kind, int deg, const double* ab, const void* coef,
                            const void* nodes, ppf_poly** out);
 ppf_status ppf_poly_export(const ppf_poly* q, int* kind, int* deg, double* ab,

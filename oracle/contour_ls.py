@@ -99,3 +99,67 @@ def apply(q: LSPoly, op, v: np.ndarray) -> np.ndarray:
 def certify(q: LSPoly) -> float:
     """min Re q(z_i) over the contour points; must be > 0."""
     return float(np.min(evaluate(q, q.points).real))
+
+
+def ritz_polygon(theta, r_min: float, step: float) -> np.ndarray:
+    """Contour from Ritz values ("constructed as a polygon from the
+    Ritz values"): the boundary of the Ritz values --
+    reading (Q29): their convex hull, counter-clockwise (MATLAB's
+    `boundary`, a shrink-factor hull, is not reproducible); a hull of collinear
+    values degenerates to the segment between the extremes, traversed both
+    ways -- then every part closer to 0 than r_min replaced by the circular
+    arc of radius r_min, discretised in steps of (approximately) uniform
+    length `step`.  Points on (-inf, 0] are never produced for r_min > 0 unless
+    the hull surrounds 0 (rejected)."""
+    th = np.asarray(theta, dtype=np.complex128)
+    pts = np.unique(np.round(np.stack([th.real, th.imag], 1), 15), axis=0)
+    if len(pts) == 1:
+        raise ValueError("need at least two distinct Ritz values")
+    # Andrew's monotone chain convex hull
+    P = sorted(map(tuple, pts))
+
+    def cross(o, a, b):
+        return (a[0] - o[0]) * (b[1] - o[1]) - (a[1] - o[1]) * (b[0] - o[0])
+    lower, upper = [], []
+    for p in P:
+        while len(lower) >= 2 and cross(lower[-2], lower[-1], p) <= 0:
+            lower.pop()
+        lower.append(p)
+    for p in reversed(P):
+        while len(upper) >= 2 and cross(upper[-2], upper[-1], p) <= 0:
+            upper.pop()
+        upper.append(p)
+    hull = lower[:-1] + upper[:-1]
+    verts = np.array([complex(x, y) for x, y in hull])
+    if len(verts) == 2:                       # collinear: there and back
+        verts = np.array([verts[0], verts[1]])
+    # densify the closed polygon
+    out = []
+    nv = len(verts)
+    for i in range(nv):
+        a, c = verts[i], verts[(i + 1) % nv]
+        L = abs(c - a)
+        k = max(1, int(np.ceil(L / step)))
+        out.extend(a + (c - a) * np.arange(k) / k)
+    z = np.array(out)
+    # the hull must not surround 0 (then every contour would meet the branch cut)
+    wind = np.sum(np.angle(np.roll(z, -1) / z))
+    if abs(wind) > np.pi:
+        raise ValueError("the Ritz polygon surrounds 0")
+    # minimum distance: project points closer than r_min radially onto the
+    # circle, then resample that arc uniformly
+    close = np.abs(z) < r_min
+    if np.any(close):
+        z = np.where(close, r_min * np.exp(1j * np.angle(z)), z)
+        # uniform resampling along the (modified) closed curve
+        seg = np.abs(np.diff(np.concatenate([z, z[:1]])))
+        total = seg.sum()
+        s = np.concatenate([[0.0], np.cumsum(seg)])
+        zc = np.concatenate([z, z[:1]])
+        tgt = np.arange(0.0, total, step)
+        idx = np.clip(np.searchsorted(s, tgt, side="right") - 1, 0, len(z) - 1)
+        frac = (tgt - s[idx]) / np.where(seg[idx] > 0, seg[idx], 1.0)
+        z = zc[idx] + frac * (zc[idx + 1] - zc[idx])
+        # chords of the arc dip below r_min by O(step^2 / r_min): back onto the circle
+        z = np.where(np.abs(z) < r_min, r_min * np.exp(1j * np.angle(z)), z)
+    return z

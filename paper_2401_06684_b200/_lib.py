@@ -80,6 +80,8 @@ SIGNATURES = {
     "ppf_ritz_workspace_bytes": (C.c_int, [vp, vp, C.c_int, C.POINTER(C.c_size_t)]),
     "ppf_poly_ritz_newton": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_size_t, C.POINTER(vp)]),
     "ppf_poly_set_newton_eval": (C.c_int, [vp, C.c_int]),
+    "ppf_contour_from_ritz": (C.c_int, [vp, C.c_int, C.c_double, C.c_double, C.c_int, vp,
+                                        C.POINTER(C.c_int)]),
     "ppf_poly_contour_ls": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(vp)]),
     "ppf_poly_ritz_newton_pow": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_size_t,
                                            C.POINTER(vp)]),

@@ -100,6 +100,19 @@ class Context:
             pass
 
 
+def contour_from_ritz(theta, r_min: float, step: float) -> np.ndarray:
+    """ppf_contour_from_ritz: the Ritz-polygon contour (complex points)."""
+    th = np.ascontiguousarray(np.asarray(theta, dtype=np.complex128))
+    n = C.c_int()
+    check(_lib().ppf_contour_from_ritz(th.ctypes.data_as(C.c_void_p), len(th), float(r_min),
+                                       float(step), 0, None, C.byref(n)))
+    out = np.empty(n.value, dtype=np.complex128)
+    check(_lib().ppf_contour_from_ritz(th.ctypes.data_as(C.c_void_p), len(th), float(r_min),
+                                       float(step), n.value, out.ctypes.data_as(C.c_void_p),
+                                       C.byref(n)))
+    return out
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(_lib().ppf_nccl_unique_id(buf))

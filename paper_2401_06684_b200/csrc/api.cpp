@@ -652,6 +652,25 @@ ppf_status ppf_poly_contour_ls(const double* points, int npts, int deg, double* 
   PPF_API_END
 }
 
+ppf_status ppf_contour_from_ritz(const double* theta, int ntheta, double r_min, double step,
+                                 int cap, double* points, int* npts) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(theta && npts && ntheta >= 2, "need >= 2 Ritz values");
+  PPF_REQUIRE(r_min > 0.0 && step > 0.0, "need r_min > 0 and step > 0");
+  std::vector<zc> th(ntheta);
+  for (int i = 0; i < ntheta; ++i) th[i] = zc(theta[2 * i], theta[2 * i + 1]);
+  std::vector<zc> z = ritz_polygon(th, r_min, step);
+  *npts = int(z.size());
+  if (points) {
+    PPF_REQUIRE(cap >= int(z.size()), "points buffer too small (query npts with points = NULL)");
+    for (size_t i = 0; i < z.size(); ++i) {
+      points[2 * i] = z[i].real();
+      points[2 * i + 1] = z[i].imag();
+    }
+  }
+  PPF_API_END
+}
+
 ppf_status ppf_poly_set_newton_eval(ppf_poly* q, int mode) {
   PPF_API_BEGIN
   PPF_REQUIRE(q, "NULL polynomial");

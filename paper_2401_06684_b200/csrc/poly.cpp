@@ -7,6 +7,7 @@
 // scalar evaluation by the Clenshaw recurrence.
 // Newton: Leja order and divided differences of z^{-1/2}.
 #include <algorithm>
+#include <utility>
 #include <cmath>
 
 #include "ppf_internal.h"
@@ -173,6 +174,71 @@ void contour_ls_newton(const std::vector<zc>& z, int deg, std::vector<zc>& nodes
   }
   for (int k = 1; k < d; ++k)
     for (int i = d - 1; i >= k; --i) dd[i] = (dd[i] - dd[i - 1]) / (nodes[i] - nodes[i - k]);
+}
+
+// Contour from Ritz values (reading Q29): the
+// convex hull of the values (Andrew's monotone chain; collinear values give
+// the segment there and back), densified in steps of length <= step, points
+// closer to 0 than r_min projected radially onto |z| = r_min (the circular
+// arc replacing that part), then resampled uniformly and re-projected.
+std::vector<zc> ritz_polygon(const std::vector<zc>& theta, double r_min, double step) {
+  std::vector<std::pair<double, double>> P;
+  for (const zc& t : theta) {
+    const double x = std::nearbyint(t.real() * 1e15) / 1e15, y = std::nearbyint(t.imag() * 1e15) / 1e15;
+    P.push_back({x, y});
+  }
+  std::sort(P.begin(), P.end());
+  P.erase(std::unique(P.begin(), P.end()), P.end());
+  if (P.size() < 2) fail(PPF_EINVAL, "need at least two distinct Ritz values");
+  auto cross = [](const std::pair<double, double>& o, const std::pair<double, double>& a,
+                  const std::pair<double, double>& b) {
+    return (a.first - o.first) * (b.second - o.second) - (a.second - o.second) * (b.first - o.first);
+  };
+  std::vector<std::pair<double, double>> lower, upper;
+  for (const auto& p : P) {
+    while (lower.size() >= 2 && cross(lower[lower.size() - 2], lower.back(), p) <= 0) lower.pop_back();
+    lower.push_back(p);
+  }
+  for (auto it = P.rbegin(); it != P.rend(); ++it) {
+    while (upper.size() >= 2 && cross(upper[upper.size() - 2], upper.back(), *it) <= 0) upper.pop_back();
+    upper.push_back(*it);
+  }
+  std::vector<zc> verts;
+  for (size_t i = 0; i + 1 < lower.size(); ++i) verts.push_back(zc(lower[i].first, lower[i].second));
+  for (size_t i = 0; i + 1 < upper.size(); ++i) verts.push_back(zc(upper[i].first, upper[i].second));
+  std::vector<zc> z;
+  const size_t nv = verts.size();
+  for (size_t i = 0; i < nv; ++i) {
+    const zc a = verts[i], c = verts[(i + 1) % nv];
+    const int k = std::max(1, int(std::ceil(std::abs(c - a) / step)));
+    for (int t = 0; t < k; ++t) z.push_back(a + (c - a) * (double(t) / k));
+  }
+  double wind = 0.0;
+  for (size_t i = 0; i < z.size(); ++i) wind += std::arg(z[(i + 1) % z.size()] / z[i]);
+  if (std::fabs(wind) > M_PI) fail(PPF_EBRANCH, "the Ritz polygon surrounds 0");
+  bool close = false;
+  for (auto& v : z)
+    if (std::abs(v) < r_min) {
+      v = std::polar(r_min, std::arg(v));
+      close = true;
+    }
+  if (close) {
+    const size_t nz = z.size();
+    std::vector<double> s(nz + 1, 0.0);
+    for (size_t i = 0; i < nz; ++i) s[i + 1] = s[i] + std::abs(z[(i + 1) % nz] - z[i]);
+    std::vector<zc> r;
+    size_t i = 0;
+    for (double t = 0.0; t < s[nz]; t += step) {
+      while (i + 1 < nz && s[i + 1] <= t) ++i;
+      const double seg = s[i + 1] - s[i];
+      const double f = seg > 0.0 ? (t - s[i]) / seg : 0.0;
+      zc v = z[i] + f * (z[(i + 1) % nz] - z[i]);
+      if (std::abs(v) < r_min) v = std::polar(r_min, std::arg(v));
+      r.push_back(v);
+    }
+    z = r;
+  }
+  return z;
 }
 
 std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& x) {

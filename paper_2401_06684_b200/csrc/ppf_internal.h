@@ -230,6 +230,7 @@ double chebyshev_eval(const ppf_poly& q, double z);
 zc poly_eval(const ppf_poly& q, zc z);
 std::vector<zc> leja_order(const std::vector<zc>& nodes);
 std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& nodes);
+std::vector<zc> ritz_polygon(const std::vector<zc>& theta, double r_min, double step);
 void contour_ls_newton(const std::vector<zc>& z, int deg, std::vector<zc>& nodes,
                        std::vector<zc>& dd, double& min_re);
 

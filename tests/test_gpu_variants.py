@@ -15,6 +15,7 @@ import pytest
 
 from inputs import configs
 from inputs import operators as ops
+from inputs.operators import CSR
 from oracle import chebyshev, krylov, reference
 from oracle.spmv import Operator
 
@@ -24,6 +25,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2401_06684_b200 as pp  # noqa: E402
+from paper_2401_06684_b200 import api  # noqa: E402
 
 X_TOL, H_TOL = 1e-10, 1e-11
 
@@ -389,3 +391,31 @@ def test_harmonic_ritz_wilson(ctx):
     xg, rep = pp.run(ctx, M, pp.Poly.newton(qo.nodes, qo.dd), dev(b), func="invsqrt",
                      krylov="cgs2", m_max=cfg.m_max, stop="est", tol=cfg.tol)
     _check(ctx, res_o, xg, rep, complex_=True, h_tol=1e-10)
+
+
+def test_contour_ls_ritz_polygon_graph(ctx):
+    """Ex. 6.3's least-squares polynomials on the C7 family: Ritz
+    values (the oracle's, 20 steps from L b) -> Ritz polygon with minimum
+    distance 0.1 -> least-squares q, in complex arithmetic on the real
+    operator; the library builds polygon and q from the same Ritz values."""
+    from oracle import contour_ls, newton
+    cfg = configs.CONFIGS["C7s"]
+    A, b, _ = configs.build("C7s")
+    op = Operator(A.to_scipy())
+    theta = newton.ritz_newton(op, op.matvec(b), 19)[0].nodes
+    span = np.ptp(theta.real) + np.ptp(theta.imag)
+    step = 2.0 * span / 1500
+    qo = contour_ls.construct(contour_ls.ritz_polygon(theta, 0.1, step), 7)
+    res_o = krylov.run(op, b.astype(complex), qo, func="sqrt", krylov="cgs2", m_max=cfg.m_max,
+                       stop="est", tol=cfg.tol, check_every=4)
+    Ac = CSR(A.n, A.row_ptr, A.col, A.val.astype(np.complex128))
+    M = pp.Matrix(ctx, pp.Plan.from_csr(Ac))
+    pts = api.contour_from_ritz(theta, 0.1, step)
+    q = pp.Poly.contour_ls(pts, 7)
+    xg, rep = pp.run(ctx, M, q, dev(b.astype(complex)), func="sqrt", krylov="cgs2",
+                     m_max=cfg.m_max, stop="est", tol=cfg.tol, check_every=4)
+    assert rep.term == "converged"
+    # the library's Newton form of the same q vs the oracle's recurrence
+    # (Q27) on a non-normal operator: the H bar is the measured-amplification
+    # class (Q28), x at the north_star bar
+    _check(ctx, res_o, xg, rep, complex_=True, h_tol=1e-6)

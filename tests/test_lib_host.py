@@ -106,6 +106,25 @@ def test_contour_ls_matches_oracle(contour, deg):
     assert q.min_re == pytest.approx(contour_ls.certify(qo), rel=1e-10)
 
 
+@pytest.mark.parametrize("case", ["circle", "cut", "real", "cloud"])
+def test_contour_from_ritz_matches_oracle(case):
+    """ppf_contour_from_ritz (host C++) against the oracle's ritz_polygon: the
+    same construction, so the same points to rounding."""
+    from paper_2401_06684_b200.api import contour_from_ritz
+    t = 2 * np.pi * np.arange(12) / 12
+    rng = np.random.default_rng(5)
+    th, r_min, step = {
+        "circle": (3.0 + 2.0 * np.exp(1j * t), 0.1, 0.01),
+        "cut": (3.0 + 2.0 * np.exp(1j * t), 1.5, 0.01),
+        "real": (np.array([0.5, 2.0, 7.0]), 0.1, 0.05),
+        "cloud": (4 + rng.standard_normal(30) + 1j * rng.standard_normal(30), 0.2, 0.02),
+    }[case]
+    z = contour_from_ritz(th, r_min, step)
+    zo = contour_ls.ritz_polygon(th, r_min, step)
+    assert z.shape == zo.shape
+    assert np.abs(z - zo).max() < 1e-12
+
+
 def test_contour_ls_rejects_branch_cut():
     # a circle around 0: the contour meets (-inf, 0]
     with pytest.raises(_lib.PPFError):

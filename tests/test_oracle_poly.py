@@ -252,3 +252,27 @@ def test_harmonic_ritz_values_closed_forms():
     mus = newton.harmonic_ritz_values(Hs)
     assert np.all(mus.real >= lam[0] - 1e-10) and np.all(mus.real <= lam[-1] + 1e-10)
     assert np.abs(mus.imag).max() < 1e-8
+
+
+def test_ritz_polygon_contour():
+    """Ritz-polygon contour: for Ritz values
+    on a circle the polygon's points lie between the inscribed and the
+    circumscribed circle of the hull; the minimum-distance rule keeps every
+    point at |z| >= r_min; spacing is uniform to the step; a collinear (real)
+    set gives the segment both ways; a set around 0 is rejected."""
+    from oracle import contour_ls
+    t = 2 * np.pi * np.arange(12) / 12
+    th = 3.0 + 2.0 * np.exp(1j * t)
+    z = contour_ls.ritz_polygon(th, 0.1, 0.01)
+    r = np.abs(z - 3.0)
+    assert r.max() <= 2.0 + 1e-12 and r.min() >= 2.0 * np.cos(np.pi / 12) - 1e-12
+    d = np.abs(np.diff(z))
+    assert d.max() <= 0.01 + 1e-12
+    z2 = contour_ls.ritz_polygon(th, 1.5, 0.01)                 # cuts into the polygon
+    assert np.abs(z2).min() >= 1.5 - 1e-12
+    seg = contour_ls.ritz_polygon(np.array([0.5, 2.0, 7.0]), 0.1, 0.05)
+    assert np.abs(seg.imag).max() == 0.0 and seg.real.min() == 0.5 and seg.real.max() <= 7.0
+    with pytest.raises(ValueError):
+        contour_ls.ritz_polygon(np.exp(1j * t), 0.1, 0.01)
+    q = contour_ls.construct(z, 10)
+    assert contour_ls.certify(q) > 0
