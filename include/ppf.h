@@ -205,14 +205,15 @@ ppf_status ppf_spmv_local(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
  *   greedy max sum log|theta - chosen|, ties to the smaller index after sorting
  *   by (Re, Im)) and forms the divided differences of z^{-1/2}.  `work` is
  *   device scratch of at least ppf_ritz_workspace_bytes.  Complex operators:
- *   any nodes off (-inf, 0]; real operators: real nodes only.
+ *   any nodes off (-inf, 0]; real operators: real nodes, or conjugate pairs in
+ *   the real-pair form.
  * ppf_poly_import: kind CHEBYSHEV: ab = {a, b}, coef = deg+1 doubles, nodes
  *   ignored.  kind NEWTON: coef = deg+1 complex divided differences, nodes =
  *   deg+1 complex Leja-ordered nodes, ab ignored.  No certificate is applied.
  *   A Newton polynomial is applied to a PPF_R64 operator only if all its nodes
  *   and divided differences are real (exactly zero imaginary parts); the Ritz
- *   construction on a PPF_R64 operator returns PPF_EINVAL for complex Ritz
- *   values (use a PPF_C128 plan of the same matrix).
+ *   construction on a PPF_R64 operator with complex (conjugate-pair) Ritz
+ *   values returns the real-pair form (ppf_poly_set_newton_eval mode 2).
  * ppf_poly_export: the same layout (caller buffers of deg+1 entries; query deg
  *   first with coef = nodes = NULL).
  * ppf_poly_eval: q at `npts` complex points (host, interleaved) -> host out.
@@ -263,7 +264,14 @@ ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const voi
  *   scheme"); mode 1: the forward Newton basis p_{j+1} = (A - theta_j) p_j with
  *   sum dd_j p_j accumulated as a second output of each SpMV (one more vector
  *   stream per launch), numerically preferable when spec(A) extends far beyond
- *   the nodes (Q28).  Same deg SpMV launches.  Chebyshev: ignored. */
+ *   the nodes (Q28).  Same deg SpMV launches.  Chebyshev: ignored.
+ *   mode 2: the real conjugate-pair form for a real operator (nodes closed
+ *   under conjugation): Leja order with each complex node followed by its
+ *   conjugate, real basis P_{j+1} = (A - Re th_j) P_j [+ (Im th)^2 P_{j-1} for
+ *   the second of a pair], real coefficients -- all in real arithmetic; the
+ *   nodes/dd are reordered (ppf_poly_export shows the new order).  The Ritz
+ *   construction on a PPF_R64 operator selects it when Ritz values are complex.
+ *   PPF_EINVAL if the nodes are not conjugate-symmetric. */
 ppf_status ppf_poly_set_newton_eval(ppf_poly* q, int mode);
 void ppf_poly_destroy(ppf_poly* q);
 

@@ -72,6 +72,11 @@ CONFIGS = {
                   "cgs2", "ritz", 1e-8, 60, 206),
     "C7s": Config("C7s", "graph", dict(n=2000, avg_deg=8.97, graph_seed=307, ritz_start="Ab"),
                   "sqrt", (7, 3), "cgs2", "ritz", 1e-7, 200, 207),
+    # convection-dominated 2D convection-diffusion (cell Peclet 3 > 1): a real
+    # operator with complex eigenvalues and complex-pair Ritz values, for the
+    # real conjugate-pair Newton form
+    "C8s": Config("C8s", "convdiff", dict(N=32, dim=2, beta=(200.0, 200.0)), "sqrt", (9,), "cgs2",
+                  "ritz", 1e-8, 120, 208),
     "C5s": Config("C5s", "wilson", dict(L=4, m0=-1.0, link_seed=305), "invsqrt", (16, 4), "cgs2", "ritz",
                   1e-8, 30, 205),
 }
@@ -82,8 +87,11 @@ def operator(cfg: Config):
     if cfg.family == "laplacian":
         return ops.laplacian(p["N"], p["dim"]), ops.laplacian_interval(p["N"], p["dim"])
     if cfg.family == "convdiff":
-        return (ops.convdiff(p["N"], p["dim"], p["beta"]),
-                ops.convdiff_interval(p["N"], p["dim"], p["beta"]))
+        A = ops.convdiff(p["N"], p["dim"], p["beta"])
+        # a real spectral interval exists only for cell Peclet numbers < 1
+        if max(abs(b) for b in p["beta"]) / (2.0 * (p["N"] + 1)) >= 1.0:
+            return A, None
+        return A, ops.convdiff_interval(p["N"], p["dim"], p["beta"])
     if cfg.family == "wilson":
         return ops.wilson_dirac(p["L"], p["m0"], seed=p["link_seed"]), None
     if cfg.family == "graph":

@@ -255,8 +255,9 @@ class Poly:
         return cls(h)
 
     def set_newton_eval(self, mode: str) -> "Poly":
-        """ppf_poly_set_newton_eval: "horner" (P:354, default) or "basis"."""
-        check(_lib().ppf_poly_set_newton_eval(self.h, {"horner": 0, "basis": 1}[mode]))
+        """ppf_poly_set_newton_eval: "horner" (P:354, default), "basis" or "pairs"
+        (real conjugate-pair form for real operators)."""
+        check(_lib().ppf_poly_set_newton_eval(self.h, {"horner": 0, "basis": 1, "pairs": 2}[mode]))
         return self
 
     @classmethod

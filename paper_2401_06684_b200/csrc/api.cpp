@@ -674,8 +674,14 @@ ppf_status ppf_contour_from_ritz(const double* theta, int ntheta, double r_min, 
 ppf_status ppf_poly_set_newton_eval(ppf_poly* q, int mode) {
   PPF_API_BEGIN
   PPF_REQUIRE(q, "NULL polynomial");
-  PPF_REQUIRE(mode == 0 || mode == 1, "mode must be 0 (Horner) or 1 (forward Newton basis)");
-  q->newton_eval = mode;
+  PPF_REQUIRE(mode >= 0 && mode <= 2,
+              "mode must be 0 (Horner), 1 (forward Newton basis) or 2 (real conjugate pairs)");
+  if (mode == 2) {
+    PPF_REQUIRE(q->kind == PPF_POLY_NEWTON, "real-pair form needs a Newton polynomial");
+    real_pair_form(*q);  // reorders nodes, recomputes dd, sets newton_eval = 2
+  } else {
+    q->newton_eval = mode;
+  }
   PPF_API_END
 }
 

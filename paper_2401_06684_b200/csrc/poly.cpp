@@ -241,6 +241,105 @@ std::vector<zc> ritz_polygon(const std::vector<zc>& theta, double r_min, double 
   return z;
 }
 
+// Real-arithmetic form of a Newton polynomial whose nodes are closed under
+// conjugation (the Ritz values of a real operator): Lejà order with each
+// complex node immediately followed by its conjugate, divided differences of
+// z^{-1/2} in that order, then the coefficients c_j in the real basis
+//   P_0 = 1,  P_{j+1} = (z - a_j) P_j                    (real node, or the first of a pair)
+//             P_{j+1} = (z - a_j) P_j + b_j^2 P_{j-1}      (the second of a pair a +- i b)
+// (P_{j+2} = ((z-a)^2 + b^2) P_j = N_{j+2}); with N_{j+1} = P_{j+1} - i b P_j
+// inside a pair, q = sum dd_j N_j = sum c_j P_j has c_j = dd_j - i b dd_{j+1},
+// c_{j+1} = dd_{j+1} there and c_j = dd_j elsewhere -- real for a real q.
+void real_pair_form(ppf_poly& q) {
+  const int d = int(q.nodes.size());
+  std::vector<zc> th = q.nodes;
+  const double scale = [&] {
+    double m = 0.0;
+    for (auto& t : th) m = std::max(m, std::abs(t));
+    return m;
+  }();
+  // representatives: real nodes and the Im > 0 member of each pair
+  std::vector<zc> rep;
+  std::vector<char> used(d, 0);
+  for (int i = 0; i < d; ++i) {
+    if (used[i]) continue;
+    if (std::fabs(th[i].imag()) <= 1e-12 * scale) {
+      rep.push_back(zc(th[i].real(), 0.0));
+      used[i] = 1;
+      continue;
+    }
+    int best = -1;
+    for (int j = 0; j < d; ++j)
+      if (j != i && !used[j] && (best < 0 || std::abs(th[j] - std::conj(th[i])) < std::abs(th[best] - std::conj(th[i]))))
+        best = j;
+    if (best < 0 || std::abs(th[best] - std::conj(th[i])) > 1e-8 * scale)
+      fail(PPF_EINVAL, "nodes are not closed under conjugation: no real-arithmetic form");
+    const zc m = 0.5 * (th[i] + std::conj(th[best]));  // symmetrise the pair
+    rep.push_back(zc(m.real(), std::fabs(m.imag())));
+    used[i] = used[best] = 1;
+  }
+  // Lejà order over representatives, each complex one followed by its conjugate
+  std::stable_sort(rep.begin(), rep.end(), [](const zc& x, const zc& y) {
+    if (x.real() != y.real()) return x.real() < y.real();
+    return x.imag() < y.imag();
+  });
+  std::vector<zc> order;
+  std::vector<char> taken(rep.size(), 0);
+  auto push = [&](size_t r) {
+    taken[r] = 1;
+    order.push_back(rep[r]);
+    if (rep[r].imag() != 0.0) order.push_back(std::conj(rep[r]));
+  };
+  size_t first = 0;
+  for (size_t r = 1; r < rep.size(); ++r)
+    if (std::abs(rep[r]) > std::abs(rep[first])) first = r;
+  push(first);
+  while (order.size() < size_t(d)) {
+    size_t best = rep.size();
+    double bv = -HUGE_VAL;
+    for (size_t r = 0; r < rep.size(); ++r) {
+      if (taken[r]) continue;
+      double sc = 0.0;
+      for (const zc& o : order) sc += std::log(std::abs(rep[r] - o));
+      if (best == rep.size() || sc > bv) {
+        best = r;
+        bv = sc;
+      }
+    }
+    push(best);
+  }
+  q.nodes = order;
+  q.dd = divided_differences_invsqrt(order);
+  q.rp_a.assign(d, 0.0);
+  q.rp_b2.assign(d, 0.0);
+  q.rp_c.assign(d, 0.0);
+  double cmax = 0.0, imax = 0.0;
+  for (int j = 0; j < d;) {
+    if (order[j].imag() == 0.0) {
+      q.rp_a[j] = order[j].real();
+      q.rp_c[j] = q.dd[j].real();
+      imax = std::max(imax, std::fabs(q.dd[j].imag()));
+      cmax = std::max(cmax, std::fabs(q.dd[j].real()));
+      ++j;
+    } else {
+      const double a = order[j].real(), bb = order[j].imag();
+      q.rp_a[j] = a;
+      q.rp_a[j + 1] = a;
+      q.rp_b2[j + 1] = bb * bb;  // step from P_{j+1} to P_{j+2} adds b^2 P_j
+      const zc cj = q.dd[j] - zc(0.0, bb) * (j + 1 < d ? q.dd[j + 1] : zc(0.0, 0.0));
+      const zc cj1 = j + 1 < d ? q.dd[j + 1] : zc(0.0, 0.0);
+      q.rp_c[j] = cj.real();
+      q.rp_c[j + 1] = cj1.real();
+      imax = std::max({imax, std::fabs(cj.imag()), std::fabs(cj1.imag())});
+      cmax = std::max({cmax, std::fabs(cj.real()), std::fabs(cj1.real())});
+      j += 2;
+    }
+  }
+  if (imax > 1e-8 * std::max(cmax, 1e-300))
+    fail(PPF_EINVAL, "real-basis coefficients are not real (nodes not conjugate-symmetric?)");
+  q.newton_eval = 2;
+}
+
 std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& x) {
   const int n = int(x.size());
   std::vector<zc> dd(n);

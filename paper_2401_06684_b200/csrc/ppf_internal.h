@@ -153,7 +153,8 @@ struct ppf_poly {
   double a, b;                      // Chebyshev interval
   std::vector<double> c;            // Chebyshev coefficients c_0..c_deg
   std::vector<ppf::zc> nodes, dd;   // Newton form (Leja order)
-  int newton_eval = 0;              // 0: Horner, 1: forward Newton basis
+  int newton_eval = 0;              // 0: Horner, 1: forward Newton basis, 2: real pairs
+  std::vector<double> rp_a, rp_b2, rp_c;  // real-pair form (real_pair_form)
 };
 
 namespace ppf {
@@ -230,6 +231,7 @@ double chebyshev_eval(const ppf_poly& q, double z);
 zc poly_eval(const ppf_poly& q, zc z);
 std::vector<zc> leja_order(const std::vector<zc>& nodes);
 std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& nodes);
+void real_pair_form(ppf_poly& q);
 std::vector<zc> ritz_polygon(const std::vector<zc>& theta, double r_min, double step);
 void contour_ls_newton(const std::vector<zc>& z, int deg, std::vector<zc>& nodes,
                        std::vector<zc>& dd, double& min_re);

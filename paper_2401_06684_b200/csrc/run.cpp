@@ -99,7 +99,7 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms, int shape = 
 // a polynomial the operator's arithmetic can apply: Chebyshev always, Newton on
 // a real operator only with real nodes and divided differences
 bool poly_fits(const ppf_poly* q, ppf_dtype dt) {
-  if (q->kind == PPF_POLY_CHEBYSHEV || dt == PPF_C128) return true;
+  if (q->kind == PPF_POLY_CHEBYSHEV || dt == PPF_C128 || q->newton_eval == 2) return true;
   for (size_t i = 0; i < q->nodes.size(); ++i)
     if (q->nodes[i].imag() != 0.0 || q->dd[i].imag() != 0.0) return false;
   return true;
@@ -439,6 +439,33 @@ struct Runner {
         spmv(T[cur], out, epi(alpha, beta, 0.0, nullptr, c[0] - c[d], in));
       else
         spmv(T[cur], out, epi(alpha, beta, -1.0, T[prev], c[0], in));
+    } else if (q->newton_eval == 2) {
+      // real conjugate-pair form (real_pair_form): P_0 = v, P_{j+1} =
+      // (A - a_j) P_j [+ b_j^2 P_{j-1}], out = sum c_j P_j carried as the
+      // SpMV's second output -- real arithmetic for a real operator whose
+      // Ritz values come in complex pairs; three rotating buffers
+      const auto& ra = q->rp_a;
+      const auto& rb = q->rp_b2;
+      const auto& rc = q->rp_c;
+      if (d == 0) {
+        lincomb(in, out, rc[0]);
+        return;
+      }
+      const void* pm1 = nullptr;  // P_{j-1}
+      const void* pj = in;        // P_j
+      for (int j = 0; j < d; ++j) {
+        void* dst = T[j % 3];
+        Epi e = epi(1.0, -ra[j], rb[j], rb[j] != 0.0 ? pm1 : nullptr, 0.0, nullptr);
+        e.acc = out;
+        e.s_acc[0] = rc[j + 1];
+        if (j == 0) {
+          e.acc_init = true;
+          e.s_acc0[0] = rc[0];
+        }
+        spmv(pj, dst, e);
+        pm1 = pj;
+        pj = dst;
+      }
     } else if (q->newton_eval == 1) {
       // forward Newton basis: p_0 = v, p_{j+1} = (A - theta_j) p_j,
       // out = sum_j dd_j p_j accumulated by the SpMV's second output (the
@@ -1138,14 +1165,16 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
     for (int i = 0; i < d; ++i) Hd[size_t(i) + size_t(d - 1) * d] += std::norm(hs) * f[i];
   }
   std::vector<zc> theta = eigenvalues(d, Hd);
+  bool pairs = false;
   if (A->dtype == PPF_R64) {
-    // a real operator runs the chain in real arithmetic: the Ritz values must
-    // be real (they are for the graph Laplacians of P:561-563); complex pairs
-    // need a complex (PPF_C128) plan of the same matrix
+    // a real operator runs the chain in real arithmetic: real Ritz values are
+    // used as they are; complex ones come in conjugate pairs and get the
+    // real-pair form (real_pair_form) below
     for (auto& t : theta) {
       if (std::abs(t.imag()) > 1e-12 * std::abs(t))
-        fail(PPF_EINVAL, "complex Ritz values of a real operator: use a PPF_C128 plan");
-      t = zc(t.real(), 0.0);
+        pairs = true;
+      else
+        t = zc(t.real(), 0.0);
     }
   }
   for (auto& t : theta)
@@ -1157,6 +1186,14 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
   q->a = q->b = 0.0;
   q->nodes = leja_order(theta);
   q->dd = divided_differences_invsqrt(q->nodes);
+  if (pairs) {
+    try {
+      real_pair_form(*q);
+    } catch (...) {
+      delete q;
+      throw;
+    }
+  }
   *out = q;
   PPF_API_END
 }

@@ -419,3 +419,37 @@ def test_contour_ls_ritz_polygon_graph(ctx):
     # (Q27) on a non-normal operator: the H bar is the measured-amplification
     # class (Q28), x at the north_star bar
     _check(ctx, res_o, xg, rep, complex_=True, h_tol=1e-6)
+
+
+@pytest.mark.parametrize("fmt", ["sell64", "csr"])
+def test_real_pair_form_run(ctx, fmt):
+    """SURVEY NEXT-2's real-arithmetic conjugate pairs: the convection-dominated
+    C8s operator is real with complex-pair Ritz values.  (i) The device Ritz
+    construction on the real plan returns the real-pair form (nodes agree with
+    the oracle's as multisets); (ii) with the oracle's q imported and converted,
+    the fp64 run matches the oracle's complex-arithmetic run: x, H, m."""
+    from oracle import newton
+    cfg = configs.CONFIGS["C8s"]
+    A, b, _ = configs.build("C8s")
+    op = Operator(A.to_scipy())
+    qo, _, _ = newton.ritz_newton(op, b, 9)
+    assert np.abs(qo.nodes.imag).max() > 1.0
+    C_ = 64 if fmt == "sell64" else 32
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt=fmt[:4] if fmt != "csr" else "csr", C_=C_))
+    ql = pp.Poly.ritz_newton(ctx, M, dev(b), 9)
+    nodes = ql.export()["nodes"]
+    assert np.abs(np.sort_complex(nodes) - np.sort_complex(qo.nodes)).max() < 1e-7 * np.abs(qo.nodes).max()
+    res_o = krylov.run(op, b, qo, func="sqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                       tol=cfg.tol)
+    res_o.x = res_o.x.real
+    res_o.H = res_o.H.real
+    q = pp.Poly.newton(qo.nodes, qo.dd).set_newton_eval("pairs")
+    xg, rep = pp.run(ctx, M, q, dev(b), func="sqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
+                     tol=cfg.tol)
+    assert rep.term == "converged"
+    _check(ctx, res_o, xg, rep, h_tol=1e-10)
+    # the device's own real-pair q converges to the same tolerance
+    x2, rep2 = pp.run(ctx, M, ql, dev(b), func="sqrt", krylov="cgs2", m_max=cfg.m_max,
+                      stop="est", tol=cfg.tol)
+    assert rep2.term == "converged" and abs(rep2.iterations - res_o.m) <= 1
+    assert np.linalg.norm(host(x2) - res_o.x) <= 1e-7 * np.linalg.norm(res_o.x)

@@ -254,3 +254,29 @@ def test_plan_halo_lists_two_slabs():
         assert np.array_equal(got, plane)
         assert len(p.halo_recv(rank)) == 0
         assert p.info()["halo_total"] == N * N
+
+
+def test_real_pair_form_same_polynomial():
+    """ppf_poly_set_newton_eval("pairs") on a Newton q with conjugate-pair nodes
+    (the Ritz values of the real, convection-dominated C8s operator): the
+    reordered real form is the same polynomial as the oracle's Newton form
+    (evaluated at points off the nodes) and still interpolates z^{-1/2}."""
+    from oracle.spmv import Operator
+    A, b, _ = configs.build("C8s")
+    qo, _, _ = newton.ritz_newton(Operator(A.to_scipy()), b, 9)
+    assert np.abs(qo.nodes.imag).max() > 1.0
+    q = Poly.newton(qo.nodes, qo.dd).set_newton_eval("pairs")
+    ex = q.export()
+    nodes = ex["nodes"]
+    # pairs adjacent: every complex node is followed by its conjugate
+    i = 0
+    while i < len(nodes):
+        if abs(nodes[i].imag) > 0:
+            assert nodes[i + 1] == np.conj(nodes[i])
+            i += 2
+        else:
+            i += 1
+    z = nodes.real.mean() + np.abs(nodes).max() * 0.3 * np.exp(1j * np.linspace(0, 6, 40))
+    ref = newton.evaluate(qo, z)
+    assert np.abs(q.eval(z) - ref).max() <= 1e-9 * np.abs(ref).max()
+    assert np.abs(q.eval(qo.nodes) - qo.nodes ** -0.5).max() <= 1e-8 * np.abs(qo.nodes ** -0.5).max()
