@@ -31,6 +31,8 @@ CASES = {
     "c5s_ritz": ("C5s", 16, dict(krylov="cgs2", stop="est")),
     "c6s_sign": ("C6s", 7, dict(krylov="cgs2", stop="est")),
     "c7s_graph_basis": ("C7s", 7, dict(krylov="cgs2", stop="est", check_every=4)),
+    # m = 76 > the 24-column CGS2 tile: tiled sweeps with rank-local partials
+    "c2_deg5_tiles": ("C2", 5, dict(krylov="cgs2", stop="est")),
 }
 WORLD = {"c4s_cgs2_sqrt": 3, "c6s_sign": 2}  # default 2 ranks
 
