@@ -14,6 +14,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -800,10 +801,12 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   const double brt = o->breakdown_rtol > 0.0 ? o->breakdown_rtol : 1e-14;
   Runner R(ctx, A, q, m_max, work, bytes, ws_shape(q, o), right);
   R.power = power;
-  // graphs pay where launches dominate: matrices of < 256 MB (L2-scale: C1,
-  // C2, the graph Laplacian, Table 1's 100^3); at C3-C5 one SpMV is 0.1-0.3 ms
+  // graphs pay most where launches dominate (L2-scale matrices: C1, C2, the
+  // graph Laplacian, Table 1's 100^3: C2 deg 20 6.7 -> 4.7 ms) and still trim
+  // the inter-kernel gaps at C3/C4 (-0.4..0.6%)
+  const bool big = double(A->stored) * double(R.sc + 4) >= 256e6;
   R.use_graph = (ws_shape(q, o) & WS_GRAPH) && ctx->use_graphs && !ctx->profile &&
-                A->nranks == 1 && double(A->stored) * double(R.sc + 4) < 256e6;
+                A->nranks == 1;
   const int64_t n = R.n;
   const size_t vb = size_t(n) * R.sc;
   double t_dense = 0.0;
@@ -845,7 +848,9 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   // device does not idle during the D2H copy, f(H_m) and the relaunch.  If the
   // run stops there, that work (<= LOOKAHEAD SpMVs) is discarded.  Not with
   // right preconditioning one-pass, whose checkpoint itself uses the device.
-  const int LOOKAHEAD = (o->stop == PPF_STOP_EST && !(right && !twopass)) ? 2 : 0;
+  // (with the step graph the second call is the whole chain: for large
+  // matrices only the plain SpMV runs ahead, so at most one SpMV is wasted)
+  const int LOOKAHEAD = (o->stop == PPF_STOP_EST && !(right && !twopass)) ? ((R.use_graph && big) ? 1 : 2) : 0;
   // the basis the iterate is combined from: V_m, or Y_m (right, one-pass)
   auto basis0 = [&]() -> const void* { return (right && !twopass) ? R.Yb(0) : R.V(0); };
   std::vector<Runner::Call> calls = R.record_step(0);
