@@ -76,6 +76,7 @@ def parse():
                    help="contour: least-squares q on the circle |z - (4+m0)| = 2.2 (P:359-404; "
                         "Wilson configs); contour-ritz: least squares on the polygon of 60 Ritz "
                         "values (P:562-563; complex arithmetic, as the paper notes)")
+    p.add_argument("--m-max", type=int, default=None, help="override the config's m_max")
     p.add_argument("--check-every", type=int, default=1,
                    help="k of the stopping check (PAPER.md:424 uses 64/d)")
     p.add_argument("--split", type=int, default=0,
@@ -345,7 +346,7 @@ def main():
     krylov_m = args.krylov or cfg.krylov
     power = 2 if cfg.func in ("sign", "invsqrt_sq") else 1
     newton_eval = args.newton_eval or ("basis" if cfg.family == "graph" else "horner")
-    run_kw = dict(func=cfg.func, krylov=krylov_m, m_max=cfg.m_max, stop="est", tol=cfg.tol,
+    run_kw = dict(func=cfg.func, krylov=krylov_m, m_max=args.m_max or cfg.m_max, stop="est", tol=cfg.tol,
                   check_every=args.check_every, record_history=False, precond=args.precond)
     q0 = make_q()
     opts = api.make_opts(**run_kw)
