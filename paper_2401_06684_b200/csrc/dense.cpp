@@ -106,11 +106,20 @@ void tridiag_invsqrt_e1(int m, const double* dd, const double* ee, double beta0,
   }
 }
 
-void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q) {
+// With `log` non-null the rotations are recorded there instead of being
+// accumulated into Q (Q is then left empty): y = Q R^{-1} Q^H e_1 only needs
+// Q^H e_1 and Q u, which the log replays in O(#rotations) -- a third of the
+// flops of the sweep saved.
+void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q, std::vector<CRot>* log) {
   auto h = [&](int i, int j) -> zc& { return H[size_t(i) + size_t(j) * m]; };
   auto q = [&](int i, int j) -> zc& { return Q[size_t(i) + size_t(j) * m]; };
-  Q.assign(size_t(m) * m, zc(0.0, 0.0));
-  for (int i = 0; i < m; ++i) q(i, i) = 1.0;
+  if (log) {
+    Q.clear();
+    log->clear();
+  } else {
+    Q.assign(size_t(m) * m, zc(0.0, 0.0));
+    for (int i = 0; i < m; ++i) q(i, i) = 1.0;
+  }
   for (int j = 0; j < m; ++j)
     for (int i = j + 2; i < m; ++i) h(i, j) = 0.0;  // Hessenberg input
   const double eps = 2.220446049250313e-16;
@@ -176,10 +185,14 @@ void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q) {
         h(i, k) = cg * h1 + std::conj(sg) * h2;
         h(i, k + 1) = -sg * h1 + cg * h2;
       }
-      for (int i = 0; i < m; ++i) {
-        const zc q1 = q(i, k), q2 = q(i, k + 1);
-        q(i, k) = cg * q1 + std::conj(sg) * q2;
-        q(i, k + 1) = -sg * q1 + cg * q2;
+      if (log) {
+        log->push_back({k, cg, sg});
+      } else {
+        for (int i = 0; i < m; ++i) {
+          const zc q1 = q(i, k), q2 = q(i, k + 1);
+          q(i, k) = cg * q1 + std::conj(sg) * q2;
+          q(i, k + 1) = -sg * q1 + cg * q2;
+        }
       }
       if (k > l) h(k + 1, k - 1) = 0.0;
     }
@@ -220,7 +233,8 @@ std::vector<zc> solve_dense_adjoint_ed(int m, const std::vector<zc>& H) {
 
 std::vector<zc> eigenvalues(int m, std::vector<zc> H) {
   std::vector<zc> Q;
-  complex_schur(m, H, Q);
+  std::vector<CRot> log;
+  complex_schur(m, H, Q, &log);
   std::vector<zc> ev(m);
   for (int i = 0; i < m; ++i) ev[i] = H[size_t(i) + size_t(i) * m];
   return ev;
@@ -228,7 +242,9 @@ std::vector<zc> eigenvalues(int m, std::vector<zc> H) {
 
 void general_invsqrt_e1(int m, const std::vector<zc>& H0, double beta0, std::vector<zc>& y) {
   std::vector<zc> T = H0, Q;
-  complex_schur(m, T, Q);
+  std::vector<CRot> log;
+  log.reserve(size_t(4) * m * m / 2 + 16);
+  complex_schur(m, T, Q, &log);
   auto t = [&](int i, int j) -> const zc& { return T[size_t(i) + size_t(j) * m]; };
   std::vector<zc> R(size_t(m) * m, zc(0.0, 0.0));
   auto r = [&](int i, int j) -> zc& { return R[size_t(i) + size_t(j) * m]; };
@@ -243,18 +259,29 @@ void general_invsqrt_e1(int m, const std::vector<zc>& H0, double beta0, std::vec
       r(i, j) = s / (r(i, i) + r(j, j));
     }
   }
-  // u = R^{-1} Q^H e1
-  std::vector<zc> u(m);
-  for (int i = 0; i < m; ++i) u[i] = std::conj(Q[size_t(0) + size_t(i) * m]);
+  // u = R^{-1} Q^H e1.  Q = G_1 G_2 ... G_K with G_t acting on columns
+  // (k, k+1) as [c, -s; conj(s), c]: Q^H e1 applies G_t^H in order, Q u
+  // applies G_t in reverse order.
+  std::vector<zc> u(m, zc(0.0, 0.0));
+  u[0] = 1.0;
+  for (const CRot& t : log) {
+    const zc a = u[t.k], b = u[t.k + 1];
+    u[t.k] = t.c * a + t.s * b;
+    u[t.k + 1] = -std::conj(t.s) * a + t.c * b;
+  }
   for (int i = m - 1; i >= 0; --i) {
     zc s = u[i];
     for (int k = i + 1; k < m; ++k) s -= r(i, k) * u[k];
     u[i] = s / r(i, i);
   }
+  for (size_t t = log.size(); t-- > 0;) {
+    const CRot& g = log[t];
+    const zc a = u[g.k], b = u[g.k + 1];
+    u[g.k] = g.c * a - g.s * b;
+    u[g.k + 1] = std::conj(g.s) * a + g.c * b;
+  }
   y.assign(m, zc(0.0, 0.0));
-  for (int k = 0; k < m; ++k)
-    for (int i = 0; i < m; ++i) y[i] += Q[size_t(i) + size_t(k) * m] * u[k];
-  for (int i = 0; i < m; ++i) y[i] *= beta0;
+  for (int i = 0; i < m; ++i) y[i] = beta0 * u[i];
 }
 
 // ---------------------------------------------------------------------------

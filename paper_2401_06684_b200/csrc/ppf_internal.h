@@ -212,7 +212,12 @@ namespace ppf {
 // y = beta0 * T^{-1/2} e1 for symmetric tridiagonal T (diag d[m], offdiag e[m-1]).
 void tridiag_invsqrt_e1(int m, const double* d, const double* e, double beta0, double* y);
 // Complex Schur H = Q T Q^H of a general m x m matrix (column-major, ld = m).
-void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q);
+struct CRot {  // a logged plane rotation of the complex Schur sweep (columns k, k+1)
+  int k;
+  double c;
+  zc s;
+};
+void complex_schur(int m, std::vector<zc>& H, std::vector<zc>& Q, std::vector<CRot>* log = nullptr);
 // y = beta0 * H^{-1/2} e1 via Schur -> triangular sqrt -> solve.
 void general_invsqrt_e1(int m, const std::vector<zc>& H, double beta0, std::vector<zc>& y);
 // y = beta0 * H^{-1/2} e1 for a REAL upper Hessenberg H (column-major, ld ldh):
