@@ -34,7 +34,7 @@ CASES = {
     # m = 76 > the 24-column CGS2 tile: tiled sweeps with rank-local partials
     "c2_deg5_tiles": ("C2", 5, dict(krylov="cgs2", stop="est")),
 }
-WORLD = {"c4s_cgs2_sqrt": 3, "c6s_sign": 2}  # default 2 ranks
+WORLD = {"c4s_cgs2_sqrt": 3, "c3s_lanczos": 4, "c6s_sign": 2}  # default 2 ranks
 
 
 def _slab_bounds(cfg, n, world):
