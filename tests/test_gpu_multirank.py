@@ -1,13 +1,20 @@
 """The sharded (nranks > 1) path of ppf_run end to end with two processes on
 one device: each rank owns a contiguous row slab (whole grid
 planes / lattice time slices), exchanges its halo index lists over gloo, and
-runs the library with a HOST transport (ppf_ctx_set_transport) that moves the
-packed boundary entries and sums the reduction partials over gloo.  The
-kernels of the two ranks never wait on each other on the device -- the hosts
+runs the library with either
+  * "host": a HOST transport (ppf_ctx_set_transport) that moves the packed
+    boundary entries and sums the reduction partials over gloo, or
+  * "nccl": the library's own NCCL code path (halo send/recv on the comm
+    stream overlapped with the diagonal-block SpMV, allreduce on the compute
+    stream), linked against tests/native/fake_nccl.cpp -- real NCCL refuses
+    two ranks on one device; the stand-in keeps NCCL's stream ordering and
+    moves the bytes through host staging and Unix sockets.
+The kernels of the ranks never wait on each other on the device -- the hosts
 do -- so this verifies the distributed algorithm (halo pack / halo block,
 rank-local reductions + allreduce + finalise, redundant f(H_m), the Ritz setup
-on a sharded operator), not multi-GPU performance.  The gathered slabs must
-match the single-process oracle."""
+on a sharded operator) and the library's stream/event ordering around its
+collectives, not multi-GPU performance.  The gathered slabs must match the
+single-process oracle."""
 import os
 import socket
 import tempfile
@@ -49,10 +56,13 @@ def _slab_bounds(cfg, n, world):
     return [c * per for c in cuts]
 
 
-def _worker(rank, world, port, case, out_path, q_path):
+def _worker(rank, world, port, case, out_path, q_path, fake_lib):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    if fake_lib:
+        from paper_2401_06684_b200 import _lib
+        _lib.LIB_PATH = fake_lib
     import paper_2401_06684_b200 as pp
     name, deg, kw = CASES[case]
     cfg = configs.CONFIGS[name]
@@ -67,7 +77,12 @@ def _worker(rank, world, port, case, out_path, q_path):
     dist.all_gather_object(all_needs, needs)
     for p in range(world):
         plan.set_halo_send(p, all_needs[p][rank] - lo)
-    ctx = pp.Context(0, rank=rank, nranks=world)
+    if fake_lib:
+        idl = [pp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idl, src=0)
+        ctx = pp.Context(0, rank=rank, nranks=world, nccl_id=idl[0])
+    else:
+        ctx = pp.Context(0, rank=rank, nranks=world)
 
     def exchange(send, scount, recv, rcount):
         ops, so, ro = [], 0, 0
@@ -84,7 +99,8 @@ def _worker(rank, world, port, case, out_path, q_path):
     def allreduce(buf):
         dist.all_reduce(torch.from_numpy(buf))
 
-    ctx.set_transport(exchange, allreduce)
+    if not fake_lib:
+        ctx.set_transport(exchange, allreduce)
     M = pp.Matrix(ctx, plan)
     bd = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).cuda()
     if cfg.poly == "ritz":
@@ -122,8 +138,15 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.fixture(scope="module")
+def fake_nccl_lib():
+    from tests.native import build_fake
+    return build_fake.build()
+
+
+@pytest.mark.parametrize("transport", ["host", "nccl"])
 @pytest.mark.parametrize("case", list(CASES))
-def test_two_rank_run_matches_oracle(case):
+def test_two_rank_run_matches_oracle(case, transport, request):
     import torch.multiprocessing as mp
     from oracle import chebyshev, krylov, newton
     from oracle.spmv import Operator
@@ -142,12 +165,13 @@ def test_two_rank_run_matches_oracle(case):
     else:
         qo = chebyshev.coefficients(*iv, deg)
     world = WORLD.get(case, 2)
+    fake = request.getfixturevalue("fake_nccl_lib") if transport == "nccl" else ""
     with tempfile.TemporaryDirectory() as td:
         out = os.path.join(td, "x.npy")
         q_path = os.path.join(td, "q.npy")
         if cfg.poly == "ritz":
             np.save(q_path, np.stack([qo.nodes, qo.dd]))
-        mp.spawn(_worker, args=(world, _free_port(), case, out, q_path), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), case, out, q_path, fake), nprocs=world, join=True)
         x = np.load(out)
         ms = open(out + ".m").read().split()
         nodes = np.load(out + ".nodes.npy") if cfg.poly == "ritz" else None

@@ -280,3 +280,17 @@ def test_real_pair_form_same_polynomial():
     ref = newton.evaluate(qo, z)
     assert np.abs(q.eval(z) - ref).max() <= 1e-9 * np.abs(ref).max()
     assert np.abs(q.eval(qo.nodes) - qo.nodes ** -0.5).max() <= 1e-8 * np.abs(qo.nodes ** -0.5).max()
+
+
+def test_fake_nccl_test_library_links():
+    """The multi-process NCCL-path test (test_gpu_multirank, transport "nccl")
+    links the product objects with tests/native/fake_nccl.cpp; it must build
+    here and export the NCCL entry points the library calls."""
+    import subprocess
+    from tests.native import build_fake
+    path = build_fake.build()
+    syms = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True,
+                          text=True).stdout
+    for s in ("ncclCommInitRank", "ncclSend", "ncclRecv", "ncclAllReduce", "ncclGroupEnd",
+              "ppf_run"):
+        assert f" {s}\n" in syms
