@@ -84,6 +84,9 @@ def parse():
     p.add_argument("--no-profile", action="store_true",
                    help="time without the per-kernel CUDA events (no roofline breakdown)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                   help="N > 1: halo exchange and reductions over NCCL, or over peer memory "
+                        "(NVLink stores into the neighbours' windows, csrc/peer.cu)")
     p.add_argument("--test-fake-nccl", action="store_true",
                    help="TEST ONLY (tests/test_gpu_bench_dist.py): run the N>1 code path with every "
                         "rank on GPU 0, gloo for the bench's own collectives and the library "
@@ -327,11 +330,23 @@ def main():
         ctx = pp.Context(local, stream=stream)
     info = plan.info()
     M = pp.Matrix(ctx, plan)
+    if world > 1 and args.comm == "peer":
+        descs = [None] * world
+        dist.all_gather_object(descs, M.peer_window())
+        M.peer_connect(descs)
     split = M.set_split(args.split)
     plan.close()
     bd = torch.from_numpy(b).cuda()
     ritz_buf = torch.empty_like(bd)
     torch.cuda.synchronize()
+
+    ritz_ws = {}
+
+    def ritz_work(d):
+        # allocated once, outside the timed steps (and never while a peer waits)
+        if d not in ritz_ws:
+            ritz_ws[d] = pp.Poly.ritz_workspace(ctx, M, d)
+        return ritz_ws[d]
 
     def make_q():
         if args.plain:
@@ -346,7 +361,7 @@ def main():
             if cfg.params.get("ritz_start") == "Ab":
                 M.spmv(bd, ritz_buf)
                 start = ritz_buf
-            theta = pp.Poly.ritz_newton(ctx, M, start, 59).export()["nodes"]
+            theta = pp.Poly.ritz_newton(ctx, M, start, 59, work=ritz_work(59)).export()["nodes"]
             span = (theta.real.max() - theta.real.min()) + (theta.imag.max() - theta.imag.min())
             pts = api.contour_from_ritz(theta, 0.1, max(2.0 * span / 2000, 1e-6))
             return pp.Poly.contour_ls(pts, deg)
@@ -356,9 +371,11 @@ def main():
             # singular A (Thm 4.1): the Ritz values from A b, whose null-space
             # component is deflated (implicit desingularisation)
             M.spmv(bd, ritz_buf)
-            q = pp.Poly.ritz_newton(ctx, M, ritz_buf, deg, power=power, harmonic=args.harmonic)
+            q = pp.Poly.ritz_newton(ctx, M, ritz_buf, deg, power=power, harmonic=args.harmonic,
+                                    work=ritz_work(deg))
         else:
-            q = pp.Poly.ritz_newton(ctx, M, bd, deg, power=power, harmonic=args.harmonic)
+            q = pp.Poly.ritz_newton(ctx, M, bd, deg, power=power, harmonic=args.harmonic,
+                                    work=ritz_work(deg))
         return q.set_newton_eval(newton_eval)
 
     krylov_m = args.krylov or cfg.krylov
@@ -481,7 +498,9 @@ def main():
                           if mat_gb > 0.126 else
                           f"matrix {mat_gb * 1e3:.0f} MB per rank fits the 126 MB L2; no flush "
                           "(the method re-reads it every SpMV: L2-resident is its real regime)"),
-                   "parallelism": f"row slabs x{world} (NCCL halo + allreduce)" if world > 1 else "single GPU"},
+                   "parallelism": (f"row slabs x{world} (" + ("NCCL halo + allreduce" if args.comm == "nccl"
+                                   else "peer-memory halo push + rank-order reductions") + ")")
+                                  if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "fused SELL SpMV + Clenshaw/Newton epilogue (spmv class)",

@@ -25,7 +25,9 @@
  *   - "device" pointers are CUDA device memory owned by the caller (PyTorch
  *     allocations), 256-byte aligned, valid for the duration of the call and of
  *     the stream work it enqueues.  The library never calls cudaMalloc or
- *     cudaFree; size-query functions say how much the caller must provide.
+ *     cudaFree (one exception: the peer window of ppf_mat_peer_window, which a
+ *     CUDA IPC export needs as an allocation of its own); size-query functions
+ *     say how much the caller must provide.
  *     "host" pointers are ordinary host memory, only read/written during the
  *     call (the library copies what it needs).
  *   - Vectors passed to ppf_run are this rank's slab (n_local entries).
@@ -98,8 +100,10 @@ int ppf_abi_version(void);
  *   broadcast unique id) initialises an NCCL communicator; nranks > 1 with
  *   id128 == NULL creates a context WITHOUT a communicator whose halo exchange
  *   is done by the caller through ppf_halo_pack / ppf_halo_buffers /
- *   ppf_spmv_local (testing the sharded SpMV in one process); ppf_run and
- *   ppf_spmv then return PPF_ESTATE.  nranks == 1 ignores id128.
+ *   ppf_spmv_local (testing the sharded SpMV in one process), through a host
+ *   transport (ppf_ctx_set_transport) or through peer memory
+ *   (ppf_mat_peer_window / ppf_mat_peer_connect); with none of these ppf_run
+ *   and ppf_spmv return PPF_ESTATE.  nranks == 1 ignores id128.
  * ------------------------------------------------------------------------- */
 ppf_status ppf_nccl_unique_id(void* out128);
 /* Host transport (nranks > 1 without NCCL): the caller moves the halo and sums
@@ -189,6 +193,49 @@ ppf_status ppf_mat_set_split(ppf_mat* A, int sell_ks, int* applied);
 ppf_status ppf_halo_pack(ppf_ctx* ctx, ppf_mat* A, const void* x);
 ppf_status ppf_halo_buffers(ppf_mat* A, void** send, void** recv);
 ppf_status ppf_spmv_local(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
+
+/* ----------------------------------------------------------------------------
+ * Peer-memory communication (SURVEY §8(e) "B200-native alternative for halos":
+ * direct peer loads/stores over NVLink instead of NCCL).  With a connected
+ * window, every halo exchange and every reduction of ppf_run / ppf_spmv on A
+ * goes through peer memory: a push kernel gathers this rank's boundary entries
+ * of x and STORES them straight into each neighbour's receive slot (NVLink
+ * writes, double-buffered by exchange epoch), then bumps the neighbour's arrival
+ * counter (system-scope atomic after a system fence); the neighbour's stream
+ * waits for the counter (cuStreamWaitValue32, GEQ -- a front-end wait, no
+ * spinning kernel) before its halo block.  The push runs on a communication
+ * stream concurrently with the diagonal-block SpMV.  Reductions: each rank
+ * stores its partial sums into slot `rank` of every rank's window and bumps
+ * their counters; after the wait every rank sums the slots in RANK ORDER, so
+ * the reduced values are bit-identical on all ranks and from run to run (the
+ * deterministic variant of SURVEY §8(e)).  No NCCL communicator is needed.
+ *
+ * ppf_mat_peer_window: allocates this rank's window (device memory owned by
+ *   the library -- an IPC export needs an allocation base -- freed with A:
+ *   counters, 2 x nranks reduction slots, 2 receive slots of halo_total
+ *   entries) and writes a PPF_PEER_DESC_BYTES descriptor to host `desc`
+ *   (CUDA IPC handle, process id, receive offsets and counts per peer).
+ *   The matrix must be sharded (nranks > 1, 1 < nranks <= PPF_PEER_MAX_RANKS)
+ *   with its send lists set.  The caller all-gathers the descriptors.
+ * ppf_mat_peer_connect: `descs` = nranks descriptors in rank order (host).
+ *   Maps every peer window: cudaIpcOpenMemHandle for another process, the
+ *   pointer itself for a rank of the same process (several contexts on one
+ *   device, used by the tests).  Checks that every peer's receive count from
+ *   this rank equals this rank's send count to it; PPF_EINVAL otherwise.
+ *   All ranks must then issue the same sequence of ppf_run / ppf_spmv calls
+ *   on A (the exchange epochs pair up by order).  ppf_mat_peer_connect(A, NULL)
+ *   returns A to the context's NCCL / host transport.  Connecting force-loads
+ *   every kernel of the library (lazy module loading would otherwise load a
+ *   kernel at its first launch, which waits for the device -- possibly for a
+ *   stream parked in a peer wait).  For the same reason query the workspace
+ *   sizes (ppf_workspace_bytes / ppf_ritz_workspace_bytes, which also size the
+ *   pinned host staging) and allocate before the ranks start a run: device or
+ *   pinned allocation in the middle of one synchronises the device.
+ * ------------------------------------------------------------------------- */
+#define PPF_PEER_DESC_BYTES 2048
+#define PPF_PEER_MAX_RANKS 64
+ppf_status ppf_mat_peer_window(ppf_mat* A, void* desc);
+ppf_status ppf_mat_peer_connect(ppf_mat* A, const void* descs);
 
 /* ----------------------------------------------------------------------------
  * Preconditioning polynomial q ~ z^{-1/2} (layer L1), a host object.

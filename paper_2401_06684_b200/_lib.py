@@ -12,6 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libppf.so")
 
 PPF_OK = 0
+PEER_DESC_BYTES = 2048   # include/ppf.h PPF_PEER_DESC_BYTES
 STATUS = {0: "PPF_OK", 1: "PPF_EINVAL", 2: "PPF_ECUDA", 3: "PPF_ENCCL", 4: "PPF_EWORKSPACE",
           5: "PPF_EBRANCH", 6: "PPF_EDENSE", 7: "PPF_ESTATE"}
 R64, C128 = 0, 1
@@ -99,6 +100,8 @@ SIGNATURES = {
                               C.POINTER(C.c_longlong)]),
     "ppf_hessenberg": (C.c_int, [vp, C.c_int, vp, C.POINTER(C.c_int), dblp]),
     "ppf_profile_enable": (C.c_int, [vp, C.c_int]),
+    "ppf_mat_peer_window": (C.c_int, [vp, vp]),
+    "ppf_mat_peer_connect": (C.c_int, [vp, vp]),
     "ppf_profile_read": (C.c_int, [vp, C.c_int, C.POINTER(C.c_longlong), dblp, dblp]),
     "ppf_dense_invsqrt_e1": (C.c_int, [C.c_int, C.c_int, vp, C.c_int, C.c_double, C.c_int, vp]),
 }

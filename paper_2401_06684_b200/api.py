@@ -208,6 +208,23 @@ class Matrix:
         check(_lib().ppf_spmv(self.ctx.h, self.h, C.c_void_p(x.data_ptr()),
                               C.c_void_p(y.data_ptr())))
 
+    def peer_window(self) -> bytes:
+        """ppf_mat_peer_window: allocate this rank's peer-memory window; returns its
+        PPF_PEER_DESC_BYTES descriptor for the caller to all-gather."""
+        buf = C.create_string_buffer(L.PEER_DESC_BYTES)
+        check(_lib().ppf_mat_peer_window(self.h, buf))
+        return buf.raw
+
+    def peer_connect(self, descs):
+        """ppf_mat_peer_connect: `descs` = every rank's descriptor in rank order
+        (None returns the matrix to NCCL / the host transport)."""
+        if descs is None:
+            check(_lib().ppf_mat_peer_connect(self.h, None))
+            return
+        blob = b"".join(bytes(d) for d in descs)
+        assert all(len(d) == L.PEER_DESC_BYTES for d in descs)
+        check(_lib().ppf_mat_peer_connect(self.h, C.create_string_buffer(blob, len(blob))))
+
     def set_split(self, sell_ks: int = 0) -> int:
         """ppf_mat_set_split: warps per SELL slice (0 = automatic); returns the value in force."""
         out = C.c_int()
@@ -241,18 +258,26 @@ class Poly:
 
     @classmethod
     def ritz_newton(cls, ctx: Context, A: Matrix, start, deg: int, power: int = 1,
-                    harmonic: bool = False) -> "Poly":
+                    harmonic: bool = False, work=None) -> "Poly":
         """Ritz values of deg+1 device Arnoldi steps with A^power
-        (power 2: the operator of func "invsqrt_sq" / "sign") from ``start``."""
-        torch = _torch()
-        nb = C.c_size_t()
-        check(_lib().ppf_ritz_workspace_bytes(ctx.h, A.h, deg, C.byref(nb)))
-        work = torch.empty(nb.value, dtype=torch.uint8, device=start.device)
+        (power 2: the operator of func "invsqrt_sq" / "sign") from ``start``.
+        ``work``: optional uint8 device tensor from ``ritz_workspace`` (allocated
+        here otherwise)."""
+        if work is None:
+            work = cls.ritz_workspace(ctx, A, deg)
         h = C.c_void_p()
         check(_lib().ppf_poly_ritz_newton_pow(ctx.h, A.h, C.c_void_p(start.data_ptr()), deg,
                                               int(power), int(bool(harmonic)),
-                                              C.c_void_p(work.data_ptr()), nb.value, C.byref(h)))
+                                              C.c_void_p(work.data_ptr()), work.numel(), C.byref(h)))
         return cls(h)
+
+    @staticmethod
+    def ritz_workspace(ctx: Context, A: Matrix, deg: int):
+        """ppf_ritz_workspace_bytes + the device scratch of the Ritz setup."""
+        torch = _torch()
+        nb = C.c_size_t()
+        check(_lib().ppf_ritz_workspace_bytes(ctx.h, A.h, deg, C.byref(nb)))
+        return torch.empty(max(nb.value, 256), dtype=torch.uint8, device=f"cuda:{ctx.device}")
 
     def set_newton_eval(self, mode: str) -> "Poly":
         """ppf_poly_set_newton_eval: "horner" (P:354, default), "basis" or "pairs"

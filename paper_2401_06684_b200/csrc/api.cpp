@@ -516,7 +516,11 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
   PPF_API_END
 }
 
-void ppf_mat_destroy(ppf_mat* m) { delete m; }
+void ppf_mat_destroy(ppf_mat* m) {
+  if (!m) return;
+  if (m->peer) ppf::peer_destroy(m->peer);
+  delete m;
+}
 
 ppf_status ppf_mat_set_split(ppf_mat* A, int ks, int* applied) {
   PPF_API_BEGIN

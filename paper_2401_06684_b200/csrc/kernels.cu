@@ -1026,18 +1026,20 @@ void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st) {
   post_launch("halo_pack_kernel");
 }
 
-void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st) {
+void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st,
+                       const void* recv) {
   if (A->halo_rows == 0) return;
+  if (!recv) recv = A->d_recv;
   const int blocks = int((A->halo_rows + 255) / 256);
   if (A->dtype == PPF_R64)
     halo_apply_kernel<double><<<blocks, 256, 0, st>>>(
         A->halo_rows, A->d_halo_rows, A->d_halo_ptr, A->d_halo_col,
-        static_cast<const double*>(A->d_halo_val), static_cast<const double*>(A->d_recv),
+        static_cast<const double*>(A->d_halo_val), static_cast<const double*>(recv),
         static_cast<double*>(out), s_ax[0]);
   else
     halo_apply_kernel<cplx><<<blocks, 256, 0, st>>>(
         A->halo_rows, A->d_halo_rows, A->d_halo_ptr, A->d_halo_col,
-        static_cast<const cplx*>(A->d_halo_val), static_cast<const cplx*>(A->d_recv),
+        static_cast<const cplx*>(A->d_halo_val), static_cast<const cplx*>(recv),
         static_cast<cplx*>(out), cplx{s_ax[0], s_ax[1]});
   post_launch("halo_apply_kernel");
 }
@@ -1241,5 +1243,8 @@ void launch_lanczos(ppf_dtype dt, int phase, int64_t n, const void* v, const voi
 #undef PPF_LZ
   post_launch("lanczos_kernel");
 }
+
+// a kernel of this translation unit (its module is force-loaded by peer.cu)
+const void* kernels_module_symbol() { return reinterpret_cast<const void*>(&finalize_kernel); }
 
 }  // namespace ppf

@@ -121,6 +121,10 @@ struct ppf_plan {
   bool sends_set = false;
 };
 
+namespace ppf {
+struct PeerState;
+}
+
 struct ppf_mat {
   ppf_ctx* ctx;
   ppf_dtype dtype;
@@ -145,6 +149,7 @@ struct ppf_mat {
   void* d_send;             // send_total scalars
   const int32_t* d_send_idx;
   std::vector<int64_t> recv_count, recv_off, send_count, send_off;  // per peer
+  ppf::PeerState* peer = nullptr;  // peer-memory window (peer.cu), null unless requested
 };
 
 struct ppf_poly {
@@ -261,7 +266,16 @@ void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_
 void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
 // the second output of an Epi with acc set, from a completed `out` (x: the SpMV input)
 void launch_acc(ppf_mat* A, const void* x, const void* out, const Epi& e, cudaStream_t st);
-void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st);
+// recv: the receive buffer to read (null: A->d_recv)
+void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st,
+                       const void* recv = nullptr);
+const void* kernels_module_symbol();
+// peer.cu: the peer-memory exchange (ppf_mat_peer_window / _connect)
+void peer_destroy(PeerState* p);
+bool peer_active(const ppf_mat* A);
+void peer_halo_begin(ppf_ctx* ctx, ppf_mat* A, const void* x);
+const void* peer_halo_wait(ppf_ctx* ctx, ppf_mat* A);
+void peer_allreduce(ppf_ctx* ctx, ppf_mat* A, double* raw, int nv, cudaStream_t st);
 // run.cpp: the sharded SpMV with communication/compute overlap
 void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e);
 bool poly_fits(const ppf_poly* q, ppf_dtype dt);

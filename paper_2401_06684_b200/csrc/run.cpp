@@ -192,6 +192,18 @@ static void halo_transport(ppf_ctx* ctx, ppf_mat* A, const void* x) {
 
 void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e) {
   cudaStream_t st = ctx->stream;
+  if (peer_active(A)) {
+    // peer memory (peer.cu): push on the comm stream || diagonal block here
+    const bool comm = A->send_total || A->halo_total;
+    if (comm) peer_halo_begin(ctx, A, x);
+    Epi ed = e;
+    ed.acc = nullptr;
+    launch_spmv(A, x, out, ed, st);
+    const void* recv = comm ? peer_halo_wait(ctx, A) : nullptr;
+    if (A->halo_rows) launch_halo_apply(A, out, e.s_ax, st, recv);
+    if (e.acc) launch_acc(A, x, out, e, st);
+    return;
+  }
   if (ctx->has_transport) {
     halo_transport(ctx, A, x);
     Epi ed = e;
@@ -202,7 +214,8 @@ void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e)
     return;
   }
   if (A->send_total || A->halo_total) {
-    if (!ctx->comm_stream) fail(PPF_ESTATE, "nranks > 1 needs a context with an NCCL communicator");
+    if (!ctx->nccl_comm)
+      fail(PPF_ESTATE, "nranks > 1 needs an NCCL communicator, a transport or a peer window");
     launch_halo_pack(A, x, st);
     PPF_CUDA(cudaEventRecord(ctx->ev_pack, st));
     PPF_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_pack, 0));
@@ -215,6 +228,24 @@ void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e)
   if (A->send_total || A->halo_total) PPF_CUDA(cudaStreamWaitEvent(st, ctx->ev_halo, 0));
   if (A->halo_rows) launch_halo_apply(A, out, e.s_ax, st);
   if (e.acc) launch_acc(A, x, out, e, st);
+}
+
+// Grow the context's pinned host staging to `need` bytes.  Pinned allocation
+// and release synchronise the device, so the workspace queries call this
+// ahead of a run: a sharded run on peer memory must not stall here while a
+// neighbour's stream waits for this rank (peer.cu).
+void ensure_pinned(ppf_ctx* ctx, size_t need) {
+  if (ctx->h_pinned_bytes >= need) return;
+  PPF_CUDA(cudaStreamSynchronize(ctx->stream));
+  PPF_CUDA(cudaFreeHost(ctx->h_pinned));
+  ctx->h_pinned = nullptr;
+  ctx->h_pinned_bytes = 0;
+  PPF_CUDA(cudaHostAlloc(&ctx->h_pinned, need, cudaHostAllocDefault));
+  ctx->h_pinned_bytes = need;
+}
+
+size_t pinned_need(const WsLayout& L, int m_max, size_t sc) {
+  return al256(size_t(L.ldh) * (m_max + 1) * sc + 64) + 2 * al256(size_t(m_max + 2) * 16);
 }
 
 namespace {
@@ -238,7 +269,9 @@ struct Runner {
   // then finalise them (sqrt, H entries, 1/norm) on the device; no-op on 1 rank.
   void reduce_fin(int op, int nv, void* o0, void* o1, void* o2, const void* ci) {
     if (!dist) return;
-    if (ctx->has_transport) {
+    if (peer_active(A)) {
+      peer_allreduce(ctx, A, rs.raw, nv, st);
+    } else if (ctx->has_transport) {
       double* hb = transport_stage(ctx, size_t(nv) * 8 + 64);
       PPF_CUDA(cudaMemcpyAsync(hb, rs.raw, size_t(nv) * 8, cudaMemcpyDeviceToHost, st));
       PPF_CUDA(cudaStreamSynchronize(st));
@@ -272,8 +305,8 @@ struct Runner {
     rs.max_blocks = L.max_blocks;
     dist = A->nranks > 1;
     if (dist) {
-      if (!c->nccl_comm && !c->has_transport)
-        fail(PPF_ESTATE, "nranks > 1 needs a context with an NCCL communicator or a transport");
+      if (!c->nccl_comm && !c->has_transport && !peer_active(A))
+        fail(PPF_ESTATE, "nranks > 1 needs an NCCL communicator, a transport or a peer window");
       rs.raw = reinterpret_cast<double*>(w + L.raw);
     }
     grid_vec = std::min(L.max_blocks, 4 * c->num_sms);
@@ -284,15 +317,7 @@ struct Runner {
     // grown on demand (the context keeps the largest)
     stage_h = al256(size_t(L.ldh) * (m_max + 1) * sc + 64);
     stage_y = al256(size_t(m_max + 2) * 16);
-    const size_t need = stage_h + 2 * stage_y;
-    if (ctx->h_pinned_bytes < need) {
-      PPF_CUDA(cudaStreamSynchronize(st));
-      PPF_CUDA(cudaFreeHost(ctx->h_pinned));
-      ctx->h_pinned = nullptr;
-      ctx->h_pinned_bytes = 0;
-      PPF_CUDA(cudaHostAlloc(&ctx->h_pinned, need, cudaHostAllocDefault));
-      ctx->h_pinned_bytes = need;
-    }
+    ensure_pinned(ctx, stage_h + 2 * stage_y);
   }
   size_t stage_h = 0, stage_y = 0;
 
@@ -1076,7 +1101,9 @@ ppf_status ppf_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, const ppf_poly* q
   PPF_API_BEGIN
   PPF_REQUIRE(ctx && A && bytes, "NULL argument");
   check_opts(o);
-  *bytes = ws_layout(A->n_local, A->dtype, o->m_max, ctx->num_sms, ws_shape(q, o)).total;
+  const WsLayout L = ws_layout(A->n_local, A->dtype, o->m_max, ctx->num_sms, ws_shape(q, o));
+  *bytes = L.total;
+  ensure_pinned(ctx, pinned_need(L, o->m_max, A->dtype == PPF_R64 ? 8 : 16));
   PPF_API_END
 }
 
@@ -1133,7 +1160,9 @@ ppf_status ppf_hessenberg(ppf_ctx* ctx, int ld, void* H, int* m, double* beta0) 
 ppf_status ppf_ritz_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, int deg, size_t* bytes) {
   PPF_API_BEGIN
   PPF_REQUIRE(ctx && A && bytes && deg >= 0 && deg < 255, "bad arguments");
-  *bytes = ws_layout(A->n_local, A->dtype, deg + 1, ctx->num_sms, WS_SQUARE).total;
+  const WsLayout L = ws_layout(A->n_local, A->dtype, deg + 1, ctx->num_sms, WS_SQUARE);
+  *bytes = L.total;
+  ensure_pinned(ctx, pinned_need(L, deg + 1, A->dtype == PPF_R64 ? 8 : 16));
   PPF_API_END
 }
 

@@ -144,16 +144,12 @@ def fake_nccl_lib():
     return build_fake.build()
 
 
-@pytest.mark.parametrize("transport", ["host", "nccl"])
-@pytest.mark.parametrize("case", list(CASES))
-def test_two_rank_run_matches_oracle(case, transport, request):
-    import torch.multiprocessing as mp
+def oracle_case(case):
+    """The single-process oracle run of a case: (cfg, A, b, iv, qo, res)."""
     from oracle import chebyshev, krylov, newton
-    from oracle.spmv import Operator
-    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from oracle.spmv import Operator, SquaredOperator
     name, deg, kw = CASES[case]
     cfg = configs.CONFIGS[name]
-    from oracle.spmv import SquaredOperator
     A, b, iv = configs.build(name)
     op = Operator(A.to_scipy())
     if cfg.poly == "ritz":
@@ -164,6 +160,26 @@ def test_two_rank_run_matches_oracle(case, transport, request):
             qo.nodes, qo.dd = qo.nodes.real.astype(complex), qo.dd.real.astype(complex)
     else:
         qo = chebyshev.coefficients(*iv, deg)
+    pre = kw.get("precond", "left")
+    ck = kw.get("check_every", 1)
+    if kw["krylov"] == "lanczos2p":
+        res = krylov.run_two_pass(op, b, qo, func=cfg.func, precond=pre, m_max=cfg.m_max,
+                                  stop=kw["stop"], tol=cfg.tol)
+    elif cfg.func == "sign":
+        res = krylov.run_sign(op, b, qo, krylov=kw["krylov"], m_max=cfg.m_max, stop=kw["stop"],
+                              tol=cfg.tol)
+    else:
+        res = krylov.run(op, b, qo, func=cfg.func, krylov=kw["krylov"], m_max=cfg.m_max,
+                         stop=kw["stop"], tol=cfg.tol, precond=pre, check_every=ck)
+    return cfg, A, b, iv, qo, res
+
+
+@pytest.mark.parametrize("transport", ["host", "nccl"])
+@pytest.mark.parametrize("case", list(CASES))
+def test_two_rank_run_matches_oracle(case, transport, request):
+    import torch.multiprocessing as mp
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    cfg, A, b, iv, qo, res = oracle_case(case)
     world = WORLD.get(case, 2)
     fake = request.getfixturevalue("fake_nccl_lib") if transport == "nccl" else ""
     with tempfile.TemporaryDirectory() as td:
@@ -177,17 +193,6 @@ def test_two_rank_run_matches_oracle(case, transport, request):
         nodes = np.load(out + ".nodes.npy") if cfg.poly == "ritz" else None
     if nodes is not None:  # the sharded Ritz setup (parity unpinned at ~1e-11, F6)
         assert np.abs(np.sort_complex(nodes) - np.sort_complex(qo.nodes)).max() < 1e-8
-    pre = kw.get("precond", "left")
-    ck = kw.get("check_every", 1)
-    if kw["krylov"] == "lanczos2p":
-        res = krylov.run_two_pass(op, b, qo, func=cfg.func, precond=pre, m_max=cfg.m_max,
-                                  stop=kw["stop"], tol=cfg.tol)
-    elif cfg.func == "sign":
-        res = krylov.run_sign(op, b, qo, krylov=kw["krylov"], m_max=cfg.m_max, stop=kw["stop"],
-                              tol=cfg.tol)
-    else:
-        res = krylov.run(op, b, qo, func=cfg.func, krylov=kw["krylov"], m_max=cfg.m_max,
-                         stop=kw["stop"], tol=cfg.tol, precond=pre, check_every=ck)
     ms_r = [int(v) for v in ms[0::2]]
     assert len(ms_r) == world and all(v == res.m for v in ms_r)   # every rank, the oracle's m
     assert np.linalg.norm(x - res.x) <= X_TOL * np.linalg.norm(res.x)
