@@ -114,6 +114,7 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
     c->h_pinned_bytes = size_t(66) * 65 * 16 + 2 * 2048;  // grown by ppf_run for larger m_max
     PPF_CUDA(cudaHostAlloc(&c->h_pinned, c->h_pinned_bytes, cudaHostAllocDefault));
     PPF_CUDA(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
+    if (nranks > 1) ppf::preload_kernels();
     if (nranks > 1 && id128) {
       ncclUniqueId id;
       std::memcpy(&id, id128, 128);

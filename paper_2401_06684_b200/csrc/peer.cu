@@ -236,6 +236,14 @@ void peer_destroy(PeerState* p) {
 
 bool peer_active(const ppf_mat* A) { return A->peer && A->peer->connected; }
 
+void preload_kernels() {
+  static bool done = false;  // per process; loading is idempotent, so a race is harmless
+  if (done) return;
+  preload_module(kernels_module_symbol());
+  preload_module(reinterpret_cast<const void*>(&peer_red_sum_kernel));
+  done = true;
+}
+
 static void ensure_comm_objects(ppf_ctx* ctx) {
   if (!ctx->comm_stream)
     PPF_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
@@ -445,8 +453,7 @@ ppf_status ppf_mat_peer_connect(ppf_mat* A, const void* descs) {
                                          int64_t(ctx->num_sms) * 2));
   ensure_comm_objects(ctx);
   wait_fn();  // fail now, not inside a run, if the driver lacks stream waits
-  preload_module(kernels_module_symbol());
-  preload_module(reinterpret_cast<const void*>(&peer_red_sum_kernel));
+  preload_kernels();
   P->connected = true;
   PPF_API_END
 }

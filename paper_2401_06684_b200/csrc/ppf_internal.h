@@ -273,6 +273,10 @@ const void* kernels_module_symbol();
 // peer.cu: the peer-memory exchange (ppf_mat_peer_window / _connect)
 void peer_destroy(PeerState* p);
 bool peer_active(const ppf_mat* A);
+// force-load every kernel of the library (multi-rank contexts): under lazy
+// module loading a first launch waits for the device, which a rank blocked in
+// a collective or a peer wait would turn into a cross-rank stall
+void preload_kernels();
 void peer_halo_begin(ppf_ctx* ctx, ppf_mat* A, const void* x);
 const void* peer_halo_wait(ppf_ctx* ctx, ppf_mat* A);
 void peer_allreduce(ppf_ctx* ctx, ppf_mat* A, double* raw, int nv, cudaStream_t st);
