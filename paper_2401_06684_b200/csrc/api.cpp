@@ -36,6 +36,22 @@ int auto_sell_ks(const ppf_mat* m, int num_sms) {
   return ks;
 }
 
+// Leading slices whose width is >= 4x the mean (and >= 32 entries per lane):
+// after a whole-matrix sigma sort (descending row length) these are the
+// power-law rows.  One warp per such slice would be the critical path of the
+// whole launch (C7: the 239-entry slices, 38.9 us/launch at KS = 1, 20.0 at a
+// uniform KS = 4 that idles the short slices' extra warps), so the SELL kernel
+// gives each of them a block of 8 warps.  0 when every slice is heavy.
+int64_t sell_heavy_prefix(const std::vector<int64_t>& ptr, int C) {
+  const int64_t ns = int64_t(ptr.size()) - 1;
+  if (ns <= 0) return 0;
+  const double mean = double(ptr[ns]) / (double(ns) * C);
+  const double thr = std::max(32.0, 4.0 * mean);
+  int64_t h = 0;
+  while (h < ns && double(ptr[h + 1] - ptr[h]) / C >= thr) ++h;
+  return h == ns ? 0 : h;
+}
+
 }  // namespace ppf
 
 using namespace ppf;
@@ -502,6 +518,7 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     m->csr_group = g;
   }
   m->sell_ks = auto_sell_ks(m, ctx->num_sms);
+  if (m->fmt == PPF_FMT_SELL && m->C == 32) m->sell_heavy = sell_heavy_prefix(p->diag.ptr, m->C);
   m->halo_rows = int64_t(p->halo.rows.size());
   m->halo_nnz = int64_t(p->halo.col.size());
   m->halo_total = p->recv_off.empty() ? 0 : p->recv_off.back();

@@ -131,21 +131,29 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
                                                     const T* __restrict__ val,
                                                     const T* __restrict__ x, T* __restrict__ out,
                                                     EpiT<T> e, bool has_x,
-                                                    const int32_t* __restrict__ perm) {
+                                                    const int32_t* __restrict__ perm,
+                                                    int64_t nheavy) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
-  const int part = warp % KS;
+  // the first nheavy slices (the longest rows after a whole-matrix sigma sort)
+  // get a whole block each, 8 warps splitting their entry columns; the rest
+  // KS warps per slice
+  const bool heavy = blockIdx.x < nheavy;
+  const int64_t slice = heavy ? int64_t(blockIdx.x)
+                              : nheavy + (int64_t(blockIdx.x) - nheavy) * (8 / KS) + warp / KS;
+  const int parts = heavy ? 8 : KS;
+  const int part = heavy ? warp : warp % KS;
   const bool live = slice < nslices;
   T acc = s_zero<T>();
   if (live) {
     const int64_t base = sptr[slice];
     const int w = int((sptr[slice + 1] - base) >> 5);
-    const int k0 = part * w / KS, k1 = (part + 1) * w / KS;
+    const int k0 = part * w / parts, k1 = (part + 1) * w / parts;
     const int32_t* cp = col + base + lane;
     const T* vp = val + base + lane;
     if constexpr (sizeof(T) == 8) {
       // fp64: ptxas' own 32-register schedule at full occupancy is faster
-      // (as for sell2_kernel; batching measured 4.2 vs 6.2 TB/s on C3)
+      // (as for sell2_kernel; batching measured 4.2 vs 6.2 TB/s on C3, and
+      // 3.4 vs 6.1 TB/s on C3 in this C = 32 layout; on C7's gathers: equal)
 #pragma unroll 4
       for (int k = k0; k < k1; ++k)
         acc = s_fma(__ldg(vp + 32 * k), __ldg(x + __ldg(cp + 32 * k)), acc);
@@ -171,8 +179,14 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
       for (; k < k1; ++k) acc = s_fma(ldg(vp + 32 * k), ldg(x + __ldg(cp + 32 * k)), acc);
     }
   }
-  if constexpr (KS > 1) {
-    __shared__ T red[8][32];
+  __shared__ T red[8][32];
+  if (heavy) {  // block-uniform
+    red[warp][lane] = acc;
+    __syncthreads();
+    if (warp != 0) return;
+#pragma unroll
+    for (int p = 1; p < 8; ++p) acc = s_add(acc, red[p][lane]);
+  } else if constexpr (KS > 1) {
     red[warp][lane] = acc;
     __syncthreads();
     if (part != 0) return;
@@ -885,6 +899,51 @@ void post_launch(const char* what) { cuda_check(cudaGetLastError(), what); }
 // ---------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------
+// SELL launch: KS warps per slice (A->sell_ks), optional second output (ACC)
+template <typename T, bool ACC>
+static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT<T>& et,
+                        bool has_x, cudaStream_t st) {
+  const int KS = A->sell_ks;
+  const int64_t spb = 8 / KS;  // slices per 256-thread block
+  const int64_t nh = A->C == 32 ? A->sell_heavy : 0;  // one block per heavy slice (sell1 only)
+  const int blocks = int(nh + (A->nslices - nh + spb - 1) / spb);
+  if (blocks == 0) return;
+#define PPF_KS(launch) \
+  switch (KS) {        \
+    case 1: launch(1); break; \
+    case 2: launch(2); break; \
+    case 4: launch(4); break; \
+    default: launch(8); break; \
+  }
+  if constexpr (sizeof(T) == 8) {
+    if (A->C == 64) {
+#define PPF_S2(K)                                                                         \
+  sell2_kernel<K, ACC><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+                                               reinterpret_cast<const double*>(val), xt, ot, et, \
+                                               has_x)
+      PPF_KS(PPF_S2)
+#undef PPF_S2
+      post_launch("sell2_kernel");
+      return;
+    }
+  }
+#define PPF_S1P(K)                                                                                  \
+  sell1_kernel<T, K, true, ACC><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+                                                        val, xt, ot, et, has_x, A->d_perm, nh)
+#define PPF_S1(K)                                                                                    \
+  sell1_kernel<T, K, false, ACC><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+                                                         val, xt, ot, et, has_x, nullptr, nh)
+  if (A->d_perm) {
+    PPF_KS(PPF_S1P)
+  } else {
+    PPF_KS(PPF_S1)
+  }
+#undef PPF_S1P
+#undef PPF_S1
+#undef PPF_KS
+  post_launch("sell1_kernel");
+}
+
 template <typename T>
 static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_t st) {
   const EpiT<T> et = to_epi<T>(e, x);
@@ -893,28 +952,9 @@ static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStrea
   T* ot = static_cast<T*>(out);
   const T* val = static_cast<const T*>(A->d_val);
   if (e.acc) {
-    // forward-Newton-basis chain step: KS = 1, second output acc
+    // forward-Newton-basis chain step: second output acc
     if (A->fmt == PPF_FMT_SELL) {
-      const int blocks = int((A->nslices + 7) / 8);
-      if (blocks == 0) return;
-      if constexpr (sizeof(T) == 8) {
-        if (A->C == 64) {
-          sell2_kernel<1, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col,
-                                                        reinterpret_cast<const double*>(val), xt, ot,
-                                                        et, has_x);
-          post_launch("sell2_kernel");
-          return;
-        }
-      }
-      if (A->d_perm)
-        sell1_kernel<T, 1, true, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr,
-                                                               A->d_col, val, xt, ot, et, has_x,
-                                                               A->d_perm);
-      else
-        sell1_kernel<T, 1, false, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr,
-                                                                A->d_col, val, xt, ot, et, has_x,
-                                                                nullptr);
-      post_launch("sell1_kernel");
+      launch_sell<T, true>(A, xt, ot, val, et, has_x, st);
     } else {
       const int G = A->csr_group;
       const int blocks = int((A->n_local * G + 255) / 256);
@@ -932,43 +972,7 @@ static void spmv_t(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStrea
     return;
   }
   if (A->fmt == PPF_FMT_SELL) {
-    const int KS = A->sell_ks;
-    const int64_t spb = 8 / KS;  // slices per 256-thread block
-    const int blocks = int((A->nslices + spb - 1) / spb);
-    if (blocks == 0) return;
-#define PPF_KS(launch) \
-  switch (KS) {        \
-    case 1: launch(1); break; \
-    case 2: launch(2); break; \
-    case 4: launch(4); break; \
-    default: launch(8); break; \
-  }
-    if constexpr (sizeof(T) == 8) {
-      if (A->C == 64) {
-#define PPF_S2(K)                                                                    \
-  sell2_kernel<K><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
-                                          reinterpret_cast<const double*>(val), xt, ot, et, has_x)
-        PPF_KS(PPF_S2)
-#undef PPF_S2
-        post_launch("sell2_kernel");
-        return;
-      }
-    }
-#define PPF_S1P(K)                                                                             \
-  sell1_kernel<T, K, true><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
-                                                   val, xt, ot, et, has_x, A->d_perm)
-#define PPF_S1(K)                                                                               \
-  sell1_kernel<T, K, false><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
-                                                    val, xt, ot, et, has_x, nullptr)
-    if (A->d_perm) {
-      PPF_KS(PPF_S1P)
-    } else {
-      PPF_KS(PPF_S1)
-    }
-#undef PPF_S1P
-#undef PPF_S1
-#undef PPF_KS
-    post_launch("sell1_kernel");
+    launch_sell<T, false>(A, xt, ot, val, et, has_x, st);
   } else {
     const int G = A->csr_group;
     const int64_t threads = A->n_local * G;

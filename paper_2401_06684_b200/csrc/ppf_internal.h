@@ -139,6 +139,7 @@ struct ppf_mat {
   const int32_t* d_perm;    // null unless sigma > 1
   int csr_group;            // lanes per row for the CSR kernel
   int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks
+  int64_t sell_heavy = 0;   // leading slices given a whole block each (see sell_heavy_prefix)
   // halo (nranks > 1)
   int64_t halo_rows, halo_nnz, halo_total, send_total;
   const int32_t* d_halo_rows;

@@ -116,6 +116,52 @@ def test_spmv_split_parity(ctx, ks, C_, which):
     assert M.set_split(0) >= 1
 
 
+def powerlaw_matrix(n, seed, complex_=False):
+    """Heavy-tailed row lengths (Zipf-like, a few rows of 300-1500 entries,
+    empty rows included) -- after a whole-matrix sigma sort the leading
+    slices are wide enough to take the SELL kernel's one-block-per-slice path
+    (sell_heavy_prefix)."""
+    rng = np.random.default_rng(seed)
+    lens = np.minimum((rng.pareto(1.2, n) * 3).astype(np.int64), n // 2)
+    lens[rng.choice(n, 40, replace=False)] = rng.integers(300, 1500, 40)
+    lens[rng.random(n) < 0.03] = 0
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+    cols = np.concatenate([np.sort(rng.choice(n, size=k, replace=False)) for k in lens]).astype(np.int64)
+    vals = rng.standard_normal(len(cols))
+    if complex_:
+        vals = vals + 1j * rng.standard_normal(len(cols))
+    return CSR(n, rp, cols, vals)
+
+
+@pytest.mark.parametrize("ks", [1, 2, 4])
+@pytest.mark.parametrize("complex_", [False, True])
+def test_spmv_heavy_slices_parity(ctx, ks, complex_):
+    """Power-law rows, whole-matrix sigma sort: the leading (heavy) slices get
+    a block of 8 warps each, the rest KS warps; every row matches the oracle
+    SpMV, and so does the forward-Newton-basis chain (second output) on it."""
+    n = 4099
+    A = powerlaw_matrix(n, 21 + ks, complex_)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32, sigma=32 * ((n + 31) // 32)))
+    assert M.set_split(ks) == ks
+    rng = np.random.default_rng(ks)
+    x = rng.standard_normal(n) + (1j * rng.standard_normal(n) if complex_ else 0)
+    yd = torch.full_like(dev(x), float("nan"))
+    M.spmv(dev(x), yd)
+    ref = A.to_scipy() @ x
+    absA = abs(A.to_scipy()) @ np.abs(x)
+    assert np.all(np.abs(host(yd) - ref) <= 1e-14 * absA + 1e-300)
+    # forward Newton basis (the chain's second output) on the same slices
+    th = 40.0 + 10.0 * rng.random(6)
+    qo = newton.from_nodes(th.astype(complex))
+    q = pp.Poly.newton(qo.nodes, qo.dd).set_newton_eval("basis")
+    got = host(q.apply(ctx, M, dev(x)))
+    ref = newton.apply(qo, Operator(A.to_scipy()), x.astype(complex))
+    if not complex_:
+        ref = ref.real
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
 def test_auto_split_choice(ctx):
     """The automatic split: KS = 1 for narrow rows and for matrices with many
     slices; a few-slice matrix with wide rows is split."""

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--split", type=int, default=0)
     ap.add_argument("--fmt", default="sell64")
+    ap.add_argument("--sigma", type=int, default=1, help="SELL sorting window (0: all rows)")
+    ap.add_argument("--eval", default=None, choices=["horner", "basis", "pairs"])
     a = ap.parse_args()
     cfg = configs.CONFIGS[a.config]
     A, iv = configs.operator(cfg)
@@ -31,12 +33,15 @@ def main():
     if cfg.complex_ and fmt[1] == 64:
         fmt = ("sell", 32)
     ctx = pp.Context(0)
-    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1]))
+    sigma = a.sigma if a.sigma > 0 else 32 * ((A.n + 31) // 32)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1], sigma=sigma))
     M.set_split(a.split)
     dt = torch.complex128 if cfg.complex_ else torch.float64
     x = torch.randn(A.n, dtype=dt, device="cuda")
-    if cfg.complex_:
+    if cfg.poly == "ritz":
         q = pp.Poly.ritz_newton(ctx, M, x, a.deg)
+        if a.eval:
+            q.set_newton_eval(a.eval)
     else:
         q = pp.Poly.chebyshev(*iv, a.deg)
     y = torch.empty_like(x)
