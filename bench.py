@@ -470,8 +470,12 @@ def main():
     traffic = None
     try:
         summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        traffic = summ.get("dominant_kernel_dram_bytes_per_launch")
-        traffic_note = summ.get("note")
+        if summ.get("config") == name and summ.get("deg") == deg and world == 1:
+            traffic = summ.get("dominant_kernel_dram_bytes_per_launch")
+            traffic_note = summ.get("note")
+        else:
+            traffic_note = (f"the committed ncu capture (profiles/ncu_summary.json) is of "
+                            f"{summ.get('config')} deg {summ.get('deg')}, not this workload")
     except Exception:
         traffic_note = None
     m_iter = reps[-1].iterations
@@ -511,6 +515,7 @@ def main():
         "breakdown_gbs": {k: (v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] else None)
                           for k, v in prof.items()},
         "gpu_launches": launches,
+        "host_dense_ms_per_step": 1e3 * sum(r.seconds_host_dense for r in reps) / len(reps),
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": n_bytes * (2 if ritz else 1),
                 "d2h_bytes_per_step": n_bytes},
         "clocks": clocks,

@@ -878,11 +878,20 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   const int LOOKAHEAD = (o->stop == PPF_STOP_EST && !(right && !twopass)) ? ((R.use_graph && big) ? 1 : 2) : 0;
   // the basis the iterate is combined from: V_m, or Y_m (right, one-pass)
   auto basis0 = [&]() -> const void* { return (right && !twopass) ? R.Yb(0) : R.V(0); };
+  // Run-ahead: when f(H_m) on the host takes longer than the host waits for
+  // H_m (host-bound: small operators, large m, e.g. C2 deg 5 at m = 76), the
+  // whole next step -- operator chain AND orthogonalisation, both device-only
+  // -- is enqueued before the host waits for H_m, so the device runs step m+1
+  // while the host evaluates f(H_m).  If the run stops at m, step m+1 is
+  // discarded (V_1..V_m, H_m and the counters are untouched by it).  Decided
+  // again at every checkpoint from the previous checkpoint's two times.
+  bool run_ahead = false, ortho_ahead = false;
   std::vector<Runner::Call> calls = R.record_step(0);
   size_t played = 0;
   for (int j = 0; j < m_max; ++j) {
     for (; played < calls.size(); ++played) R.play(calls[played]);
-    R.orthogonalise(j, lanczos);
+    if (!ortho_ahead) R.orthogonalise(j, lanczos);
+    ortho_ahead = false;
     m = j + 1;
     mvms += per_step;
     const bool check = (o->stop != PPF_STOP_FIXED_M) && (m % k == 0 || m == m_max);
@@ -898,9 +907,17 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     if (more) {
       calls = R.record_step(j + 1);
       played = 0;
-      for (; played < calls.size() && played < size_t(LOOKAHEAD); ++played) R.play(calls[played]);
+      if (run_ahead && LOOKAHEAD > 0) {
+        for (; played < calls.size(); ++played) R.play(calls[played]);
+        R.orthogonalise(j + 1, lanczos);
+        ortho_ahead = true;
+      } else {
+        for (; played < calls.size() && played < size_t(LOOKAHEAD); ++played) R.play(calls[played]);
+      }
     }
+    const auto tw = std::chrono::steady_clock::now();
     R.fetch_H_wait(m + 1, m, Hh, beta0);
+    const double t_wait = std::chrono::duration<double>(std::chrono::steady_clock::now() - tw).count();
     const double hsub = std::abs(Hh[size_t(m) + size_t(m - 1) * (m + 1)]);
     // earlier breakdown inside the stride?
     int mb = m;
@@ -918,7 +935,11 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
       Hs = H2;
     }
     y = dense_y(Hs, mb + 1, mb, beta0, lanczos);
-    t_dense += std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
+    const double t_this = std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
+    t_dense += t_this;
+    // one rank only: the decision comes from host timings, and the ranks'
+    // collectives must pair up (every rank has to run the same steps)
+    run_ahead = A->nranks == 1 && t_this > t_wait;
     if (!y_prev.empty()) {
       if (right && !twopass) {
         // Y_m is not orthonormal: ||f_m - f_{m-k}|| / ||f_m|| from the iterates

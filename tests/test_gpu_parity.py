@@ -426,9 +426,10 @@ def test_graph_replay_bitwise(ctx, name, deg, kry):
     assert np.array_equal(out[True][0], out[False][0])
     assert np.array_equal(out[True][1], out[False][1])
     assert out[True][2].iterations == out[False][2].iterations
-    # (launch counts differ only by the look-ahead at the final checkpoint: the
-    # graph mode runs the next step's whole chain ahead, 2 deg - 1 more kernels)
-    assert out[True][2].kernel_launches - out[False][2].kernel_launches == 2 * deg - 1
+    assert out[True][2].mvms == out[False][2].mvms
+    # (launch counts differ by the work run ahead of the final checkpoint and
+    # discarded: the look-ahead SpMVs, or a whole step when the host's f(H_m)
+    # was the slower side -- a timing-dependent choice, so not compared)
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 7, 65, 257])
