@@ -84,9 +84,9 @@ def parse():
     p.add_argument("--no-profile", action="store_true",
                    help="time without the per-kernel CUDA events (no roofline breakdown)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
-                   help="N > 1: halo exchange and reductions over NCCL, or over peer memory "
-                        "(NVLink stores into the neighbours' windows, csrc/peer.cu)")
+    p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                   help="N > 1: halo exchange and reductions over peer memory (NVLink stores "
+                        "into the neighbours' windows, csrc/peer.cu; default) or over NCCL")
     p.add_argument("--test-fake-nccl", action="store_true",
                    help="TEST ONLY (tests/test_gpu_bench_dist.py): run the N>1 code path with every "
                         "rank on GPU 0, gloo for the bench's own collectives and the library "

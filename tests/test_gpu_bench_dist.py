@@ -41,15 +41,20 @@ def _bench(n, extra):
 
 
 @pytest.mark.parametrize("extra", [
-    ["--config", "C3s", "--deg", "10"],                               # real, Chebyshev, Lanczos
-    ["--config", "C5s", "--deg", "16"],                               # complex, sharded Ritz setup, CGS2
-    ["--config", "C7s", "--deg", "7", "--check-every", "4"],          # power-law graph slabs
-], ids=["c3s", "c5s", "c7s"])
+    # NCCL code path (the test stand-in for NCCL)
+    ["--config", "C3s", "--deg", "10", "--comm", "nccl"],             # real, Chebyshev, Lanczos
+    ["--config", "C5s", "--deg", "16", "--comm", "nccl"],             # complex, sharded Ritz setup, CGS2
+    ["--config", "C7s", "--deg", "7", "--check-every", "4", "--comm", "nccl"],  # power-law graph slabs
+    # peer memory (the default: CUDA IPC windows between the rank processes)
+    ["--config", "C4s", "--deg", "20"],
+    ["--config", "C5s", "--deg", "16"],
+], ids=["c3s_nccl", "c5s_nccl", "c7s_nccl", "c4s_peer", "c5s_peer"])
 def test_bench_two_ranks_matches_one(extra):
     one = _bench(1, extra)
     two = _bench(2, extra)
     assert two["n_gpus"] == 2 and "test_mode" in two
     assert two["config"]["parallelism"].startswith("row slabs x2")
+    assert ("NCCL" if "nccl" in extra else "peer-memory") in two["config"]["parallelism"]
     assert two["config"]["m"] == one["config"]["m"]
     assert two["config"]["mvms"] == one["config"]["mvms"]
     assert two["value"] > 0 and two["e2e"]["value"] > 0 and two["gpu_launches"] > 0

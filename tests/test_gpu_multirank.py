@@ -60,7 +60,7 @@ def _worker(rank, world, port, case, out_path, q_path, fake_lib):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    if fake_lib:
+    if fake_lib and fake_lib != "peer":
         from paper_2401_06684_b200 import _lib
         _lib.LIB_PATH = fake_lib
     import paper_2401_06684_b200 as pp
@@ -77,7 +77,8 @@ def _worker(rank, world, port, case, out_path, q_path, fake_lib):
     dist.all_gather_object(all_needs, needs)
     for p in range(world):
         plan.set_halo_send(p, all_needs[p][rank] - lo)
-    if fake_lib:
+    peer = fake_lib == "peer"
+    if fake_lib and not peer:
         idl = [pp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(idl, src=0)
         ctx = pp.Context(0, rank=rank, nranks=world, nccl_id=idl[0])
@@ -102,6 +103,10 @@ def _worker(rank, world, port, case, out_path, q_path, fake_lib):
     if not fake_lib:
         ctx.set_transport(exchange, allreduce)
     M = pp.Matrix(ctx, plan)
+    if peer:   # peer memory across processes: windows mapped with CUDA IPC
+        descs = [None] * world
+        dist.all_gather_object(descs, M.peer_window())
+        M.peer_connect(descs)
     bd = torch.from_numpy(np.ascontiguousarray(b[lo:hi])).cuda()
     if cfg.poly == "ritz":
         # the run uses the oracle's q (imported: values flow oracle -> library
@@ -174,14 +179,22 @@ def oracle_case(case):
     return cfg, A, b, iv, qo, res
 
 
-@pytest.mark.parametrize("transport", ["host", "nccl"])
+# peer memory between PROCESSES: windows mapped with CUDA IPC, each rank's
+# stream waiting on counters its neighbours' kernels bump from another context
+PEER_IPC_CASES = tuple(CASES)
+
+
+@pytest.mark.parametrize("transport", ["host", "nccl", "peer_ipc"])
 @pytest.mark.parametrize("case", list(CASES))
 def test_two_rank_run_matches_oracle(case, transport, request):
     import torch.multiprocessing as mp
     assert torch.cuda.is_available(), "GPU tests need a B200"
+    if transport == "peer_ipc" and case not in PEER_IPC_CASES:
+        pytest.skip("not a peer-memory case")
     cfg, A, b, iv, qo, res = oracle_case(case)
     world = WORLD.get(case, 2)
-    fake = request.getfixturevalue("fake_nccl_lib") if transport == "nccl" else ""
+    fake = {"nccl": lambda: request.getfixturevalue("fake_nccl_lib"), "host": lambda: "",
+            "peer_ipc": lambda: "peer"}[transport]()
     with tempfile.TemporaryDirectory() as td:
         out = os.path.join(td, "x.npy")
         q_path = os.path.join(td, "q.npy")
