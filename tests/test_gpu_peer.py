@@ -212,3 +212,33 @@ def test_peer_spmv_many_epochs(tmp_path):
     for k in range(1, ys.shape[0]):
         y = op.matvec(y)
         assert np.linalg.norm(ys[k] - y) <= 1e-13 * k * np.linalg.norm(y), k
+
+
+def test_peer_window_errors():
+    """ppf_mat_peer_window / _connect argument checking (include/ppf.h): a
+    single-rank matrix has no window; descriptors must come in rank order with
+    matching halo counts; connect needs a window and happens once; a matrix
+    disconnected again has no transport left (ppf_run: PPF_ESTATE)."""
+    import paper_2401_06684_b200 as pp
+    from paper_2401_06684_b200._lib import PPFError
+    name = "C3s"
+    cfg = configs.CONFIGS[name]
+    A, b, iv = configs.build(name)
+    ctx1 = pp.Context(0)
+    M1 = pp.Matrix(ctx1, pp.Plan.from_csr(A))
+    with pytest.raises(PPFError, match="EINVAL"):
+        M1.peer_window()
+    bounds, ranks = _make_ranks(A, b, cfg, 2)           # connected, same process
+    d0, d1 = ranks[0]["M"].peer_window(), ranks[1]["M"].peer_window()   # fresh windows
+    with pytest.raises(PPFError, match="EINVAL"):
+        ranks[0]["M"].peer_connect([d1, d0])               # not in rank order
+    with pytest.raises(PPFError, match="EINVAL"):
+        ranks[0]["M"].peer_connect([d0, d0])               # rank 1's slot holds rank 0's descriptor
+    ranks[0]["M"].peer_connect([d0, d1])
+    with pytest.raises(PPFError, match="EINVAL"):
+        ranks[0]["M"].peer_connect([d0, d1])               # already connected
+    ranks[0]["M"].peer_connect(None)                       # back to no transport
+    q = pp.Poly.chebyshev(*iv, 4)
+    with pytest.raises(PPFError, match="ESTATE"):
+        pp.run(ranks[0]["ctx"], ranks[0]["M"], q, ranks[0]["bd"], func=cfg.func, m_max=5,
+               stop="fixed")
