@@ -18,6 +18,9 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <deque>
+#include <future>
+#include <utility>
 
 #include "ppf_internal.h"
 
@@ -881,11 +884,100 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   // Run-ahead: when f(H_m) on the host takes longer than the host waits for
   // H_m (host-bound: small operators, large m, e.g. C2 deg 5 at m = 76), the
   // whole next step -- operator chain AND orthogonalisation, both device-only
-  // -- is enqueued before the host waits for H_m, so the device runs step m+1
-  // while the host evaluates f(H_m).  If the run stops at m, step m+1 is
-  // discarded (V_1..V_m, H_m and the counters are untouched by it).  Decided
-  // again at every checkpoint from the previous checkpoint's two times.
+  // -- is enqueued before the host waits for H_m, and f(H_m) itself goes to a
+  // worker thread (up to kPend checkpoints in flight, decided in order), so
+  // the device keeps stepping while the host evaluates.  If the run stops at
+  // m, the steps run beyond it are discarded (V_1..V_m, H_m and the counters
+  // are untouched by them).  Re-decided from the measured times.
   bool run_ahead = false, ortho_ahead = false;
+  // the decision at checkpoint mc (mbc: m after an early breakdown inside the
+  // stride): the estimate from y_{m-k}, the history, the stop test;
+  // true = stop, with term set
+  auto decide = [&](int mc, int mbc, double hsubc, long long mvmsc, const std::vector<zc>& yc) -> bool {
+    if (!y_prev.empty()) {
+      if (right && !twopass) {
+        // Y_m is not orthonormal: ||f_m - f_{m-k}|| / ||f_m|| from the iterates
+        // themselves (P:172-174): T0 = Y_m y_m, T1 = Y_m [y_{m-k}; 0]
+        std::vector<zc> yp(yc.size(), zc(0.0, 0.0));
+        for (size_t i = 0; i < y_prev.size(); ++i) yp[i] = y_prev[i];
+        R.upload_y(yc, R.L.ybuf, 0);
+        R.upload_y(yp, R.L.ybuf2, 1);
+        R.timed(2, double(vb) * (mbc + 1), [&] {
+          launch_combine(R.dt, n, basis0(), R.L.ldv, mbc, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
+        });
+        R.timed(2, double(vb) * (mbc + 1), [&] {
+          launch_combine(R.dt, n, basis0(), R.L.ldv, mbc, R.vec(R.L.ybuf2), R.vec(R.L.T1), R.st);
+        });
+        R.timed(2, 2.0 * vb, [&] {
+          launch_diffnorm(R.dt, n, R.vec(R.L.T1), R.vec(R.L.T0), R.scal(S_ERR), R.rs, R.grid_vec,
+                          R.st);
+        });
+        R.reduce_fin(FIN_SQRT, 2, R.scal(S_ERR), nullptr, nullptr, nullptr);
+        double e2[2];
+        PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
+        PPF_CUDA(cudaStreamSynchronize(R.st));
+        est = e2[0] / e2[1];
+      } else {
+        std::vector<zc> dlt = yc;
+        for (size_t i = 0; i < y_prev.size(); ++i) dlt[i] -= y_prev[i];
+        est = nrm(dlt) / nrm(yc);
+      }
+    }
+    y_prev = yc;
+    if (o->stop == PPF_STOP_TRUE_ERR) {
+      R.upload_y(yc);
+      R.timed(2, double(vb) * (mbc + 1), [&] {
+        launch_combine(R.dt, n, basis0(), R.L.ldv, mbc, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
+      });
+      R.timed(2, 2.0 * vb, [&] {
+        launch_diffnorm(R.dt, n, R.vec(R.L.T0), o->x_ref, R.scal(S_ERR), R.rs, R.grid_vec, R.st);
+      });
+      R.reduce_fin(FIN_SQRT, 2, R.scal(S_ERR), nullptr, nullptr, nullptr);
+      double e2[2];
+      PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
+      PPF_CUDA(cudaStreamSynchronize(R.st));
+      err = e2[0] / e2[1];
+    }
+    if (o->record_history) ctx->hist.push_back({mbc, est, err, mvmsc - (mc - mbc) * per_step});
+    if (mbc != mc || hsubc <= brt * beta0) {
+      term = PPF_BREAKDOWN;
+      return true;
+    }
+    if (o->stop == PPF_STOP_EST && !std::isnan(est) && est <= o->tol) {
+      term = PPF_CONVERGED;
+      return true;
+    }
+    if (o->stop == PPF_STOP_TRUE_ERR && err <= o->tol) {
+      term = PPF_CONVERGED;
+      return true;
+    }
+    return false;
+  };
+  // f(H_m) of checkpoints evaluated on worker threads (run-ahead mode), up to
+  // kPend in flight, decided strictly in checkpoint order
+  struct Pending {
+    int m = 0, mb = 0;
+    double hsub = 0.0;
+    long long mvms = 0;
+    std::future<std::pair<std::vector<zc>, double>> fut;
+  };
+  constexpr size_t kPend = 4;
+  std::deque<Pending> pend;
+  double t_wait = 0.0;
+  // decide the oldest pending checkpoint; true = the run stops there
+  auto resolve_front = [&]() -> bool {
+    Pending& p = pend.front();
+    auto r = p.fut.get();
+    t_dense += r.second;
+    run_ahead = A->nranks == 1 && r.second > t_wait;
+    const bool stop = decide(p.m, p.mb, p.hsub, p.mvms, r.first);
+    if (stop) {
+      m = p.mb;
+      y = std::move(r.first);
+    }
+    pend.pop_front();
+    return stop;
+  };
   std::vector<Runner::Call> calls = R.record_step(0);
   size_t played = 0;
   for (int j = 0; j < m_max; ++j) {
@@ -917,7 +1009,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     }
     const auto tw = std::chrono::steady_clock::now();
     R.fetch_H_wait(m + 1, m, Hh, beta0);
-    const double t_wait = std::chrono::duration<double>(std::chrono::steady_clock::now() - tw).count();
+    t_wait = std::chrono::duration<double>(std::chrono::steady_clock::now() - tw).count();
     const double hsub = std::abs(Hh[size_t(m) + size_t(m - 1) * (m + 1)]);
     // earlier breakdown inside the stride?
     int mb = m;
@@ -926,7 +1018,6 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
         mb = jj + 1;
         break;
       }
-    auto td = std::chrono::steady_clock::now();
     std::vector<zc> Hs = Hh;
     if (mb != m) {
       std::vector<zc> H2(size_t(mb + 1) * mb);
@@ -934,68 +1025,44 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
         for (int i = 0; i <= mb; ++i) H2[size_t(i) + size_t(jj) * (mb + 1)] = Hh[size_t(i) + size_t(jj) * (m + 1)];
       Hs = H2;
     }
+    // (1) earlier checkpoints left to worker threads are decided first, in
+    // order: those already finished, and the oldest while kPend are in flight
+    bool stopped = false;
+    while (!stopped && !pend.empty() &&
+           (pend.size() >= kPend ||
+            pend.front().fut.wait_for(std::chrono::seconds(0)) == std::future_status::ready))
+      stopped = resolve_front();
+    if (stopped) break;
+    // (2) this checkpoint on a worker thread while the device runs ahead,
+    // unless a breakdown or the last step forces the decision now; a stop
+    // found later discards the steps run meanwhile (<= kPend + 1)
+    if (run_ahead && more && mb == m && !(hsub <= brt * beta0) && o->stop == PPF_STOP_EST &&
+        !(right && !twopass)) {
+      Pending p;
+      p.m = m;
+      p.mb = mb;
+      p.hsub = hsub;
+      p.mvms = mvms;
+      p.fut = std::async(std::launch::async, [Hs, mb, beta0, lanczos]() {
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<zc> yy = dense_y(Hs, mb + 1, mb, beta0, lanczos);
+        return std::make_pair(std::move(yy), std::chrono::duration<double>(
+                                                 std::chrono::steady_clock::now() - t0).count());
+      });
+      pend.push_back(std::move(p));
+      continue;
+    }
+    while (!stopped && !pend.empty()) stopped = resolve_front();
+    if (stopped) break;
+    auto td = std::chrono::steady_clock::now();
     y = dense_y(Hs, mb + 1, mb, beta0, lanczos);
     const double t_this = std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
     t_dense += t_this;
     // one rank only: the decision comes from host timings, and the ranks'
     // collectives must pair up (every rank has to run the same steps)
     run_ahead = A->nranks == 1 && t_this > t_wait;
-    if (!y_prev.empty()) {
-      if (right && !twopass) {
-        // Y_m is not orthonormal: ||f_m - f_{m-k}|| / ||f_m|| from the iterates
-        // themselves (P:172-174): T0 = Y_m y_m, T1 = Y_m [y_{m-k}; 0]
-        std::vector<zc> yp(y.size(), zc(0.0, 0.0));
-        for (size_t i = 0; i < y_prev.size(); ++i) yp[i] = y_prev[i];
-        R.upload_y(y, R.L.ybuf, 0);
-        R.upload_y(yp, R.L.ybuf2, 1);
-        R.timed(2, double(vb) * (mb + 1), [&] {
-          launch_combine(R.dt, n, basis0(), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
-        });
-        R.timed(2, double(vb) * (mb + 1), [&] {
-          launch_combine(R.dt, n, basis0(), R.L.ldv, mb, R.vec(R.L.ybuf2), R.vec(R.L.T1), R.st);
-        });
-        R.timed(2, 2.0 * vb, [&] {
-          launch_diffnorm(R.dt, n, R.vec(R.L.T1), R.vec(R.L.T0), R.scal(S_ERR), R.rs, R.grid_vec,
-                          R.st);
-        });
-        R.reduce_fin(FIN_SQRT, 2, R.scal(S_ERR), nullptr, nullptr, nullptr);
-        double e2[2];
-        PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
-        PPF_CUDA(cudaStreamSynchronize(R.st));
-        est = e2[0] / e2[1];
-      } else {
-        std::vector<zc> dlt = y;
-        for (size_t i = 0; i < y_prev.size(); ++i) dlt[i] -= y_prev[i];
-        est = nrm(dlt) / nrm(y);
-      }
-    }
-    y_prev = y;
-    if (o->stop == PPF_STOP_TRUE_ERR) {
-      R.upload_y(y);
-      R.timed(2, double(vb) * (mb + 1), [&] {
-        launch_combine(R.dt, n, basis0(), R.L.ldv, mb, R.vec(R.L.ybuf), R.vec(R.L.T0), R.st);
-      });
-      R.timed(2, 2.0 * vb, [&] {
-        launch_diffnorm(R.dt, n, R.vec(R.L.T0), o->x_ref, R.scal(S_ERR), R.rs, R.grid_vec, R.st);
-      });
-      R.reduce_fin(FIN_SQRT, 2, R.scal(S_ERR), nullptr, nullptr, nullptr);
-      double e2[2];
-      PPF_CUDA(cudaMemcpyAsync(e2, R.scal(S_ERR), 16, cudaMemcpyDeviceToHost, R.st));
-      PPF_CUDA(cudaStreamSynchronize(R.st));
-      err = e2[0] / e2[1];
-    }
-    if (o->record_history) ctx->hist.push_back({mb, est, err, mvms - (m - mb) * per_step});
-    if (mb != m || hsub <= brt * beta0) {
+    if (decide(m, mb, hsub, mvms, y)) {
       m = mb;
-      term = PPF_BREAKDOWN;
-      break;
-    }
-    if (o->stop == PPF_STOP_EST && !std::isnan(est) && est <= o->tol) {
-      term = PPF_CONVERGED;
-      break;
-    }
-    if (o->stop == PPF_STOP_TRUE_ERR && err <= o->tol) {
-      term = PPF_CONVERGED;
       break;
     }
   }
