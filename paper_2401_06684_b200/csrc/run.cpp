@@ -962,6 +962,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     std::future<std::pair<std::vector<zc>, double>> fut;
   };
   constexpr size_t kPend = 4;
+  constexpr int kAhead = 5;
   std::deque<Pending> pend;
   double t_wait = 0.0;
   // decide the oldest pending checkpoint; true = the run stops there
@@ -986,6 +987,17 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     ortho_ahead = false;
     m = j + 1;
     mvms += per_step;
+    // checkpoints left to worker threads: decide those already finished, and
+    // wait for one once the device has been given kAhead steps beyond it (the
+    // steps run past a stop are discarded: this bounds them for any k)
+    {
+      bool stopped = false;
+      while (!stopped && !pend.empty() &&
+             (m - pend.front().m >= kAhead ||
+              pend.front().fut.wait_for(std::chrono::seconds(0)) == std::future_status::ready))
+        stopped = resolve_front();
+      if (stopped) break;
+    }
     const bool check = (o->stop != PPF_STOP_FIXED_M) && (m % k == 0 || m == m_max);
     const bool more = j + 1 < m_max;
     if (!check) {
