@@ -890,6 +890,12 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   // m, the steps run beyond it are discarded (V_1..V_m, H_m and the counters
   // are untouched by them).  Re-decided from the measured times.
   bool run_ahead = false, ortho_ahead = false;
+  // PPF_RUN_AHEAD=1 / 0 forces the mode on / off (tests: results must not
+  // depend on it); unset: chosen from the measured times
+  const int force_ahead = [] {
+    const char* e = std::getenv("PPF_RUN_AHEAD");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
   // the decision at checkpoint mc (mbc: m after an early breakdown inside the
   // stride): the estimate from y_{m-k}, the history, the stop test;
   // true = stop, with term set
@@ -970,7 +976,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     Pending& p = pend.front();
     auto r = p.fut.get();
     t_dense += r.second;
-    run_ahead = A->nranks == 1 && r.second > t_wait;
+    run_ahead = A->nranks == 1 && (force_ahead > 0 || (force_ahead < 0 && r.second > t_wait));
     const bool stop = decide(p.m, p.mb, p.hsub, p.mvms, r.first);
     if (stop) {
       m = p.mb;
@@ -1072,7 +1078,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     t_dense += t_this;
     // one rank only: the decision comes from host timings, and the ranks'
     // collectives must pair up (every rank has to run the same steps)
-    run_ahead = A->nranks == 1 && t_this > t_wait;
+    run_ahead = A->nranks == 1 && (force_ahead > 0 || (force_ahead < 0 && t_this > t_wait));
     if (decide(m, mb, hsub, mvms, y)) {
       m = mb;
       break;

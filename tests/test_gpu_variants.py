@@ -453,3 +453,36 @@ def test_real_pair_form_run(ctx, fmt):
                       stop="est", tol=cfg.tol)
     assert rep2.term == "converged" and abs(rep2.iterations - res_o.m) <= 1
     assert np.linalg.norm(host(x2) - res_o.x) <= 1e-7 * np.linalg.norm(res_o.x)
+
+
+@pytest.mark.parametrize("name,deg,kry,ck,extra", [
+    ("C2", 5, "cgs2", 1, {}),                          # m = 76, CGS2 tiles
+    ("C2", 10, "cgs2", 4, {}),                         # check stride 4: steps run past a checkpoint
+    ("C3s", 10, "lanczos", 1, {}),
+    ("C3s", 10, "lanczos2p", 2, {}),                   # two-pass: the ring of 3 basis vectors
+    ("C4s", 20, "cgs2", 1, {"func": "sqrt"}),
+])
+def test_run_ahead_is_invisible(ctx, name, deg, kry, ck, extra, monkeypatch):
+    """Running whole steps ahead while f(H_m) is evaluated on worker threads
+    (forced on with PPF_RUN_AHEAD=1, off with 0) changes neither m, the
+    mat-vec count, H nor x: checkpoints are decided in order and the steps run
+    past the stop are discarded."""
+    cfg = configs.CONFIGS[name]
+    A, b, iv = configs.build(name)
+    M = pp.Matrix(ctx, pp.Plan.from_csr(A))
+    q = pp.Poly.chebyshev(*iv, deg)
+    kw = dict(func=extra.get("func", cfg.func), krylov=kry, m_max=cfg.m_max, stop="est",
+              tol=cfg.tol, check_every=ck, record_history=True)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PPF_RUN_AHEAD", mode)
+        x, rep = pp.run(ctx, M, q, dev(b), **kw)
+        out[mode] = (host(x), pp.hessenberg(ctx, False)[0], rep, pp.api.history(ctx))
+    assert out["1"][2].iterations == out["0"][2].iterations
+    assert out["1"][2].mvms == out["0"][2].mvms
+    assert out["1"][2].term == out["0"][2].term
+    assert np.array_equal(out["1"][1], out["0"][1])
+    assert np.array_equal(out["1"][0], out["0"][0])
+    h1, h0 = out["1"][3], out["0"][3]                  # the same checkpoints and estimates
+    assert [(h["m"], h["mvms"]) for h in h1] == [(h["m"], h["mvms"]) for h in h0]
+    assert np.array_equal([h["est"] for h in h1], [h["est"] for h in h0], equal_nan=True)
