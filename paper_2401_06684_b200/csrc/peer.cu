@@ -43,8 +43,10 @@
 #include <cuda.h>
 #include <unistd.h>
 
+#include <chrono>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "ppf_internal.h"
 
@@ -153,7 +155,7 @@ void preload_module(const void* sym) {
 template <typename T>
 __global__ void __launch_bounds__(256) peer_push_kernel(
     const T* __restrict__ x, const int32_t* __restrict__ idx, const PushEnt* __restrict__ ent,
-    int nent, int64_t total, int slot, unsigned* const* __restrict__ sig, int nsig,
+    int nent, int64_t total, int slot, unsigned* const* __restrict__ sig, int nready, int nsig,
     unsigned* blk) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -168,7 +170,13 @@ __global__ void __launch_bounds__(256) peer_push_kernel(
     if (atomicAdd(blk, 1u) == gridDim.x - 1) {
       *blk = 0;  // the next push is stream-ordered after this one
       __threadfence_system();
-      for (int k = 0; k < nsig; ++k) atomicAdd_system(sig[k], 1u);
+      // "consumed" signals first, then (after a fence) the arrivals: a rank
+      // that has seen this push arrive has also received every signal of it,
+      // so once its run is over no write of ours is still headed for its
+      // window (it may free the window at teardown)
+      for (int k = nready; k < nsig; ++k) atomicAdd_system(sig[k], 1u);
+      __threadfence_system();
+      for (int k = 0; k < nready; ++k) atomicAdd_system(sig[k], 1u);
     }
   }
 }
@@ -226,7 +234,19 @@ struct PeerState {
 void peer_destroy(PeerState* p) {
   if (!p) return;
   cudaSetDevice(p->device);
-  cudaDeviceSynchronize();  // no push or reduction may still touch a window
+  cudaDeviceSynchronize();  // no push or reduction of ours may still touch a window
+  // A receiver's last push signals "consumed" into OUR window; wait (bounded)
+  // until every receiver's count has reached the number of exchanges before
+  // freeing the window under it (all ranks run the same exchanges).
+  if (p->connected && p->halo_epoch > 0) {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (unsigned* f : p->wait_freed) {
+      uint32_t v = 0;
+      while (cudaMemcpy(&v, f, 4, cudaMemcpyDeviceToHost) == cudaSuccess && v < p->halo_epoch &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::seconds(10))
+        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+  }
   for (size_t q = 0; q < p->peer.size(); ++q)
     if (p->ipc_opened[q]) cudaIpcCloseMemHandle(p->peer[q]);
   if (p->d_tab) cudaFree(p->d_tab);
@@ -266,11 +286,11 @@ void peer_halo_begin(ppf_ctx* ctx, ppf_mat* A, const void* x) {
   if (A->dtype == PPF_R64)
     peer_push_kernel<double><<<P->push_blocks, 256, 0, cs>>>(
         static_cast<const double*>(x), A->d_send_idx, P->d_ent, P->nent, A->send_total, slot,
-        P->d_push_sig, nsig, blk);
+        P->d_push_sig, P->n_to, nsig, blk);
   else
     peer_push_kernel<double2><<<P->push_blocks, 256, 0, cs>>>(
         static_cast<const double2*>(x), A->d_send_idx, P->d_ent, P->nent, A->send_total, slot,
-        P->d_push_sig, nsig, blk);
+        P->d_push_sig, P->n_to, nsig, blk);
   check_launch("peer_push_kernel");
   PPF_CUDA(cudaEventRecord(ctx->ev_halo, cs));
 }
