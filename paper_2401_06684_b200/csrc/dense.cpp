@@ -270,11 +270,18 @@ void general_invsqrt_e1(int m, const std::vector<zc>& H0, double beta0, std::vec
     if (on_branch_cut(t(i, i))) fail(PPF_EBRANCH, "eigenvalue of H_m on (-inf, 0]");
     r(i, i) = std::sqrt(t(i, i));  // principal branch
   }
+  // R's rows are also kept row-major (Rt): the inner sum walks row i of R and
+  // column j of R, both contiguous then (same terms, same order)
+  std::vector<zc> Rt(size_t(m) * m, zc(0.0, 0.0));
+  for (int i = 0; i < m; ++i) Rt[size_t(i) * m + i] = r(i, i);
   for (int j = 1; j < m; ++j) {
+    const zc* rj = &r(0, j);
     for (int i = j - 1; i >= 0; --i) {
+      const zc* ri = &Rt[size_t(i) * m];
       zc s = t(i, j);
-      for (int k = i + 1; k < j; ++k) s -= r(i, k) * r(k, j);
+      for (int k = i + 1; k < j; ++k) s -= ri[k] * rj[k];
       r(i, j) = s / (r(i, i) + r(j, j));
+      Rt[size_t(i) * m + j] = r(i, j);
     }
   }
   // u = R^{-1} Q^H e1.  Q = G_1 G_2 ... G_K with G_t acting on columns
@@ -289,7 +296,8 @@ void general_invsqrt_e1(int m, const std::vector<zc>& H0, double beta0, std::vec
   }
   for (int i = m - 1; i >= 0; --i) {
     zc s = u[i];
-    for (int k = i + 1; k < m; ++k) s -= r(i, k) * u[k];
+    const zc* ri = &Rt[size_t(i) * m];
+    for (int k = i + 1; k < m; ++k) s -= ri[k] * u[k];
     u[i] = s / r(i, i);
   }
   for (size_t t = log.size(); t-- > 0;) {
