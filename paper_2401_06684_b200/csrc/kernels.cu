@@ -254,6 +254,17 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
       for (int k = k0; k < k1; ++k) prefetch_l2(col + base + 64 * k + 2 * lane);
   }
   pdl_wait();
+  // the slice's rows of the epilogue vectors and of x (its own rows: the
+  // diagonal and the +-1 neighbours): one 128-B line per 8 lanes
+  if (live && part == 0 && (lane & 7) == 0) {
+    const int64_t r0 = slice * 64 + 2 * lane;
+    if (r0 < n) {
+      prefetch_l2(x + r0);
+      if (e.z) prefetch_l2(e.z + r0);
+      if (e.u) prefetch_l2(e.u + r0);
+      if (has_x && e.xe != x) prefetch_l2(e.xe + r0);
+    }
+  }
   if (live) {
     const int2* cp = reinterpret_cast<const int2*>(col + base) + lane;
     const double2* vp = reinterpret_cast<const double2*>(val + base) + lane;
