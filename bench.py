@@ -295,7 +295,12 @@ def main():
         b = b.astype(np.complex128)
     cplx_run = cfg.complex_ or args.poly == "contour-ritz"
     if args.fmt is None:
-        args.fmt = "sell32" if (cplx_run or cfg.family == "graph") else "sell64"
+        # fp64 two-rows-per-lane C = 64 slices stream best once there are enough of
+        # them to fill the GPU (C3/C4); below one warp per SM slot (C1, C2: 1024
+        # slices of 64 rows < 148 SMs x 8 warps) C = 32 doubles the warps
+        # (C2 deg 20: 4.89 -> 4.04 ms)
+        few = A.n < 64 * 8 * 148
+        args.fmt = "sell32" if (cplx_run or cfg.family == "graph" or few) else "sell64"
     fmt = {"sell32": ("sell", 32), "sell64": ("sell", 64), "csr": ("csr", 32)}[args.fmt]
     if cplx_run and fmt == ("sell", 64):
         fmt = ("sell", 32)
