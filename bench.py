@@ -325,9 +325,12 @@ def main():
         dist.all_gather_object(all_needs, needs)
         for p in range(world):
             plan.set_halo_send(p, all_needs[p][rank] - lo)
-        idl = [pp.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idl, src=0)
-        ctx = pp.Context(local, rank=rank, nranks=world, nccl_id=idl[0], stream=stream)
+        if args.comm == "nccl":
+            idl = [pp.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idl, src=0)
+            ctx = pp.Context(local, rank=rank, nranks=world, nccl_id=idl[0], stream=stream)
+        else:  # peer memory needs no communicator (the windows are connected below)
+            ctx = pp.Context(local, rank=rank, nranks=world, stream=stream)
         b = b[lo:hi].copy()
     else:
         bounds = [0, A.n]
