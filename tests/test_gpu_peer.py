@@ -101,12 +101,12 @@ def _run_threads(fn, ranks, timeout=240):
             raise e
 
 
-def child_run(case, q_path, out_path):
+def child_run(case, q_path, out_path, world=None):
     """Child process: the case on `world` emulated ranks with peer memory."""
     import paper_2401_06684_b200 as pp
     name, deg, kw = CASES[case]
     cfg = configs.CONFIGS[name]
-    world = WORLD.get(case, 2)
+    world = world or WORLD.get(case, 2)
     A, b, iv = configs.build(name)
     _, ranks = _make_ranks(A, b, cfg, world)
     power = 2 if cfg.func == "sign" else 1
@@ -175,14 +175,21 @@ def _child(call):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("case", list(CASES))
-def test_peer_ranks_match_oracle(case, tmp_path):
+# (case, ranks): every sharded case at its usual rank count, plus the 8-rank
+# layout of an 8-GPU node (C3s: 30 planes -> slabs of 3-4 planes; C5s: a ring of
+# 4 time slices -> 4 ranks, each with two neighbours)
+PEER_RUNS = [(c, WORLD.get(c, 2)) for c in CASES] + [("c3s_lanczos", 8), ("c4s_cgs2_sqrt", 8),
+                                                      ("c5s_ritz", 4)]
+
+
+@pytest.mark.parametrize("case,world", PEER_RUNS)
+def test_peer_ranks_match_oracle(case, world, tmp_path):
     assert torch.cuda.is_available(), "GPU tests need a B200"
     cfg, A, b, iv, qo, res = oracle_case(case)
     q_path, out = str(tmp_path / "q.npy"), str(tmp_path / "out.npz")
     if cfg.poly == "ritz":
         np.save(q_path, np.stack([qo.nodes, qo.dd]))
-    _child(f"child_run({case!r}, {q_path!r}, {out!r})")
+    _child(f"child_run({case!r}, {q_path!r}, {out!r}, {world})")
     o = np.load(out)
     assert all(int(m) == res.m for m in o["m"])               # every rank, the oracle's m
     assert all(np.array_equal(H, o["H"][0]) for H in o["H"])  # rank-order sums: identical H
@@ -192,7 +199,7 @@ def test_peer_ranks_match_oracle(case, tmp_path):
     err = np.linalg.norm(o["x"] - res.x) / np.linalg.norm(res.x)
     if err > X_TOL:   # which slabs are off (diagnostic)
         name = CASES[case][0]
-        bounds = _slab_bounds(configs.CONFIGS[name], len(res.x), WORLD.get(case, 2))
+        bounds = _slab_bounds(configs.CONFIGS[name], len(res.x), world)
         per = [float(np.linalg.norm((o["x"] - res.x)[lo:hi]) / np.linalg.norm(res.x[lo:hi]))
                for lo, hi in zip(bounds[:-1], bounds[1:])]
         pytest.fail(f"x rel. error {err:.3g}; per slab {per}")
