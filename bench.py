@@ -84,6 +84,8 @@ def parse():
     p.add_argument("--no-profile", action="store_true",
                    help="time without the per-kernel CUDA events (no roofline breakdown)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-graphs", action="store_true",
+                   help="launch the step's q(A)q(A) chain directly instead of replaying a CUDA graph")
     p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
                    help="N > 1: halo exchange and reductions over peer memory (NVLink stores "
                         "into the neighbours' windows, csrc/peer.cu; default) or over NCCL")
@@ -337,6 +339,8 @@ def main():
         plan = pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1], sigma=sigma)
         ctx = pp.Context(local, stream=stream)
     info = plan.info()
+    if args.no_graphs:
+        ctx.set_graphs(False)
     M = pp.Matrix(ctx, plan)
     if world > 1 and args.comm == "peer":
         descs = [None] * world
