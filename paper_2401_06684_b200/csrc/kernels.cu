@@ -155,9 +155,10 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
   // get a whole block each, 8 warps splitting their entry columns; the rest
   // KS warps per slice
   const bool heavy = blockIdx.x < nheavy;
+  const int nw = blockDim.x >> 5;
   const int64_t slice = heavy ? int64_t(blockIdx.x)
-                              : nheavy + (int64_t(blockIdx.x) - nheavy) * (8 / KS) + warp / KS;
-  const int parts = heavy ? 8 : KS;
+                              : nheavy + (int64_t(blockIdx.x) - nheavy) * (nw / KS) + warp / KS;
+  const int parts = heavy ? nw : KS;
   const int part = heavy ? warp : warp % KS;
   const bool live = slice < nslices;
   T acc = s_zero<T>();
@@ -201,8 +202,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
     red[warp][lane] = acc;
     __syncthreads();
     if (warp != 0) return;
-#pragma unroll
-    for (int p = 1; p < 8; ++p) acc = s_add(acc, red[p][lane]);
+    for (int p = 1; p < nw; ++p) acc = s_add(acc, red[p][lane]);
   } else if constexpr (KS > 1) {
     red[warp][lane] = acc;
     __syncthreads();
@@ -969,8 +969,15 @@ template <typename T, bool ACC>
 static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT<T>& et,
                         bool has_x, cudaStream_t st) {
   const int KS = A->sell_ks;
-  const int64_t spb = 8 / KS;  // slices per 256-thread block
   const int64_t nh = A->C == 32 ? A->sell_heavy : 0;  // one block per heavy slice (sell1 only)
+  static const int s1t = [] {
+    const char* e = std::getenv("PPF_SELL1_BLOCK");
+    return e ? std::atoi(e) : 128;
+  }();
+  // threads of a sell1 block: 4 warps (the last blocks drain sooner), 8 when
+  // KS = 8 or when heavy slices want 8 warps each (C7: 4 warps cost 8%)
+  const int t1 = (KS > s1t / 32 || nh > 0) ? 256 : s1t;
+  const int64_t spb = (t1 / 32) / KS;  // slices per block
   const int blocks = int(nh + (A->nslices - nh + spb - 1) / spb);
   if (blocks == 0) return;
 #define PPF_KS(launch) \
@@ -998,10 +1005,10 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
     }
   }
 #define PPF_S1P(K)                                                                                  \
-  sell1_kernel<T, K, true, ACC><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+  sell1_kernel<T, K, true, ACC><<<blocks, t1, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
                                                         val, xt, ot, et, has_x, A->d_perm, nh)
 #define PPF_S1(K)                                                                                    \
-  sell1_kernel<T, K, false, ACC><<<blocks, 256, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
+  sell1_kernel<T, K, false, ACC><<<blocks, t1, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
                                                          val, xt, ot, et, has_x, nullptr, nh)
   if (A->d_perm) {
     PPF_KS(PPF_S1P)
