@@ -1168,6 +1168,13 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
       if (nd == 2) ctx->lastH[oo + 1] = v.imag();
     }
   ctx->launches += R.launches;
+  if (ctx->nccl_comm && A->nranks > 1) {
+    // NCCL reports communication failures asynchronously (SURVEY §8(b) errors)
+    ncclResult_t as = ncclSuccess;
+    if (ncclCommGetAsyncError(static_cast<ncclComm_t>(ctx->nccl_comm), &as) != ncclSuccess ||
+        as != ncclSuccess)
+      fail(PPF_ENCCL, "NCCL communicator reported an asynchronous error");
+  }
   rep->iterations = m;
   rep->term = term;
   rep->mvms = mv_total;
