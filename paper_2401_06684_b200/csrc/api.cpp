@@ -36,7 +36,7 @@ int auto_sell_ks(const ppf_mat* m, int num_sms) {
   return ks;
 }
 
-// Leading slices whose width is >= 4x the mean (and >= 32 entries per lane):
+// Leading slices whose width is >= 2x the mean (and >= 16 entries per lane):
 // after a whole-matrix sigma sort (descending row length) these are the
 // power-law rows.  One warp per such slice would be the critical path of the
 // whole launch (C7: the 239-entry slices, 38.9 us/launch at KS = 1, 20.0 at a
@@ -46,7 +46,8 @@ int64_t sell_heavy_prefix(const std::vector<int64_t>& ptr, int C) {
   const int64_t ns = int64_t(ptr.size()) - 1;
   if (ns <= 0) return 0;
   const double mean = double(ptr[ns]) / (double(ns) * C);
-  const double thr = std::max(32.0, 4.0 * mean);
+  // (C7: 2x/16 -> 17.1 us per SpMV, 4x/32 -> 18.8, 1.5x/12 -> 18.9)
+  const double thr = std::max(16.0, 2.0 * mean);
   int64_t h = 0;
   while (h < ns && double(ptr[h + 1] - ptr[h]) / C >= thr) ++h;
   return h == ns ? 0 : h;
