@@ -294,3 +294,39 @@ def test_fake_nccl_test_library_links():
     for s in ("ncclCommInitRank", "ncclSend", "ncclRecv", "ncclAllReduce", "ncclGroupEnd",
               "ppf_run"):
         assert f" {s}\n" in syms
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/ppf.h is a C header (no C++ in the signatures): a C99 program
+    includes it, links against libppf.so and calls the host-only entry points
+    (ABI version, status strings, the Chebyshev polynomial of P:323-335)."""
+    import subprocess
+    from paper_2401_06684_b200 import _lib
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "abi.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include "ppf.h"
+int main(void) {
+  ppf_poly* q = NULL;
+  double ab[2];
+  int kind = -1, deg = -1;
+  if (ppf_abi_version() != PPF_ABI_VERSION) return 1;
+  if (ppf_poly_chebyshev(0.5, 8.0, 6, &q) != PPF_OK) return 2;
+  if (ppf_poly_export(q, &kind, &deg, ab, NULL, NULL) != PPF_OK) return 3;
+  ppf_poly_destroy(q);
+  if (kind != PPF_POLY_CHEBYSHEV || deg != 6 || ab[0] != 0.5 || ab[1] != 8.0) return 4;
+  if (ppf_poly_chebyshev(-1.0, 8.0, 6, &q) != PPF_EINVAL) return 5;
+  printf("%s|%s\n", ppf_status_string(PPF_EINVAL), ppf_last_error());
+  return 0;
+}
+""")
+    exe = tmp_path / "abi"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                        str(src), "-o", str(exe), "-L", libdir, "-l:libppf.so",
+                        f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert "EINVAL" in r.stdout.upper() or "INVAL" in r.stdout.upper()
