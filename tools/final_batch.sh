@@ -1,6 +1,5 @@
 set -x
 mkdir -p gpurun_out/final
-mkdir -p gpurun_out/final
 B="python bench.py --steps 5 --warmup 3"
 $B --config C1 --steps 20 --warmup 5 > gpurun_out/final/r01_bench_c1.json 2>/dev/null
 for d in 5 10 20; do $B --config C2 --deg $d --no-cpu-baseline > gpurun_out/final/r01_bench_c2_deg$d.json 2>/dev/null; done
