@@ -970,13 +970,9 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
                         bool has_x, cudaStream_t st) {
   const int KS = A->sell_ks;
   const int64_t nh = A->C == 32 ? A->sell_heavy : 0;  // one block per heavy slice (sell1 only)
-  static const int s1t = [] {
-    const char* e = std::getenv("PPF_SELL1_BLOCK");
-    return e ? std::atoi(e) : 128;
-  }();
   // threads of a sell1 block: 4 warps (the last blocks drain sooner), 8 when
   // KS = 8 or when heavy slices want 8 warps each (C7: 4 warps cost 8%)
-  const int t1 = (KS > s1t / 32 || nh > 0) ? 256 : s1t;
+  const int t1 = (KS > 4 || nh > 0) ? 256 : 128;
   const int64_t spb = (t1 / 32) / KS;  // slices per block
   const int blocks = int(nh + (A->nslices - nh + spb - 1) / spb);
   if (blocks == 0) return;
