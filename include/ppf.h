@@ -214,7 +214,8 @@ ppf_status ppf_spmv_local(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y);
  *   the library -- an IPC export needs an allocation base -- freed with A:
  *   counters, 2 x nranks reduction slots, 2 receive slots of halo_total
  *   entries) and writes a PPF_PEER_DESC_BYTES descriptor to host `desc`
- *   (CUDA IPC handle, process id, receive offsets and counts per peer).
+ *   (CUDA IPC handle, process id + a random per-process nonce, receive
+ *   offsets and counts per peer).
  *   The matrix must be sharded (nranks > 1, 1 < nranks <= PPF_PEER_MAX_RANKS)
  *   with its send lists set.  The caller all-gathers the descriptors.
  * ppf_mat_peer_connect: `descs` = nranks descriptors in rank order (host).

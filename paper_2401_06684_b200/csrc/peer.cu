@@ -45,6 +45,7 @@
 
 #include <chrono>
 #include <cstring>
+#include <random>
 #include <string>
 #include <thread>
 
@@ -65,7 +66,7 @@ struct PeerDesc {
   uint32_t magic, version;
   int32_t rank, nranks;
   int64_t pid;
-  int64_t hostid;
+  int64_t nonce;  // random per process: "same process" needs pid AND nonce to match
   uint64_t win;  // device address in the owner's process
   int64_t halo_total;
   int32_t sc, device;
@@ -85,6 +86,16 @@ struct PushEnt {      // one receiver of this rank's boundary entries
 size_t halo_off(int nranks) {
   const size_t red = OFF_RED + size_t(2) * nranks * RCAP * 8;
   return (red + 255) / 256 * 256;
+}
+
+// identifies this process among the ranks (pid alone may repeat across hosts
+// or containers)
+int64_t process_nonce() {
+  static const int64_t v = [] {
+    std::random_device rd;
+    return (int64_t(rd()) << 32) ^ int64_t(rd()) ^ int64_t(getpid());
+  }();
+  return v;
 }
 
 using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -369,7 +380,7 @@ ppf_status ppf_mat_peer_window(ppf_mat* A, void* desc) {
   d.rank = A->rank;
   d.nranks = A->nranks;
   d.pid = int64_t(getpid());
-  d.hostid = int64_t(gethostid());
+  d.nonce = process_nonce();
   d.win = reinterpret_cast<uint64_t>(P->win);
   d.halo_total = A->halo_total;
   d.sc = int32_t(sc);
@@ -412,11 +423,11 @@ ppf_status ppf_mat_peer_connect(ppf_mat* A, const void* descs) {
   PPF_REQUIRE(D[me].win == reinterpret_cast<uint64_t>(P->win), "own descriptor is stale");
   P->peer.assign(R, nullptr);
   P->ipc_opened.assign(R, false);
-  const int64_t mypid = int64_t(getpid()), myhost = int64_t(gethostid());
+  const int64_t mypid = int64_t(getpid()), mynonce = process_nonce();
   for (int q = 0; q < R; ++q) {
     if (q == me) {
       P->peer[q] = P->win;
-    } else if (D[q].pid == mypid && D[q].hostid == myhost) {
+    } else if (D[q].pid == mypid && D[q].nonce == mynonce) {
       P->peer[q] = reinterpret_cast<char*>(D[q].win);  // a rank of this process
     } else {
       void* p = nullptr;
