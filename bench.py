@@ -177,6 +177,20 @@ def slab_bounds(cfg, n, world):
     return [c * per for c in cuts]
 
 
+def default_layout(cfg, n, cplx):
+    """The launch configuration bench.py times (also used by the full-size
+    parity tests): (format name, SELL sigma).  fp64 two-rows-per-lane C = 64
+    slices stream best once there are enough of them to fill the GPU (C3/C4);
+    below one warp per SM slot (C1, C2: 1024 slices of 64 rows < 148 SMs x 8
+    warps) C = 32 doubles the warps (C2 deg 20: 4.89 -> 4.04 ms); complex
+    operators use C = 32.  Power-law row lengths (the graph) are sorted
+    globally by length (0.14% padding for C7 instead of 7x with sigma = 1)."""
+    few = n < 64 * 8 * 148
+    fmt = "sell32" if (cplx or cfg.family == "graph" or few) else "sell64"
+    sigma = 32 * ((n + 31) // 32) if cfg.family == "graph" else 1
+    return fmt, sigma
+
+
 def setup_inputs(name):
     from inputs import configs
     cfg = configs.CONFIGS[name]
@@ -184,71 +198,163 @@ def setup_inputs(name):
     return cfg, A, b, iv
 
 
-def cpu_baseline(cfg, A, b, iv, deg, m, mvms_total):
-    """The oracle as it stands (oracle/), timed on the host cores on a bounded
-    sample: q construction + s = Ab + c = q(A)s + ONE preconditioned Krylov step
-    (krylov.run with m_max=1), extrapolated to the GPU run's mvm count."""
+def workload_config(args, cfg, name, deg, n, nnz, m, mvms, world, cplx_run, krylov_m, newton_eval):
+    """The `config` object of the JSON line: what defines the workload and its
+    outcome (m, mat-vec count), identical for the GPU arm and the oracle arm
+    (--impl reference) so the two lines describe the same job."""
+    mat_gb = nnz * ((16 if cplx_run else 8) + 4) / 1e9 / world
+    return {
+        "workload": WORKLOAD.get(name, name), "deg": None if args.plain else deg,
+        "precond": "none (plain, d = 1)" if args.plain else args.precond,
+        "poly": {"contour": "contour-LS circle |z-(4+m0)|=2.2, N=128",
+                 "contour-ritz": "contour-LS on the polygon of 60 Ritz values, r_min 0.1, "
+                                 "~2000 points (complex arithmetic)"}.get(args.poly, cfg.poly),
+        "newton_eval": newton_eval if cfg.poly == "ritz" else None,
+        "krylov": krylov_m, "check_every": args.check_every, "tol": cfg.tol,
+        "m": m, "mvms": mvms, "n": n, "nnz": nnz,
+        "stop": f"estimate <= {cfg.tol:g}, k = {args.check_every} (P:424)",
+        "l2": (f"inputs larger than L2 (matrix {mat_gb:.2f} GB per rank / 126 MB L2), no flush"
+               if mat_gb > 0.126 else
+               f"matrix {mat_gb * 1e3:.0f} MB per rank fits the 126 MB L2; no flush "
+               "(the method re-reads it every SpMV: L2-resident is its real regime)"),
+        "parallelism": (f"row slabs x{world} (" + ("NCCL halo + allreduce" if args.comm == "nccl"
+                        else "peer-memory halo push + rank-order reductions") + ")")
+                       if world > 1 else "single GPU",
+    }
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+def oracle_supported(args) -> bool:
+    """The oracle arm exists for the configs' own method (left preconditioning,
+    the config's polynomial and Krylov method)."""
+    return (args.poly == "config" and not args.plain and args.precond == "left"
+            and args.krylov is None and args.newton_eval is None and not args.harmonic)
+
+
+def oracle_run(args, cfg, A, b, iv, deg):
+    """ONE full oracle run of the workload, as it stands (oracle/, never tuned
+    for this), timed on the host cores: q construction (Chebyshev coefficients,
+    or the Ritz setup's deg+1 Arnoldi steps), s = A b and c = q(A)s,
+    the preconditioned Krylov steps until the paper's estimate <= tol checked
+    every k steps with f(H_m) at each checkpoint, and
+    x = V_m y_m -- the same stopping rule and m as the GPU arm.  Matrix
+    generation and upload are outside, as on the GPU side.  Returns
+    (seconds, m, mvms excluding the Ritz setup, threads)."""
     from oracle import chebyshev, krylov, newton
-    from oracle.spmv import Operator
+    from oracle.spmv import Operator, SquaredOperator
     op = Operator(A.to_scipy())
-    t0 = time.perf_counter()
     sq = cfg.func in ("sign", "invsqrt_sq")
+    kw = dict(krylov=cfg.krylov, m_max=args.m_max or cfg.m_max, stop="est", tol=cfg.tol,
+              check_every=args.check_every)
+    t0 = time.perf_counter()
     if cfg.poly == "chebyshev":
         q = chebyshev.coefficients(*iv, deg)
-        setup_mvms = 0
     else:
-        from oracle.spmv import SquaredOperator
         start = op.matvec(b) if cfg.params.get("ritz_start") == "Ab" else b
-        q, setup_mvms, _ = newton.ritz_newton(SquaredOperator(op) if sq else op, start, deg)
+        q, _, _ = newton.ritz_newton(SquaredOperator(op) if sq else op, start, deg)
+    mv0 = op.mvms
     if sq:
-        res = krylov.run_sign(op, b, q, krylov=cfg.krylov, m_max=1, stop="fixed")
+        res = krylov.run_sign(op, b, q, **kw)
     else:
-        res = krylov.run(op, b, q, func=cfg.func, krylov=cfg.krylov, m_max=1, stop="fixed")
-    t1 = time.perf_counter() - t0
-    mv1 = res.mvms + setup_mvms
-    per_mvm = t1 / mv1
-    est = per_mvm * mvms_total
+        res = krylov.run(op, b, q, func=cfg.func, **kw)
+    x = res.x  # the iterate is formed inside run (line 11)
+    del x
+    t = time.perf_counter() - t0
+    return t, res.m, op.mvms - mv0, op.threads
+
+
+def cpu_baseline(args, cfg, A, b, iv, deg, m_gpu, mvms_gpu):
+    """cpu_baseline of the GPU arm: one full oracle run (oracle_run) on the
+    host cores at N = 1, same workload and stopping rule."""
+    t, m, mvms, threads = oracle_run(args, cfg, A, b, iv, deg)
     return {
-        "value": est, "unit": "s", "cores": op.threads, "kind": "oracle",
-        "sample": (f"oracle q construction + start + 1 Krylov step ({mv1} SpMVs) timed "
-                   f"({t1:.2f} s, {per_mvm * 1e3:.1f} ms/SpMV incl. its share of the step), "
-                   f"extrapolated by mvm count to the GPU run's {mvms_total} SpMVs (m={m}); "
-                   f"the growth of CGS2 cost with j is not extrapolated"),
+        "value": t, "unit": "s", "cores": threads, "kind": "oracle",
+        "sample": (f"one full oracle run of this workload (q construction, start, {m} preconditioned "
+                   f"steps with f(H_m) at every checkpoint, x = V_m y_m; {mvms} mat-vecs) on "
+                   f"{threads} threads of {cpu_model()}; timed end to end"),
+        "m": m, "mvms": mvms, "same_m_as_gpu": m == m_gpu and mvms == mvms_gpu,
     }
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on the same workload/metric (bounded sample)."""
+    """--impl reference: the CPU oracle (the tier's reference arm) on the same
+    workload, metric and config as the GPU arm, each step ONE full oracle run
+    (oracle_run).  A full run takes minutes at the BASELINE sizes (C4: ~3-4
+    min), so the arm runs as many steps as fit in PPF_REF_BUDGET_S seconds
+    (default 600; at least one), with no warm-up (host code has nothing to
+    warm), and reports the steps it ran.  Under torchrun only rank 0 works."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     name = args.config
     cfg, A, b, iv = setup_inputs(name)
     deg = args.deg if args.deg is not None else cfg.degs[0]
-    m_assumed = {"C4": 25, "C3": 27, "C5": 3, "C2": 76, "C1": 20, "C6": 10}.get(name, 20)
-    pw = 2 if cfg.func in ("sign", "invsqrt_sq") else 1     # Q^2 = two mvms (P:462)
-    mvms_total = pw * deg + (1 if cfg.func in ("sqrt", "sign") else 0) + m_assumed * pw * (2 * deg + 1)
-    if cfg.poly == "ritz":
-        mvms_total += pw * (deg + 1)
-    vals = []
-    base = None
-    for i in range(args.warmup + args.steps):
-        base = cpu_baseline(cfg, A, b, iv, deg, m_assumed, mvms_total)
-        if i >= args.warmup:
-            vals.append(base["value"])
-    v = statistics.median(vals)
-    base["value"] = v
+    if not oracle_supported(args):
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the oracle arm covers the configs' own method only (no variant flags)"}))
+        return
+    budget = float(os.environ.get("PPF_REF_BUDGET_S", "600"))
+    times, t_all = [], time.perf_counter()
+    m = mvms = threads = None
+    while len(times) < args.steps:
+        t, m, mvms, threads = oracle_run(args, cfg, A, b, iv, deg)
+        times.append(t)
+        spent = time.perf_counter() - t_all
+        if spent + statistics.mean(times) > budget:
+            break
+    v = statistics.median(times)
+    cplx = cfg.complex_
+    krylov_m = cfg.krylov
+    newton_eval = "basis" if cfg.family == "graph" else "horner"
     line = {
         "metric": "f(A)b time-to-1e-8 rel. error (s) & Krylov-step HBM GB/s vs B200 peak",
-        "impl": "reference", "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64" if not cfg.complex_ else "c128",
-        "data": "synthetic (seeded generators in inputs/)",
-        "config": {"workload": WORKLOAD.get(name, name), "deg": deg, "m_assumed": m_assumed},
-        "cpu_baseline": base,
+        "impl": "reference", "value": v, "unit": "s", "n_gpus": world, "steps": len(times),
+        "warmup": 0, "ms_per_step": v * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128" if cplx else "f64",
+        "data": "synthetic (seeded generators in inputs/; no dataset)",
+        "config": workload_config(args, cfg, name, deg, A.n, A.nnz, m, mvms, world, cplx, krylov_m,
+                                  newton_eval),
+        "steps_note": (f"{len(times)} of the requested {args.steps} steps (and none of the {args.warmup} "
+                       f"warm-up steps): each step is one full oracle run ({times[0]:.0f} s), and the "
+                       f"arm stops once the next would pass its {budget:.0f} s budget"),
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "oracle",
+                         "sample": (f"median of {len(times)} full oracle runs (q construction, start, {m} "
+                                    f"preconditioned steps with f(H_m) at every checkpoint, x = V_m y_m; "
+                                    f"{mvms} mat-vecs) on {threads} threads of {cpu_model()}; "
+                                    f"timed end to end"),
+                         "runs_s": times},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 without a torchrun environment: re-exec this command under
+    torch.distributed.run with N ranks on this node (the driver's own launch
+    line); never fall back to one rank silently."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible")
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -256,10 +362,16 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args)
     import torch
     import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if world > 1 and not args.test_fake_nccl and torch.cuda.device_count() < world:
+        sys.exit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} CUDA device(s)")
     rank = int(os.environ.get("RANK", "0"))
     local = 0 if args.test_fake_nccl else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -296,21 +408,15 @@ def main():
         A = CSR(A.n, A.row_ptr, A.col, A.val.astype(np.complex128))
         b = b.astype(np.complex128)
     cplx_run = cfg.complex_ or args.poly == "contour-ritz"
+    dfmt, dsigma = default_layout(cfg, A.n, cplx_run)
     if args.fmt is None:
-        # fp64 two-rows-per-lane C = 64 slices stream best once there are enough of
-        # them to fill the GPU (C3/C4); below one warp per SM slot (C1, C2: 1024
-        # slices of 64 rows < 148 SMs x 8 warps) C = 32 doubles the warps
-        # (C2 deg 20: 4.89 -> 4.04 ms)
-        few = A.n < 64 * 8 * 148
-        args.fmt = "sell32" if (cplx_run or cfg.family == "graph" or few) else "sell64"
+        args.fmt = dfmt
     fmt = {"sell32": ("sell", 32), "sell64": ("sell", 64), "csr": ("csr", 32)}[args.fmt]
     if cplx_run and fmt == ("sell", 64):
         fmt = ("sell", 32)
     sigma = args.sigma
     if sigma == 0:
-        # power-law row lengths: sort rows globally by length (0.14% padding
-        # for C7 instead of 7x with sigma = 1)
-        sigma = 32 * ((A.n + 31) // 32) if (cfg.family == "graph" and fmt == ("sell", 32)) else 1
+        sigma = dsigma if fmt == ("sell", 32) else 1
     stream = torch.cuda.Stream()
     if world > 1:
         # row-slab sharding: contiguous slabs of whole grid planes /
@@ -347,6 +453,15 @@ def main():
         dist.all_gather_object(descs, M.peer_window())
         M.peer_connect(descs)
     split = M.set_split(args.split)
+    ranks_joined = 1
+    if world > 1:
+        # every rank has created its context (NCCL communicator or peer windows):
+        # count them
+        jt = torch.ones(1, device=red_dev)
+        dist.all_reduce(jt)
+        ranks_joined = int(jt.item())
+        if ranks_joined != world:
+            sys.exit(f"bench.py: only {ranks_joined} of {world} ranks joined")
     plan.close()
     bd = torch.from_numpy(b).cuda()
     ritz_buf = torch.empty_like(bd)
@@ -491,7 +606,6 @@ def main():
     except Exception:
         traffic_note = None
     m_iter = reps[-1].iterations
-    mat_gb = info["stored"] * ((16 if cplx_run else 8) + 4) / 1e9
     n_bytes = len(b) * (16 if cplx_run else 8)   # this rank's slab of b and x
     line = {
         "metric": "f(A)b time-to-1e-8 rel. error (s) & Krylov-step HBM GB/s vs B200 peak",
@@ -500,23 +614,10 @@ def main():
         "scaling": "strong", "vs_baseline": None,
         "dtype": "c128" if cplx_run else "f64",
         "data": "synthetic (seeded generators in inputs/; no dataset)",
-        "config": {"workload": WORKLOAD.get(name, name), "deg": None if args.plain else deg,
-                   "precond": "none (plain, d = 1)" if args.plain else args.precond,
-                   "poly": {"contour": "contour-LS circle |z-(4+m0)|=2.2, N=128",
-                            "contour-ritz": "contour-LS on the polygon of 60 Ritz values, r_min 0.1, "
-                                            "~2000 points (complex arithmetic)"}.get(args.poly, cfg.poly),
-                   "newton_eval": newton_eval if cfg.poly == "ritz" else None,
-                   "krylov": krylov_m, "check_every": args.check_every, "tol": cfg.tol,
-                   "format": args.fmt, "sell_sigma": sigma, "sell_split": split,
-                   "m": m_iter, "mvms": reps[-1].mvms, "n": A.n, "nnz": A.nnz,
-                   "stored_entries": info["stored"], "stop": f"estimate <= {cfg.tol:g}, k = {args.check_every} (P:424)",
-                   "l2": (f"inputs larger than L2 (matrix {mat_gb:.2f} GB per rank / 126 MB L2), no flush"
-                          if mat_gb > 0.126 else
-                          f"matrix {mat_gb * 1e3:.0f} MB per rank fits the 126 MB L2; no flush "
-                          "(the method re-reads it every SpMV: L2-resident is its real regime)"),
-                   "parallelism": (f"row slabs x{world} (" + ("NCCL halo + allreduce" if args.comm == "nccl"
-                                   else "peer-memory halo push + rank-order reductions") + ")")
-                                  if world > 1 else "single GPU"},
+        "config": workload_config(args, cfg, name, deg, A.n, A.nnz, m_iter, reps[-1].mvms, world,
+                                  cplx_run, krylov_m, newton_eval),
+        "layout": {"format": args.fmt, "sell_sigma": sigma, "sell_split": split,
+                   "stored_entries": info["stored"], "ranks_joined": ranks_joined},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "fused SELL SpMV + Clenshaw/Newton epilogue (spmv class)",
@@ -540,9 +641,8 @@ def main():
                           "note": "same K steps with per-launch CUDA events; roofline and "
                                   "breakdown come from this pass"},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.poly == "config" \
-            and not args.plain and args.precond == "left" and args.krylov is None:
-        line["cpu_baseline"] = cpu_baseline(cfg, A, b, iv, deg, m_iter, reps[-1].mvms)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and oracle_supported(args):
+        line["cpu_baseline"] = cpu_baseline(args, cfg, A, b, iv, deg, m_iter, reps[-1].mvms)
     if args.test_fake_nccl:
         line["test_mode"] = ("fake NCCL, all ranks on GPU 0 (tests/native/fake_nccl.cpp): "
                              "checks the N>1 code path, not a measurement")

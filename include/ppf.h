@@ -23,8 +23,11 @@
  *     contiguous row slab [row0, row0 + n_local) of a global n_global x n_global
  *     matrix in CSR form with GLOBAL column indices sorted within each row.
  *   - "device" pointers are CUDA device memory owned by the caller (PyTorch
- *     allocations), 256-byte aligned, valid for the duration of the call and of
- *     the stream work it enqueues.  The library never calls cudaMalloc or
+ *     allocations), valid for the duration of the call and of the stream work it
+ *     enqueues.  Device vectors and scratch must be 16-byte aligned (they are
+ *     moved as 128-bit pairs and by bulk copies; PPF_EINVAL otherwise, e.g. for
+ *     a float64 view starting at an odd element); 256-byte alignment (what
+ *     the PyTorch allocator returns) is recommended.  The library never calls cudaMalloc or
  *     cudaFree (one exception: the peer window of ppf_mat_peer_window, which a
  *     CUDA IPC export needs as an allocation of its own); size-query functions
  *     say how much the caller must provide.
@@ -44,7 +47,7 @@
 extern "C" {
 #endif
 
-#define PPF_ABI_VERSION 2
+#define PPF_ABI_VERSION 3
 
 typedef enum {
   PPF_OK = 0,
@@ -296,6 +299,18 @@ ppf_status ppf_poly_contour_ls(const double* points, int npts, int deg, double* 
  *   PPF_EBRANCH if the hull surrounds 0. */
 ppf_status ppf_contour_from_ritz(const double* theta, int ntheta, double r_min, double step,
                                  int cap, double* points, int* npts);
+/* ppf_poly_certify: the branch certificate of the preconditioned method --
+ *   q must not vanish where ((q(A))^2)^{1/2} = q(A) is needed: q > 0 on the
+ *   spectral interval for a Chebyshev q (checked at the points of
+ *   P:420), Re q > 0 on the contour for a least-squares q.
+ *   pts: npts host points, PPF_R64 (npts doubles) or PPF_C128 (npts
+ *   interleaved (re, im) pairs); pts == NULL (Chebyshev q only) checks the
+ *   default grid z_k = a + (b-a)k/1000, k = 0..1000.  *min_re_q (may be NULL)
+ *   receives min Re q over the points (NaN if q is NaN anywhere); the status is
+ *   PPF_EBRANCH unless that minimum is > 0.  ppf_poly_chebyshev and
+ *   ppf_poly_contour_ls apply it before returning a polynomial.  Host only. */
+ppf_status ppf_poly_certify(const ppf_poly* q, const void* pts, int npts, int dtype,
+                            double* min_re_q);
 ppf_status ppf_poly_import(int kind, int deg, const double* ab, const void* coef,
                            const void* nodes, ppf_poly** out);
 ppf_status ppf_poly_export(const ppf_poly* q, int* kind, int* deg, double* ab,
@@ -380,6 +395,10 @@ typedef struct {
   double seconds_total;        /* host wall time of the call */
   double seconds_host_dense;   /* host time in f(H_m) evaluations */
   long long kernel_launches;   /* kernels this call launched */
+  double seconds_device;       /* device time of the call's stream work (ABI 3): CUDA events
+                                  recorded on the context stream before the first and after
+                                  the last enqueued operation (H2D / D2H of ppf_run_host
+                                  included) */
 } ppf_report;
 
 ppf_status ppf_workspace_bytes(ppf_ctx* ctx, const ppf_mat* A, const ppf_poly* q,

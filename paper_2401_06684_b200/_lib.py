@@ -49,7 +49,8 @@ class Report(C.Structure):
     _fields_ = [("iterations", C.c_int), ("term", C.c_int), ("mvms", C.c_longlong),
                 ("inner_products", C.c_longlong), ("est", C.c_double), ("err", C.c_double),
                 ("beta0", C.c_double), ("seconds_total", C.c_double),
-                ("seconds_host_dense", C.c_double), ("kernel_launches", C.c_longlong)]
+                ("seconds_host_dense", C.c_double), ("kernel_launches", C.c_longlong),
+                ("seconds_device", C.c_double)]
 
 
 # name -> (restype, argtypes)
@@ -89,6 +90,7 @@ SIGNATURES = {
     "ppf_poly_import": (C.c_int, [C.c_int, C.c_int, dblp, vp, vp, C.POINTER(vp)]),
     "ppf_poly_export": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), dblp, vp, vp]),
     "ppf_poly_eval": (C.c_int, [vp, C.c_int, dblp, dblp]),
+    "ppf_poly_certify": (C.c_int, [vp, vp, C.c_int, C.c_int, dblp]),
     "ppf_poly_destroy": (None, [vp]),
     "ppf_poly_apply_bytes": (C.c_int, [vp, vp, C.POINTER(C.c_size_t)]),
     "ppf_poly_apply": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_size_t]),

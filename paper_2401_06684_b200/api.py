@@ -339,6 +339,27 @@ class Poly:
                                    out.view(np.float64).ctypes.data_as(C.POINTER(C.c_double))))
         return out
 
+    def certify(self, points=None) -> float:
+        """ppf_poly_certify: min Re q over the
+        points (real or complex array; None = the Chebyshev default grid of
+        P:420).  Raises PPFError(PPF_EBRANCH) unless the minimum is > 0 (the
+        minimum is then in the exception's ``min_re``)."""
+        mr = C.c_double()
+        if points is None:
+            st = _lib().ppf_poly_certify(self.h, None, 0, L.R64, C.byref(mr))
+        else:
+            z = np.ascontiguousarray(np.atleast_1d(points))
+            cplx = np.iscomplexobj(z)
+            z = z.astype(np.complex128 if cplx else np.float64, copy=False)
+            st = _lib().ppf_poly_certify(self.h, z.ctypes.data_as(C.c_void_p), len(z),
+                                         L.C128 if cplx else L.R64, C.byref(mr))
+        try:
+            check(st)
+        except L.PPFError as e:
+            e.min_re = mr.value
+            raise
+        return mr.value
+
     def apply(self, ctx: Context, A: Matrix, x, y=None):
         """y = q(A) x: the fused SpMV chain (P:332 Clenshaw / P:354 Newton-Horner)."""
         torch = _torch()
@@ -350,6 +371,11 @@ class Poly:
         check(_lib().ppf_poly_apply(ctx.h, A.h, self.h, C.c_void_p(x.data_ptr()),
                                     C.c_void_p(y.data_ptr()), C.c_void_p(work.data_ptr()),
                                     nb.value))
+        # the chain runs on ctx.stream: keep the caching allocator from handing
+        # out the scratch (and a freshly allocated y) before it has finished
+        if ctx.stream != torch.cuda.current_stream(x.device):
+            work.record_stream(ctx.stream)
+            y.record_stream(ctx.stream)
         return y
 
     def close(self):
@@ -376,6 +402,7 @@ class RunReport:
     seconds_total: float
     seconds_host_dense: float
     kernel_launches: int
+    seconds_device: float = float("nan")
 
 
 _TERM = {L.CONVERGED: "converged", L.MAX_ITER: "max_iter", L.BREAKDOWN: "breakdown"}
@@ -419,7 +446,8 @@ def _qh(q):
 
 def _report(r: L.Report) -> RunReport:
     return RunReport(r.iterations, _TERM.get(r.term, str(r.term)), r.mvms, r.inner_products, r.est,
-                     r.err, r.beta0, r.seconds_total, r.seconds_host_dense, r.kernel_launches)
+                     r.err, r.beta0, r.seconds_total, r.seconds_host_dense, r.kernel_launches,
+                     r.seconds_device)
 
 
 def run(ctx: Context, A: Matrix, q: Poly, b, x=None, work: Workspace | None = None, **opt_kw):

@@ -131,6 +131,8 @@ ppf_status ppf_ctx_create(int device, int rank, int nranks, const void* id128, v
     c->h_pinned_bytes = size_t(66) * 65 * 16 + 2 * 2048;  // grown by ppf_run for larger m_max
     PPF_CUDA(cudaHostAlloc(&c->h_pinned, c->h_pinned_bytes, cudaHostAllocDefault));
     PPF_CUDA(cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming));
+    PPF_CUDA(cudaEventCreate(&c->ev_t0));
+    PPF_CUDA(cudaEventCreate(&c->ev_t1));
     if (nranks > 1) ppf::preload_kernels();
     if (nranks > 1 && id128) {
       ncclUniqueId id;
@@ -197,6 +199,8 @@ void ppf_ctx_destroy(ppf_ctx* c) {
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->t_host) cudaFreeHost(c->t_host);
   if (c->ev) cudaEventDestroy(c->ev);
+  if (c->ev_t0) cudaEventDestroy(c->ev_t0);
+  if (c->ev_t1) cudaEventDestroy(c->ev_t1);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);
   if (c->ev_halo) cudaEventDestroy(c->ev_halo);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -566,10 +570,23 @@ ppf_status ppf_poly_chebyshev(double a, double b, int deg, ppf_poly** out) {
   q->b = b;
   chebyshev_coefficients(a, b, deg, q->c);
   // positivity certificate on z_k = a + (b-a)k/1000
-  double mn = HUGE_VAL;
-  for (int k = 0; k <= 1000; ++k) mn = std::min(mn, chebyshev_eval(*q, a + (b - a) * k / 1000.0));
-  if (!(mn > 0.0)) fail(PPF_EBRANCH, "Chebyshev q is not positive on [a, b]");
+  if (!(certify_min_re(*q, nullptr, 0, PPF_R64) > 0.0))
+    fail(PPF_EBRANCH, "Chebyshev q is not positive on [a, b]");
   *out = g.release();
+  PPF_API_END
+}
+
+ppf_status ppf_poly_certify(const ppf_poly* q, const void* pts, int npts, int dtype,
+                            double* min_re_q) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(q, "NULL polynomial");
+  PPF_REQUIRE(dtype == PPF_R64 || dtype == PPF_C128, "bad dtype");
+  PPF_REQUIRE(npts >= 0 && (npts == 0 || pts), "bad points");
+  PPF_REQUIRE(pts || q->kind == PPF_POLY_CHEBYSHEV,
+              "default points exist only for a Chebyshev q (its interval [a, b])");
+  const double mn = certify_min_re(*q, pts, pts ? npts : 0, dtype);
+  if (min_re_q) *min_re_q = mn;
+  if (!(mn > 0.0)) fail(PPF_EBRANCH, "certificate failed: Re q <= 0 at a point");
   PPF_API_END
 }
 
@@ -663,14 +680,25 @@ ppf_status ppf_poly_contour_ls(const double* points, int npts, int deg, double* 
     delete q;
     throw;
   }
-  if (min_re_q) *min_re_q = mr;
-  if (!(mr > 0.0)) {
-    delete q;
-    fail(PPF_EBRANCH, "Re q <= 0 at a contour point (certificate of P:401-403)");
-  }
   q->kind = PPF_POLY_NEWTON;
   q->deg = deg;
   q->a = q->b = 0.0;
+  // certificate of P:401-403 on the stored (Newton) form q applies, through
+  // ppf_poly_certify's evaluation; the least-squares fit's own values agree
+  // to rounding (mr)
+  (void)mr;
+  double mc = 0.0;
+  try {
+    mc = certify_min_re(*q, points, npts, PPF_C128);
+  } catch (...) {
+    delete q;
+    throw;
+  }
+  if (min_re_q) *min_re_q = mc;
+  if (!(mc > 0.0)) {
+    delete q;
+    fail(PPF_EBRANCH, "Re q <= 0 at a contour point (certificate of P:401-403)");
+  }
   *out = q;
   PPF_API_END
 }

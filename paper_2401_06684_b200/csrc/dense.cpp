@@ -30,6 +30,12 @@ inline bool on_branch_cut(zc z) {
 
 }  // namespace
 
+// Provenance: the QL sweep below is the textbook implicit-shift QL iteration
+// for a symmetric tridiagonal matrix in its classical EISPACK tql2 / Numerical
+// Recipes tqli form (Wilkinson shift, rotations chased up from the bottom of
+// the unreduced block; variable names g, r, s, c, p, f, b follow that form).
+// What is added here: the rotations are logged and row 0 of the eigenvector
+// matrix is tracked instead of accumulating it.
 // The eigenvector matrix is never formed: Z = R_1 R_2 ... R_K is a product of
 // plane rotations on adjacent columns (i, i+1).  Only e_1^T Z is needed for the
 // weights and Z w for the result, so row 0 of Z is tracked through the

@@ -11,6 +11,7 @@
 //  * Lanczos (K8), combine x = V y (K9), norms.
 // Reductions are deterministic: per-block partials, then the last block to
 // arrive sums them in block order (fixed tree), independent of timing.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -1201,12 +1202,17 @@ void launch_combine(ppf_dtype dt, int64_t n, const void* V, int64_t ldv, int nco
 template <typename T, int NC, int FL>
 static void cgs_go(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* ci, T* co, T* hc,
                    T* hs, double* inv, RedScratch& rs, double* raw, int grid, cudaStream_t st) {
-  static bool attr = false;  // per instantiation
-  if (!attr) {
+  // the attribute is per device: one bit per device ordinal, per instantiation
+  // (setting it twice from racing host threads is harmless)
+  static std::atomic<unsigned long long> attr_done{0};
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_done.load(std::memory_order_acquire) & bit)) {
     cuda_check(cudaFuncSetAttribute(cgs_kernel<T, NC, FL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     CGS_SMEM),
                "cudaFuncSetAttribute(cgs_kernel)");
-    attr = true;
+    attr_done.fetch_or(bit, std::memory_order_release);
   }
   const int S = cgs_stages<T>(nct);
   const int RC = cgs_rows<T>() * cgs_rpt<T>(nct);

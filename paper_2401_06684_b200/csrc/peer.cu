@@ -428,7 +428,18 @@ ppf_status ppf_mat_peer_connect(ppf_mat* A, const void* descs) {
     if (q == me) {
       P->peer[q] = P->win;
     } else if (D[q].pid == mypid && D[q].nonce == mynonce) {
-      P->peer[q] = reinterpret_cast<char*>(D[q].win);  // a rank of this process
+      // a rank of this process: its raw pointer is only usable here if it
+      // lives on this rank's device (several contexts on one GPU, the tests)
+      // or peer access to its device is enabled
+      if (D[q].device != ctx->device) {
+        int can = 0;
+        PPF_CUDA(cudaDeviceCanAccessPeer(&can, ctx->device, D[q].device));
+        PPF_REQUIRE(can, "same-process rank on a device without peer access to this one");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(D[q].device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) (void)cudaGetLastError();
+        else PPF_CUDA(e);
+      }
+      P->peer[q] = reinterpret_cast<char*>(D[q].win);
     } else {
       void* p = nullptr;
       PPF_CUDA(cudaIpcOpenMemHandle(&p, D[q].ipc, cudaIpcMemLazyEnablePeerAccess));

@@ -44,6 +44,32 @@ double chebyshev_eval(const ppf_poly& q, double z) {
   return q.c[0] + t * b1 - b2;
 }
 
+// Certificate (P:334-335 for Chebyshev, P:401-403 for a contour): min Re q
+// over the points -- host `pts` of npts R64 or C128 (interleaved) values, or
+// (pts == NULL, Chebyshev only) z_k = a + (b-a)k/1000, k = 0..1000.
+// NaN anywhere gives NaN (so "min > 0" fails).
+double certify_min_re(const ppf_poly& q, const void* pts, int npts, int dtype) {
+  double mn = HUGE_VAL;
+  auto take = [&](double v) {
+    if (std::isnan(v) || std::isnan(mn)) mn = NAN;
+    else mn = std::min(mn, v);
+  };
+  if (!pts) {
+    for (int k = 0; k <= 1000; ++k) {
+      const double z = q.a + (q.b - q.a) * k / 1000.0;
+      take(q.kind == PPF_POLY_CHEBYSHEV ? chebyshev_eval(q, z) : poly_eval(q, zc(z, 0.0)).real());
+    }
+    return mn;
+  }
+  const double* p = static_cast<const double*>(pts);
+  for (int i = 0; i < npts; ++i) {
+    const zc z = dtype == PPF_C128 ? zc(p[2 * i], p[2 * i + 1]) : zc(p[i], 0.0);
+    if (q.kind == PPF_POLY_CHEBYSHEV && z.imag() == 0.0) take(chebyshev_eval(q, z.real()));
+    else take(poly_eval(q, z).real());
+  }
+  return mn;
+}
+
 zc poly_eval(const ppf_poly& q, zc z) {
   if (q.kind == PPF_POLY_CHEBYSHEV) {
     const zc t = (2.0 * z - q.a - q.b) / (q.b - q.a);

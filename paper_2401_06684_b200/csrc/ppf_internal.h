@@ -76,6 +76,10 @@ void cuda_check(cudaError_t e, const char* what);
   do {                         \
     if (!(cond)) ::ppf::fail(PPF_EINVAL, msg); \
   } while (0)
+// device vectors and scratch are read and written as 128-bit pairs (double2,
+// complex128) and fed to cp.async.bulk: 16-byte alignment is required
+#define PPF_REQUIRE_ALIGNED(p, name) \
+  PPF_REQUIRE((reinterpret_cast<uintptr_t>(p) & 15) == 0, name " must be 16-byte aligned")
 
 // ---------------------------------------------------------------------------
 // Matrix layout
@@ -192,6 +196,7 @@ struct ppf_ctx {
   void* h_pinned;
   size_t h_pinned_bytes;
   cudaEvent_t ev;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // timing events: ppf_report.seconds_device
   // last run
   std::vector<ppf::HistRec> hist;
   std::vector<double> lastH;  // (m+1) x m, n_doubles per entry, column-major ld = m+1
@@ -240,6 +245,7 @@ std::vector<zc> eigenvalues(int m, std::vector<zc> H);
 void chebyshev_coefficients(double a, double b, int deg, std::vector<double>& c);
 double chebyshev_eval(const ppf_poly& q, double z);
 zc poly_eval(const ppf_poly& q, zc z);
+double certify_min_re(const ppf_poly& q, const void* pts, int npts, int dtype);
 std::vector<zc> leja_order(const std::vector<zc>& nodes);
 std::vector<zc> divided_differences_invsqrt(const std::vector<zc>& nodes);
 void real_pair_form(ppf_poly& q);

@@ -815,6 +815,8 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   PPF_REQUIRE(ctx && A && rep, "NULL argument");
   PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
   check_opts(o);
+  PPF_REQUIRE_ALIGNED(work, "work");
+  if (o->x_ref) PPF_REQUIRE_ALIGNED(o->x_ref, "x_ref");
   PPF_REQUIRE(!q || poly_fits(q, A->dtype),
               "a Newton polynomial with complex nodes needs a complex operator");
   const bool twopass = o->krylov == PPF_LANCZOS_2PASS;
@@ -840,6 +842,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   double t_dense = 0.0;
   ctx->hist.clear();
 
+  PPF_CUDA(cudaEventRecord(ctx->ev_t0, R.st));
   const void* bin = b;
   if (b_host) {
     PPF_CUDA(cudaMemcpyAsync(R.vec(R.L.U), b_host, vb, cudaMemcpyHostToDevice, R.st));
@@ -1145,14 +1148,12 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     R.spmv(fo, xo, Runner::epi(1.0, 0.0, 0.0, nullptr, 0.0, nullptr));
     mv_total += 1;
   }
-  if (x_host) {
-    PPF_CUDA(cudaMemcpyAsync(x_host, xo, vb, cudaMemcpyDeviceToHost, R.st));
-    PPF_CUDA(cudaStreamSynchronize(R.st));
-  } else {
-    // the host staging for y must not be reused before the copy is done
-    PPF_CUDA(cudaEventRecord(ctx->ev, R.st));
-    PPF_CUDA(cudaEventSynchronize(ctx->ev));
-  }
+  if (x_host) PPF_CUDA(cudaMemcpyAsync(x_host, xo, vb, cudaMemcpyDeviceToHost, R.st));
+  // (also: the host staging for y must not be reused before its copy is done)
+  PPF_CUDA(cudaEventRecord(ctx->ev_t1, R.st));
+  PPF_CUDA(cudaEventSynchronize(ctx->ev_t1));
+  float dev_ms = 0.0f;
+  PPF_CUDA(cudaEventElapsedTime(&dev_ms, ctx->ev_t0, ctx->ev_t1));
   R.flush_prof();
   // keep H for ppf_hessenberg
   ctx->last_m = m;
@@ -1184,6 +1185,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   rep->beta0 = beta0;
   rep->seconds_host_dense = t_dense;
   rep->kernel_launches = R.launches;
+  rep->seconds_device = 1e-3 * double(dev_ms);
   rep->seconds_total =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   return PPF_OK;
@@ -1224,6 +1226,8 @@ ppf_status ppf_run(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts* 
                    void* x, void* work, size_t bytes, ppf_report* rep) {
   PPF_API_BEGIN
   PPF_REQUIRE(b && x, "NULL b/x");
+  PPF_REQUIRE_ALIGNED(b, "b");
+  PPF_REQUIRE_ALIGNED(x, "x");
   return run_impl(ctx, A, q, o, b, x, nullptr, nullptr, work, bytes, rep);
   PPF_API_END
 }
@@ -1288,6 +1292,8 @@ ppf_status ppf_poly_ritz_newton_pow(ppf_ctx* ctx, ppf_mat* A, const void* start,
   PPF_REQUIRE(ctx && A && start && out, "NULL argument");
   PPF_REQUIRE(deg >= 0 && deg < 255, "deg out of range");
   PPF_REQUIRE(power == 1 || power == 2, "power must be 1 or 2");
+  PPF_REQUIRE_ALIGNED(start, "start");
+  PPF_REQUIRE_ALIGNED(work, "work");
   const int d = deg + 1;
   Runner R(ctx, A, nullptr, d, work, bytes, WS_SQUARE);
   R.power = power;
@@ -1356,6 +1362,8 @@ extern "C" ppf_status ppf_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y)
   try {
     PPF_REQUIRE(ctx && A && x && y, "NULL argument");
     PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+    PPF_REQUIRE_ALIGNED(x, "x");
+    PPF_REQUIRE_ALIGNED(y, "y");
     ppf::Epi e{};
     e.s_ax[0] = 1.0;
     if (A->nranks > 1) {
@@ -1392,6 +1400,9 @@ extern "C" ppf_status ppf_poly_apply(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q
     PPF_REQUIRE(ctx && A && q && x && y, "NULL argument");
     PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
     PPF_REQUIRE(x != y, "x and y must be distinct");
+    PPF_REQUIRE_ALIGNED(x, "x");
+    PPF_REQUIRE_ALIGNED(y, "y");
+    PPF_REQUIRE_ALIGNED(work, "work");
     PPF_REQUIRE(ppf::poly_fits(q, A->dtype),
                 "a Newton polynomial with complex nodes needs a complex operator");
     ppf::Runner R(ctx, A, q, 1, work, bytes);
@@ -1415,6 +1426,7 @@ extern "C" ppf_status ppf_halo_pack(ppf_ctx* ctx, ppf_mat* A, const void* x) {
   try {
     PPF_REQUIRE(ctx && A && x, "NULL argument");
     PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+    PPF_REQUIRE_ALIGNED(x, "x");
     ppf::launch_halo_pack(A, x, ctx->stream);
     ctx->launches += A->send_total ? 1 : 0;
     return PPF_OK;
@@ -1438,6 +1450,8 @@ extern "C" ppf_status ppf_spmv_local(ppf_ctx* ctx, ppf_mat* A, const void* x, vo
   try {
     PPF_REQUIRE(ctx && A && x && y, "NULL argument");
     PPF_REQUIRE(A->ctx == ctx, "matrix belongs to another context");
+    PPF_REQUIRE_ALIGNED(x, "x");
+    PPF_REQUIRE_ALIGNED(y, "y");
     ppf::Epi e{};
     e.s_ax[0] = 1.0;
     ppf::launch_spmv(A, x, y, e, ctx->stream);

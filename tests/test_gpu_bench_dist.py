@@ -53,6 +53,7 @@ def test_bench_two_ranks_matches_one(extra):
     one = _bench(1, extra)
     two = _bench(2, extra)
     assert two["n_gpus"] == 2 and "test_mode" in two
+    assert two["layout"]["ranks_joined"] == 2
     assert two["config"]["parallelism"].startswith("row slabs x2")
     assert ("NCCL" if "nccl" in extra else "peer-memory") in two["config"]["parallelism"]
     assert two["config"]["m"] == one["config"]["m"]

@@ -1,24 +1,53 @@
-"""Full BASELINE.json sizes, in the launch configuration bench.py times
-(SELL-C-64 for fp64, SELL-C-32 for complex128, estimate stop at k = 1):
-sampled outputs the oracle computes one by one (rows of A x), and properties
-that hold at any size (true error against the closed forms R1/R2, the invariant
-D (D^{-1/2} (D^{-1/2} b)) = b for the Wilson operator, P:115-124 branch
-conditions on the Ritz nodes)."""
+"""Oracle parity at the FULL BASELINE.json sizes (C3 deg 10/20/40, C4, C5; the
+Ex. 6.3 context workload C7), in the launch configuration bench.py times
+(bench.default_layout: SELL-C-64 for the fp64 stencils, SELL-C-32 for complex
+and the sorted graph; CUDA-graph replay of the chain; estimate stop k = 1).
+
+The oracle's side comes from tests/fullsize_oracle.py -- stored in
+tests/golden/fullsize/ by tools/make_fullsize_goldens.py (oracle-only), or run
+live on this box's host cores with PPF_LIVE_ORACLE=1.  Per workload and stop
+rule (true error = m*, reading Q11; the paper's estimate) the GPU
+run must give
+  * the same m, termination, mat-vec count and estimate history,
+  * beta0 = ||c|| to 1e-13,
+  * H_m normwise within 1e-11, or 10x the measured oracle-vs-oracle gap where
+    the Arnoldi process itself amplifies rounding beyond it (reading Q19),
+  * x: ||dx_S|| / ||x_S|| <= 1e-10 on the sampled rows S (65,536 seeded rows
+    plus the first and last 1024) and the same bar on the 32 Gaussian
+    projections (||G dx|| / ||G x|| estimates ||dx|| / ||x|| over ALL entries;
+    checked at half the bar for the chi-square spread of 32 probes), and
+    ||x|| to 1e-10.
+The measured GPU gaps are printed next to every bar (run with -s).
+Also: sampled rows of the full-size SpMV against SciPy, and the C6 sign
+involution (context workload).
+"""
 import numpy as np
 import pytest
 
+import bench
 from inputs import configs
-from oracle import reference
+from inputs.vectors import probe_projections
+
+from . import fullsize_oracle as fo
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2401_06684_b200 as pp  # noqa: E402
 
+X_TOL, H_TOL, B_TOL = 1e-10, 1e-11, 1e-13
+
 
 @pytest.fixture(scope="module")
 def ctx():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
     return pp.Context(0)
+
+
+def _matrix(ctx, cfg, A, cplx):
+    fmt, sigma = bench.default_layout(cfg, A.n, cplx)
+    C_ = 64 if fmt == "sell64" else 32
+    return pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=C_, sigma=sigma))
 
 
 def _sampled_spmv(ctx, A, M, rng, nsample=4096):
@@ -38,68 +67,154 @@ def _sampled_spmv(ctx, A, M, rng, nsample=4096):
     assert np.all(np.abs(y - ref) <= 1e-14 * scale)
 
 
-def test_c4_fullsize(ctx):
-    cfg = configs.CONFIGS["C4"]
-    A, b, iv = configs.build("C4")
-    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=64))
-    _sampled_spmv(ctx, A, M, np.random.default_rng(1))
-    q = pp.Poly.chebyshev(*iv, 20)
-    xg, rep = pp.run(ctx, M, q, torch.from_numpy(b).cuda(), func="sqrt", krylov="cgs2",
-                     m_max=cfg.m_max, stop="est", tol=cfg.tol)
-    torch.cuda.synchronize()
-    xr = reference.convdiff_fAb(256, 3, (10.0, 10.0, 10.0), b, "sqrt")
-    err = np.linalg.norm(xg.cpu().numpy() - xr) / np.linalg.norm(xr)
-    assert rep.term == "converged" and rep.iterations <= 30
-    # the estimate tracks the error; stopping at est <= 1e-8 leaves err ~ 1e-8
-    assert err <= 3e-8, err
-    assert rep.mvms == 20 + 1 + rep.iterations * 41
+def _compare_x(g, mode, x, tag):
+    idx = g["idx"]
+    xs = g[f"{mode}_x_samples"]
+    e_s = np.linalg.norm(x[idx] - xs) / np.linalg.norm(xs)
+    proj = probe_projections(x, fo.PROBE_K, fo.PROBE_SEED)
+    po = g[f"{mode}_x_proj"]
+    e_p = np.linalg.norm(proj - po) / np.linalg.norm(po)
+    e_n = abs(np.linalg.norm(x) - g[f"{mode}_x_norm"]) / g[f"{mode}_x_norm"]
+    print(f"[{tag}] x: sampled {e_s:.2e}, projected {e_p:.2e}, norm {e_n:.2e} (bar {X_TOL:g})")
+    assert e_s <= X_TOL, e_s
+    assert e_p <= 0.5 * X_TOL, e_p
+    assert e_n <= X_TOL, e_n
 
 
-def test_c3_fullsize(ctx):
-    cfg = configs.CONFIGS["C3"]
-    A, b, iv = configs.build("C3")
-    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=64))
-    _sampled_spmv(ctx, A, M, np.random.default_rng(2))
-    xr = reference.laplacian_fAb(200, 3, b)
-    for deg in cfg.degs:
-        q = pp.Poly.chebyshev(*iv, deg)
-        xg, rep = pp.run(ctx, M, q, torch.from_numpy(b).cuda(), func="invsqrt", krylov="lanczos",
-                         m_max=cfg.m_max, stop="true", tol=cfg.tol, x_ref=torch.from_numpy(xr).cuda())
-        torch.cuda.synchronize()
-        err = np.linalg.norm(xg.cpu().numpy() - xr) / np.linalg.norm(xr)
-        assert rep.term == "converged" and err <= 1e-8
-        # m* at the paper's own kind of workload (52 / 27 / 14 with another seed)
-        assert abs(rep.iterations - {10: 52, 20: 27, 40: 14}[deg]) <= 2
+def _compare_run(ctx, g, mode, rep, x, cplx, tag, h_bar, fixed=False):
+    assert rep.iterations == g[f"{mode}_m"], (rep.iterations, g[f"{mode}_m"])
+    if not fixed:
+        assert rep.term == g[f"{mode}_term"]
+    assert rep.mvms == g[f"{mode}_mvms"]
+    Hg, beta0 = pp.hessenberg(ctx, cplx)
+    Ho = g[f"{mode}_H"]
+    assert Hg.shape == Ho.shape
+    e_h = np.abs(Hg - Ho).max() / np.abs(Ho).max()
+    e_b = abs(beta0 - g[f"{mode}_beta0"]) / g[f"{mode}_beta0"]
+    print(f"[{tag}] m = {rep.iterations} (oracle {g[f'{mode}_m']}), H gap {e_h:.2e} "
+          f"(bar {h_bar:.1e}; oracle-vs-oracle {g['h_gap_oracle']:.1e}: {g['h_gap_how']}), "
+          f"beta0 gap {e_b:.1e}")
+    assert e_h <= h_bar, e_h
+    assert e_b <= B_TOL, e_b
+    if fixed:   # no checkpoints in a fixed-m run
+        _compare_x(g, mode, x, tag)
+        return
+    hist = pp.history(ctx)
+    hm = g[f"{mode}_hist_m"]
+    assert [h["m"] for h in hist] == list(hm)
+    for hg, eo in zip(hist, g[f"{mode}_hist_est"]):
+        if not np.isnan(eo):
+            assert hg["est"] == pytest.approx(eo, rel=1e-6, abs=1e-13)
+    _compare_x(g, mode, x, tag)
 
 
-def test_c5_fullsize_invariant(ctx):
-    cfg = configs.CONFIGS["C5"]
-    A, b, _ = configs.build("C5")
-    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32))
-    _sampled_spmv(ctx, A, M, np.random.default_rng(3))
+def _h_bar(g):
+    return max(H_TOL, 10.0 * g["h_gap_oracle"])
+
+
+def _poly(ctx, g, iv, cfg):
+    if g["poly"] == "chebyshev":
+        q = pp.Poly.chebyshev(*iv, int(g["deg"]))
+        # the host construction itself (a0) against the oracle's coefficients
+        ex = q.export()
+        assert np.abs(ex["c"] - g["q_c"]).max() <= 1e-14 * np.abs(g["q_c"]).max()
+        return q
+    nodes, dd = g["q_nodes"], g["q_dd"]
+    if cfg.family == "graph":        # real operator: real Ritz values and dd
+        assert np.abs(nodes.imag).max() == 0.0
+        nodes, dd = nodes.real.astype(np.complex128), dd.real.astype(np.complex128)
+    q = pp.Poly.newton(nodes, dd)     # the oracle's q imported (reading Q19)
+    if cfg.family == "graph":
+        q.set_newton_eval("basis")
+    return q
+
+
+@pytest.mark.parametrize("key", ["C3_deg10", "C3_deg20", "C3_deg40", "C4_deg20", "C5_deg16",
+                                 "C7_deg15"])
+def test_fullsize_oracle_parity(ctx, key):
+    g = fo.load(key)
+    name = g["config"]
+    cfg = configs.CONFIGS[name]
+    A, b, iv = configs.build(name)
+    cplx = np.iscomplexobj(b)
+    M = _matrix(ctx, cfg, A, cplx)
+    _sampled_spmv(ctx, A, M, np.random.default_rng(len(key)))
+    q = _poly(ctx, g, iv, cfg)
     bd = torch.from_numpy(b).cuda()
-    q = pp.Poly.ritz_newton(ctx, M, bd, 16)
-    nodes = q.export()["nodes"]
-    assert np.all(nodes.real > 0)
-    assert np.abs(q.eval(nodes) - nodes ** -0.5).max() < 1e-8
-    x1, rep1 = pp.run(ctx, M, q, bd, func="invsqrt", krylov="cgs2", m_max=cfg.m_max, stop="est",
-                      tol=1e-12)
-    x2, rep2 = pp.run(ctx, M, q, x1.clone(), func="invsqrt", krylov="cgs2", m_max=cfg.m_max,
-                      stop="est", tol=1e-12)
+    kw = dict(func=cfg.func, krylov=cfg.krylov, m_max=int(g["m_max"]), tol=float(g["tol"]),
+              check_every=int(g["check_every"]))
+    if "true_m" in g:
+        if cfg.family in ("laplacian", "convdiff"):
+            # m*: the GPU stops itself at true error <= tol against the closed form
+            xr = fo.reference_solution(name, A, b)
+            xg, rep = pp.run(ctx, M, q, bd, stop="true", x_ref=torch.from_numpy(xr).cuda(), **kw)
+            torch.cuda.synchronize()
+            errs = [h["err"] for h in pp.history(ctx)]
+            np.testing.assert_allclose(errs, g["true_hist_err"], rtol=1e-4)
+        else:
+            # Haar links: the reference is itself an Arnoldi run (R4) -- fixed m at the oracle's m*
+            kw_f = dict(kw, m_max=int(g["true_m"]))
+            xg, rep = pp.run(ctx, M, q, bd, stop="fixed", **kw_f)
+        torch.cuda.synchronize()
+        _compare_run(ctx, g, "true", rep, xg.cpu().numpy(), cplx, f"{key} m*", _h_bar(g),
+                     fixed=cfg.family not in ("laplacian", "convdiff"))
+    xg, rep = pp.run(ctx, M, q, bd, stop="est", **kw)
     torch.cuda.synchronize()
-    res = A.to_scipy() @ x2.cpu().numpy() - b
-    assert np.linalg.norm(res) / np.linalg.norm(b) <= 1e-9
-    assert rep1.iterations <= 8
+    _compare_run(ctx, g, "est", rep, xg.cpu().numpy(), cplx, f"{key} est", _h_bar(g))
+
+
+def test_c4_mstar_is_23():
+    """The headline config's m* (seed 104): 23 by the true error, 23 by the
+    estimate (the iteration count bench.py's C4 line must report)."""
+    g = fo.load("C4_deg20")
+    assert g["true_m"] == 23 and g["est_m"] == 23
+
+
+@pytest.mark.parametrize("key", ["C5_deg16", "C7_deg15"])
+def test_fullsize_library_ritz(ctx, key):
+    """The library's own Ritz construction on the device (from L b for the
+    graph, Thm 4.1) as bench.py runs it: nodes agree with the oracle's as
+    multisets (node values are parity-unpinned at ~1e-11), the run
+    stops at the oracle's m, and x matches the oracle's x (own q each side)."""
+    g = fo.load(key)
+    name = g["config"]
+    cfg = configs.CONFIGS[name]
+    A, b, _ = configs.build(name)
+    cplx = np.iscomplexobj(b)
+    M = _matrix(ctx, cfg, A, cplx)
+    bd = torch.from_numpy(b).cuda()
+    start = bd
+    if cfg.params.get("ritz_start") == "Ab":
+        start = torch.empty_like(bd)
+        M.spmv(bd, start)
+    q = pp.Poly.ritz_newton(ctx, M, start, int(g["deg"]))
+    if cfg.family == "graph":
+        q.set_newton_eval("basis")
+    nodes = q.export()["nodes"]
+    on = g["q_nodes"]
+    gap = np.abs(np.sort_complex(nodes) - np.sort_complex(on)).max() / np.abs(on).max()
+    print(f"[{key} own Ritz] node multiset gap {gap:.1e} (bar 1e-8)")
+    assert gap <= 1e-8
+    xg, rep = pp.run(ctx, M, q, bd, func=cfg.func, krylov=cfg.krylov, m_max=int(g["m_max"]),
+                     stop="est", tol=float(g["tol"]), check_every=int(g["check_every"]))
+    torch.cuda.synchronize()
+    assert rep.iterations == g["est_m"]
+    # graph: the estimate-stop iterate of a strongly non-normal operator carries
+    # the node difference amplified (measured, see DESIGN.md Q19): own-q bar 1e-8
+    tol = X_TOL if cfg.family != "graph" else 1e-8
+    x = xg.cpu().numpy()
+    e_s = np.linalg.norm(x[g["idx"]] - g["est_x_samples"]) / np.linalg.norm(g["est_x_samples"])
+    print(f"[{key} own Ritz] x sampled gap {e_s:.2e} (bar {tol:g})")
+    assert e_s <= tol
 
 
 def test_c6_fullsize_sign_involution(ctx):
-    """sign(Q)b for the 16^4 overlap kernel (bench C6): sign(Q)(sign(Q) b) = b
-    (sign(Q)^2 = I) in the bench's launch configuration, Ritz values of Q^2 off
-    the branch cut, and the (Q^2)^{-1/2} b iterate satisfies Q^2 f ~ ... via
-    sign: Q f = sign(Q) b."""
+    """sign(Q)b for the 16^4 overlap kernel (bench C6, context workload):
+    sign(Q)(sign(Q) b) = b (sign(Q)^2 = I) in the bench's launch configuration,
+    Ritz values of Q^2 off the branch cut."""
     cfg = configs.CONFIGS["C6"]
     A, b, _ = configs.build("C6")
-    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32))
+    M = _matrix(ctx, cfg, A, True)
     _sampled_spmv(ctx, A, M, np.random.default_rng(6))
     bd = torch.from_numpy(b).cuda()
     q = pp.Poly.ritz_newton(ctx, M, bd, 15, power=2)
@@ -112,31 +227,3 @@ def test_c6_fullsize_sign_involution(ctx):
     assert r1.term == "converged" and r2.term == "converged"
     torch.cuda.synchronize()
     assert np.linalg.norm(s2.cpu().numpy() - b) <= 1e-9 * np.linalg.norm(b)
-
-
-def test_c7_fullsize_sqrt_invariant(ctx):
-    """L^{1/2} b for the synthetic 281,903-node graph Laplacian (bench C7, global
-    SELL-32 sorting, forward-basis Newton chain): L^{1/2}(L^{1/2} b) = L b
-    (Theorem 4.1's setting) with the Ritz q from L b."""
-    cfg = configs.CONFIGS["C7"]
-    A, b, _ = configs.build("C7")
-    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=32, sigma=32 * ((A.n + 31) // 32)))
-    _sampled_spmv(ctx, A, M, np.random.default_rng(7))
-    bd = torch.from_numpy(b).cuda()
-    Lb = torch.empty_like(bd)
-    M.spmv(bd, Lb)
-    q = pp.Poly.ritz_newton(ctx, M, Lb, 15).set_newton_eval("basis")
-    assert np.all(q.export()["nodes"].real > 0)
-    x1, r1 = pp.run(ctx, M, q, bd, func="sqrt", krylov="cgs2", m_max=250, stop="est", tol=1e-10,
-                    check_every=2)
-    x2, r2 = pp.run(ctx, M, q, x1.clone(), func="sqrt", krylov="cgs2", m_max=250, stop="est",
-                    tol=1e-10, check_every=2)
-    assert r1.term == "converged" and r2.term == "converged"
-    torch.cuda.synchronize()
-    Lbh = Lb.cpu().numpy()
-    # bar: 10x what the oracle itself reaches with this stopping rule (estimate
-    # 1e-10 at k = 2): 9.0e-5 at full size (m = 186 / 148), because on this
-    # strongly non-normal operator the paper's estimate is optimistic (at
-    # n = 20000 the oracle's est 1e-10 is a true error of 4e-8) and the
-    # composition doubles it; a wrong result would be O(1) off
-    assert np.linalg.norm(x2.cpu().numpy() - Lbh) <= 9e-4 * np.linalg.norm(Lbh)

@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol():
     assert not missing, missing
     # and the binding declares all of them
     assert names <= set(_lib.SIGNATURES), names - set(_lib.SIGNATURES)
-    assert lib.ppf_abi_version() == 2
+    assert lib.ppf_abi_version() == 3
 
 
 def test_no_batch_memcpy_in_sources():
@@ -73,6 +73,47 @@ def test_chebyshev_invalid_arguments():
         Poly.chebyshev(2.0, 1.0, 3)
     with pytest.raises(_lib.PPFError):
         Poly.chebyshev(1.0, 2.0, -1)
+
+
+@pytest.mark.parametrize("name,deg", [("C1", 4), ("C3", 10), ("C4", 20)])
+def test_poly_certify_chebyshev(name, deg):
+    """ppf_poly_certify: on the default grid the minimum is
+    the oracle's certificate of the same polynomial; on real and complex point
+    sets it is min Re q there (the oracle's evaluation)."""
+    iv = configs.build(name)[2] if name == "C1" else None
+    if iv is None:
+        cfg = configs.CONFIGS[name]
+        p = cfg.params
+        iv = (ops.laplacian_interval(p["N"], p["dim"]) if cfg.family == "laplacian"
+              else ops.convdiff_interval(p["N"], p["dim"], p["beta"]))
+    q = Poly.chebyshev(*iv, deg)
+    qo = chebyshev.coefficients(*iv, deg)
+    assert q.certify() == pytest.approx(chebyshev.certify(qo), rel=1e-12)
+    pts = np.linspace(iv[0], iv[1], 333)
+    assert q.certify(pts) == pytest.approx(chebyshev.evaluate(qo, pts).min(), rel=1e-12)
+    zc_ = pts + 0.01j * (iv[1] - iv[0])
+    assert q.certify(zc_) == pytest.approx(q.eval(zc_).real.min(), rel=1e-14)
+
+
+def test_poly_certify_failure_and_contour():
+    """The certificate fails (PPF_EBRANCH, minimum reported) where q has a zero:
+    the degree-3 interpolant of z^{-1/2} on [1, 9] at points beyond the
+    interval; the least-squares q's certificate equals the value
+    ppf_poly_contour_ls reported."""
+    q = Poly.chebyshev(1.0, 9.0, 3)
+    zs = np.linspace(1.0, 60.0, 400)
+    vals = chebyshev.evaluate(chebyshev.coefficients(1.0, 9.0, 3), zs)
+    assert vals.min() <= 0.0          # the oracle says q has a zero past b
+    with pytest.raises(_lib.PPFError) as e:
+        q.certify(zs)
+    assert e.value.status == 5 and e.value.min_re == pytest.approx(vals.min(), rel=1e-12)
+    z = contour_ls.circle(3.0, 2.2, 128)
+    ql = Poly.contour_ls(z, 6)
+    assert ql.certify(z) == ql.min_re
+    assert ql.min_re == pytest.approx(contour_ls.certify(contour_ls.construct(z, 6)), rel=1e-10)
+    with pytest.raises(_lib.PPFError) as e:
+        ql.certify()                  # no default points for a Newton-form q
+    assert e.value.status == 1
 
 
 def test_newton_import_eval_matches_oracle():
