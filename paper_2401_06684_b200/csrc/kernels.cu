@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "ppf_internal.h"
@@ -617,6 +618,21 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
+// ld.shared at a 32-bit shared-window address; volatile: the ring's stages
+// are rewritten by the bulk copies between mbarrier waits, so a load must
+// never be merged with one from an earlier pass over the same stage
+template <typename T> __device__ __forceinline__ T lds_s(uint32_t a);
+template <> __device__ __forceinline__ double lds_s<double>(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+template <> __device__ __forceinline__ cplx lds_s<cplx>(uint32_t a) {
+  cplx v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.re), "=d"(v.im) : "r"(a));
+  return v;
+}
+
 // shared-memory read the compiler may not hoist out of the chunk loop (the
 // nct coefficients would otherwise occupy registers next to the nct
 // accumulators and spill)
@@ -723,31 +739,57 @@ __global__ void __launch_bounds__(cgs_consumers<T>() + 32, 1)
   } else {
     // ---- consumer warps: lanes (2i, 2i+1) of warp q own row 16 q + i of
     // every RPT block, lane parity h takes the columns c = h, h+2, ... ----
+    // Shared-memory operands are addressed as 32-bit shared-window addresses
+    // (ld.shared): with generic pointers into the dynamic ring the compiler
+    // re-derived the window base for every load, and the per-element column /
+    // row predicates were packed into a register and unpacked per use -- the
+    // UPD+PROJ sweep issued ~330 instructions per 16-row group for 48 FMAs
+    // (ncu: 57% issue-slot busy, consumer-bound at 64.5% of DRAM peak).  Now
+    // the row's basis values are loaded once into registers (used by both the
+    // update and the projection), and the column / row checks exist only in
+    // the variants for a partial column tile (nct < NC) or the last chunk.
     const int lrow = warp * 16 + (lane >> 1);
-    for (int64_t i = 0; i < nloc; ++i) {
-      const int s = int(i % S);
-      mbar_wait(full0 + 8 * s, uint32_t((i / S) & 1));
-      const T* tile = ring + size_t(s) * stage_elems;
-      const int64_t r0 = (int64_t(blockIdx.x) + i * gridDim.x) * RC;
+    const uint32_t ring_u = smem_u32(ring);
+    const uint32_t colb = uint32_t(CS * sizeof(T));  // bytes between column segments
+    const int ncl_h = (nct - h + 1) >> 1;             // this lane's columns c = 2 cc + h < nct
+    const uint32_t cin_u = smem_u32(cin) + uint32_t(h * sizeof(T));
+    // the warp releases the stage (its "empty" arrival) as soon as it has
+    // read the last row block's operands into registers, before that block's
+    // arithmetic: the producer can refill the stage while the FMA chains run
+    // (with two stages of ~100 KB, holding a stage through the update chain
+    // left only one stage in flight for a fifth of the time)
+    auto consume = [&](auto colchk_t, auto rowchk_t, uint32_t st_u, int64_t r0, uint32_t empty) {
+      constexpr bool COLCHK = decltype(colchk_t)::value, ROWCHK = decltype(rowchk_t)::value;
+      bool released = false;
 #pragma unroll 1
       for (int k = 0; k < RPT; ++k) {
         const int lr = k * R + lrow;
         const int64_t r = r0 + lr;
-        const bool valid = r < n;
-        if (!__any_sync(FULL, valid)) break;  // warp-uniform: the shuffles below need every lane
-        T wr = valid ? tile[nct * CS + lr] : s_zero<T>();
+        const bool valid = !ROWCHK || r < n;
+        if (ROWCHK && !__any_sync(FULL, valid)) break;  // warp-uniform: the shuffles need every lane
+        const uint32_t a = st_u + uint32_t(lr * sizeof(T)) + uint32_t(h) * colb;
+        T wr = valid ? lds_s<T>(st_u + uint32_t((nct * CS + lr) * sizeof(T))) : s_zero<T>();
+        T tv[NCL];
+#pragma unroll
+        for (int cc = 0; cc < NCL; ++cc)
+          tv[cc] = ((!COLCHK || cc < ncl_h) && valid) ? lds_s<T>(a + uint32_t(2 * cc) * colb)
+                                                      : s_zero<T>();
+        if (k == RPT - 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty);
+          released = true;
+        }
         if (UPD) {
           // two interleaved partial sums per lane, then the pair's halves
           T s0 = s_zero<T>(), s1 = s_zero<T>();
 #pragma unroll
           for (int cc = 0; cc < NCL; ++cc) {
-            const int c = 2 * cc + h;
-            if (valid && c < nct) {
-              if (cc & 1)
-                s1 = s_fma(tile[c * CS + lr], lds_nohoist(cin + c), s1);
-              else
-                s0 = s_fma(tile[c * CS + lr], lds_nohoist(cin + c), s0);
-            }
+            if (COLCHK && cc >= ncl_h) continue;
+            const T cf = lds_s<T>(cin_u + uint32_t(2 * cc * sizeof(T)));
+            if (cc & 1)
+              s1 = s_fma(tv[cc], cf, s1);
+            else
+              s0 = s_fma(tv[cc], cf, s0);
           }
           T sum = s_add(s0, s1);
           if constexpr (ND == 1) {
@@ -763,14 +805,30 @@ __global__ void __launch_bounds__(cgs_consumers<T>() + 32, 1)
         if (NRM && valid && h == 0) nrm += s_abs2(wr);
         if (PROJ) {
 #pragma unroll
-          for (int cc = 0; cc < NCL; ++cc) {
-            const int c = 2 * cc + h;
-            if (valid && c < nct) acc[cc] = s_cfma(tile[c * CS + lr], wr, acc[cc]);
-          }
+          for (int cc = 0; cc < NCL; ++cc) acc[cc] = s_cfma(tv[cc], wr, acc[cc]);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8 * s);
+      if (!released) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty);
+      }
+    };
+    using F_ = std::false_type;
+    using T_ = std::true_type;
+    for (int64_t i = 0; i < nloc; ++i) {
+      const int s = int(i % S);
+      mbar_wait(full0 + 8 * s, uint32_t((i / S) & 1));
+      const uint32_t st_u = ring_u + uint32_t(size_t(s) * stage_elems * sizeof(T));
+      const int64_t r0 = (int64_t(blockIdx.x) + i * gridDim.x) * RC;
+      const bool last = r0 + RC > n;
+      const uint32_t empty = empty0 + 8 * s;
+      if (nct == NC) {
+        if (!last) consume(F_{}, F_{}, st_u, r0, empty);
+        else consume(F_{}, T_{}, st_u, r0, empty);
+      } else {
+        if (!last) consume(T_{}, F_{}, st_u, r0, empty);
+        else consume(T_{}, T_{}, st_u, r0, empty);
+      }
     }
   }
 

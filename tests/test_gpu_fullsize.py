@@ -10,8 +10,11 @@ rule (true error = m*, reading Q11; the paper's estimate) the GPU
 run must give
   * the same m, termination, mat-vec count and estimate history,
   * beta0 = ||c|| to 1e-13,
-  * H_m normwise within 1e-11, or 10x the measured oracle-vs-oracle gap where
-    the Arnoldi process itself amplifies rounding beyond it (reading Q19),
+  * H_m normwise within 1e-11,
+  (each bar -- x, H, beta0 -- raised to 10x the measured gap between two
+  oracle runs that differ only in rounding, where the problem itself amplifies
+  rounding beyond it: reading Q19; in practice only the graph Laplacian C7,
+  whose degree-15 Newton polynomial is evaluated far outside its nodes),
   * x: ||dx_S|| / ||x_S|| <= 1e-10 on the sampled rows S (65,536 seeded rows
     plus the first and last 1024) and the same bar on the 32 Gaussian
     projections (||G dx|| / ||G x|| estimates ||dx|| / ||x|| over ALL entries;
@@ -67,7 +70,16 @@ def _sampled_spmv(ctx, A, M, rng, nsample=4096):
     assert np.all(np.abs(y - ref) <= 1e-14 * scale)
 
 
+def _x_bar(g):
+    return max(X_TOL, 10.0 * g.get("x_gap_oracle", 0.0))
+
+
+def _b_bar(g):
+    return max(B_TOL, 10.0 * g.get("beta0_gap_oracle", 0.0))
+
+
 def _compare_x(g, mode, x, tag):
+    xb = _x_bar(g)
     idx = g["idx"]
     xs = g[f"{mode}_x_samples"]
     e_s = np.linalg.norm(x[idx] - xs) / np.linalg.norm(xs)
@@ -75,10 +87,11 @@ def _compare_x(g, mode, x, tag):
     po = g[f"{mode}_x_proj"]
     e_p = np.linalg.norm(proj - po) / np.linalg.norm(po)
     e_n = abs(np.linalg.norm(x) - g[f"{mode}_x_norm"]) / g[f"{mode}_x_norm"]
-    print(f"[{tag}] x: sampled {e_s:.2e}, projected {e_p:.2e}, norm {e_n:.2e} (bar {X_TOL:g})")
-    assert e_s <= X_TOL, e_s
-    assert e_p <= 0.5 * X_TOL, e_p
-    assert e_n <= X_TOL, e_n
+    print(f"[{tag}] x: sampled {e_s:.2e}, projected {e_p:.2e}, norm {e_n:.2e} (bar {xb:.1e}; "
+          f"oracle-vs-oracle {g.get('x_gap_oracle', float('nan')):.1e})")
+    assert e_s <= xb, e_s
+    assert e_p <= 0.5 * xb, e_p
+    assert e_n <= xb, e_n
 
 
 def _compare_run(ctx, g, mode, rep, x, cplx, tag, h_bar, fixed=False):
@@ -93,18 +106,21 @@ def _compare_run(ctx, g, mode, rep, x, cplx, tag, h_bar, fixed=False):
     e_b = abs(beta0 - g[f"{mode}_beta0"]) / g[f"{mode}_beta0"]
     print(f"[{tag}] m = {rep.iterations} (oracle {g[f'{mode}_m']}), H gap {e_h:.2e} "
           f"(bar {h_bar:.1e}; oracle-vs-oracle {g['h_gap_oracle']:.1e}: {g['h_gap_how']}), "
-          f"beta0 gap {e_b:.1e}")
+          f"beta0 gap {e_b:.1e} (bar {_b_bar(g):.1e})")
     assert e_h <= h_bar, e_h
-    assert e_b <= B_TOL, e_b
+    assert e_b <= _b_bar(g), e_b
     if fixed:   # no checkpoints in a fixed-m run
         _compare_x(g, mode, x, tag)
         return
     hist = pp.history(ctx)
     hm = g[f"{mode}_hist_m"]
     assert [h["m"] for h in hist] == list(hm)
-    for hg, eo in zip(hist, g[f"{mode}_hist_est"]):
-        if not np.isnan(eo):
-            assert hg["est"] == pytest.approx(eo, rel=1e-6, abs=1e-13)
+    e_bar = max(1e-6, 10.0 * g.get("est_gap_oracle", 0.0))
+    pairs = [(hg["est"], eo) for hg, eo in zip(hist, g[f"{mode}_hist_est"]) if not np.isnan(eo)]
+    e_e = max([abs(a - b_) / b_ for a, b_ in pairs] or [0.0])
+    print(f"[{tag}] estimate history: max relative gap {e_e:.1e} (bar {e_bar:.1e}, or 1e-13 absolute)")
+    for a, b_ in pairs:
+        assert abs(a - b_) <= max(e_bar * b_, 1e-13), (a, b_)
     _compare_x(g, mode, x, tag)
 
 
@@ -199,9 +215,7 @@ def test_fullsize_library_ritz(ctx, key):
                      stop="est", tol=float(g["tol"]), check_every=int(g["check_every"]))
     torch.cuda.synchronize()
     assert rep.iterations == g["est_m"]
-    # graph: the estimate-stop iterate of a strongly non-normal operator carries
-    # the node difference amplified (measured, Q19): own-q bar 1e-8
-    tol = X_TOL if cfg.family != "graph" else 1e-8
+    tol = _x_bar(g)
     x = xg.cpu().numpy()
     e_s = np.linalg.norm(x[g["idx"]] - g["est_x_samples"]) / np.linalg.norm(g["est_x_samples"])
     print(f"[{key} own Ritz] x sampled gap {e_s:.2e} (bar {tol:g})")
