@@ -1283,6 +1283,207 @@ static void cgs_go(int64_t n, const T* V, int64_t ldv, int nct, T* w, const T* c
   post_launch("cgs_kernel");
 }
 
+// ---------------------------------------------------------------------------
+// "Flat" CGS2 sweeps for operators whose tiled sweeps are launch- and
+// latency-bound (n of a few 10^5 rows or less: a 24-column tile launch then
+// covers at most a few chunks per SM, and a step at j ~ 75 issued up to 16
+// launches).  ONE launch per sweep over ALL columns: each block walks row
+// blocks of FLAT_RB rows (grid-stride); the update (UPD) is one thread per row
+// summing over the columns in column order (8 loads in flight, 4 interleaved
+// partial sums); the projection (PROJ) is one warp per column (columns
+// c = warp, warp + 8, ...), lanes over the row block's rows (coalesced),
+// accumulated per block in shared memory; the updated w of the row block is
+// shared through shared memory, so UPD+PROJ is one pass (the row block's V
+// rows are re-read from L1/L2).  Per-block partials, the last block to arrive
+// sums them in block order, one thread per value.
+// ---------------------------------------------------------------------------
+constexpr int FLAT_THREADS = 256;
+constexpr int FLAT_RB = FLAT_THREADS;
+
+// In the last block: sum partials[b * stride + i] over b = 0..nb-1 (nb <=
+// 32 * FLAT_NBL) for each i in [0, nv).  Each warp takes FLAT_VPW values at a
+// time; every lane first loads its blocks b = lane + 32 k of all of them (all
+// loads in flight at once -- a loop of dependent adds would pay one L2
+// latency per block), adds them in k order, then the warp tree; fixed order.
+constexpr int FLAT_NBL = 10, FLAT_VPW = 4;
+template <typename F>
+__device__ __forceinline__ void reduce_partials_wide(const double* partials, int nb, int stride,
+                                                     int nv, F f) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i0 = w * FLAT_VPW; i0 < nv; i0 += nw * FLAT_VPW) {
+    double t[FLAT_NBL][FLAT_VPW];
+#pragma unroll
+    for (int kk = 0; kk < FLAT_NBL; ++kk)
+#pragma unroll
+      for (int v = 0; v < FLAT_VPW; ++v) {
+        const int b = lane + 32 * kk;
+        t[kk][v] = (b < nb && i0 + v < nv) ? __ldcg(partials + int64_t(b) * stride + i0 + v) : 0.0;
+      }
+#pragma unroll
+    for (int v = 0; v < FLAT_VPW; ++v) {
+      double s = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < FLAT_NBL; ++kk) s += t[kk][v];
+      s = warp_sum(s);
+      if (lane == 0 && i0 + v < nv) f(i0 + v, s);
+    }
+  }
+}
+
+template <typename T, int FL>
+__global__ void __launch_bounds__(FLAT_THREADS) cgs_flat_kernel(
+    int64_t n, const T* __restrict__ V, int64_t ldv, int ncols, T* __restrict__ w,
+    const T* __restrict__ coef_in, T* __restrict__ coef_out, T* __restrict__ Hcol,
+    T* __restrict__ Hsub, double* __restrict__ inv, double* partials, unsigned* counter,
+    double* raw) {
+  constexpr int ND = n_doubles<T>();
+  constexpr bool UPD = FL & F_UPD, PROJ = FL & F_PROJ, NRM = FL & F_NRM;
+  constexpr int NW = FLAT_THREADS / 32;
+  extern __shared__ __align__(16) unsigned char flat_smem[];
+  T* cs = reinterpret_cast<T*>(flat_smem);                      // ncols coefficients (UPD)
+  double* bacc = reinterpret_cast<double*>(cs + ncols);          // ncols x ND block sums (PROJ)
+  __shared__ T wsh[FLAT_RB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int c = tid; c < ncols; c += FLAT_THREADS) {
+    if (UPD) cs[c] = coef_in[c];
+    if (PROJ)
+      for (int d = 0; d < ND; ++d) bacc[c * ND + d] = 0.0;
+  }
+  __syncthreads();
+  double nrm = 0.0;
+  for (int64_t r0 = int64_t(blockIdx.x) * FLAT_RB; r0 < n; r0 += int64_t(gridDim.x) * FLAT_RB) {
+    const int64_t r = r0 + tid;
+    const bool valid = r < n;
+    T wr = valid ? w[r] : s_zero<T>();
+    if (UPD) {
+      T s0 = s_zero<T>(), s1 = s_zero<T>(), s2 = s_zero<T>(), s3 = s_zero<T>();
+      if (valid) {
+        const T* vr = V + r;
+        int c = 0;
+        for (; c + 8 <= ncols; c += 8) {
+          T v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = ldg(vr + int64_t(c + u) * ldv);
+          s0 = s_fma(v[0], cs[c], s0);
+          s1 = s_fma(v[1], cs[c + 1], s1);
+          s2 = s_fma(v[2], cs[c + 2], s2);
+          s3 = s_fma(v[3], cs[c + 3], s3);
+          s0 = s_fma(v[4], cs[c + 4], s0);
+          s1 = s_fma(v[5], cs[c + 5], s1);
+          s2 = s_fma(v[6], cs[c + 6], s2);
+          s3 = s_fma(v[7], cs[c + 7], s3);
+        }
+        for (; c < ncols; ++c) s0 = s_fma(ldg(vr + int64_t(c) * ldv), cs[c], s0);
+      }
+      wr = s_sub(wr, s_add(s_add(s0, s1), s_add(s2, s3)));
+      if (valid) w[r] = wr;
+      if (NRM) nrm += s_abs2(wr);
+    }
+    if (PROJ) {
+      wsh[tid] = wr;
+      __syncthreads();
+      // FLAT_CPW columns per warp at a time (c = warp + NW q), all their loads
+      // in flight together, then the warp trees interleaved
+      constexpr int CPW = 4;
+      for (int cb = warp; cb < ncols; cb += NW * CPW) {
+        T s[CPW];
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) s[q] = s_zero<T>();
+#pragma unroll
+        for (int kk = 0; kk < FLAT_RB / 32; ++kk) {
+          const int i = kk * 32 + lane;
+          const bool ok = r0 + i < n;
+          const T wi = wsh[i];
+#pragma unroll
+          for (int q = 0; q < CPW; ++q) {
+            const int c = cb + q * NW;
+            if (ok && c < ncols) s[q] = s_cfma(ldg(V + int64_t(c) * ldv + r0 + i), wi, s[q]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < CPW; ++q) {
+          const int c = cb + q * NW;
+          const double* a = reinterpret_cast<const double*>(&s[q]);
+#pragma unroll
+          for (int d = 0; d < ND; ++d) {
+            const double v = warp_sum(a[d]);
+            if (lane == 0 && c < ncols) bacc[c * ND + d] += v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (PROJ) {
+    for (int q = tid; q < ncols * ND; q += FLAT_THREADS)
+      partials[int64_t(blockIdx.x) * ncols * ND + q] = bacc[q];
+  }
+  if (NRM) {
+    __shared__ double smn[32];
+    const double v = block_sum(nrm, smn);
+    if (tid == 0) partials[blockIdx.x] = v;
+  }
+  if (last_block(counter)) {
+    if (PROJ) {
+      reduce_partials_wide(partials, gridDim.x, ncols * ND, ncols * ND, [&](int q, double v) {
+        if (raw) {
+          raw[q] = v;
+          return;
+        }
+        reinterpret_cast<double*>(coef_out)[q] = v;
+        if (Hcol) reinterpret_cast<double*>(Hcol)[q] = reinterpret_cast<const double*>(coef_in)[q] + v;
+      });
+    }
+    if (NRM) {
+      reduce_partials_wide(partials, gridDim.x, 1, 1, [&](int, double v) {
+        if (raw) {
+          raw[0] = v;
+          return;
+        }
+        const double nr = sqrt(v);
+        double* hs = reinterpret_cast<double*>(Hsub);
+        hs[0] = nr;
+        if (ND == 2) hs[1] = 0.0;
+        inv[0] = 1.0 / nr;
+      });
+    }
+    __syncthreads();
+    if (tid == 0) *counter = 0;
+  }
+}
+
+// rows below which the flat sweeps replace the tiled TMA ones (per rank):
+// ~2 chunks of a full 24-column tile per SM
+static bool cgs_use_flat(int64_t n, int num_sms_cap, int ncols, int tile) {
+  // PPF_CGS_FLAT=1 / 0 forces the flat / tiled sweeps (tests; read per call)
+  const char* e = std::getenv("PPF_CGS_FLAT");
+  const int force = e ? (e[0] == '1' ? 1 : 0) : -1;
+  if (force >= 0) return force == 1;
+  // (one tile: the tiled sweeps already need only one launch each)
+  return ncols > tile && n < int64_t(2) * 512 * (num_sms_cap / 8);
+}
+
+template <typename T>
+static int cgs_flat(int mode, int64_t n, const T* V, int64_t ldv, int ncols, T* w, const T* ci,
+                    T* co, T* hc, T* hs, double* inv, RedScratch& rs, int grid, cudaStream_t st) {
+  constexpr int ND = n_doubles<T>();
+  // two blocks per SM at most: the per-block partials (ncols x ND each) and
+  // the tail sum stay short
+  const int blocks = blocks_for(n, FLAT_RB, grid);
+  const size_t smem = size_t(ncols) * (sizeof(T) + ND * sizeof(double));
+  if (mode == 0)
+    cgs_flat_kernel<T, F_PROJ><<<blocks, FLAT_THREADS, smem, st>>>(
+        n, V, ldv, ncols, w, nullptr, co, nullptr, nullptr, nullptr, rs.partials, rs.counter, rs.raw);
+  else if (mode == 1)
+    cgs_flat_kernel<T, F_UPD | F_PROJ><<<blocks, FLAT_THREADS, smem, st>>>(
+        n, V, ldv, ncols, w, ci, co, hc, nullptr, nullptr, rs.partials, rs.counter, rs.raw);
+  else
+    cgs_flat_kernel<T, F_UPD | F_NRM><<<blocks, FLAT_THREADS, smem, st>>>(
+        n, V, ldv, ncols, w, ci, nullptr, nullptr, hs, inv, rs.partials, rs.counter, rs.raw);
+  post_launch("cgs_flat_kernel");
+  return 1;
+}
+
 // column tile width per launch: 24 (two stages of 25 x 4 KB column segments
 // fit in shared memory, cgs_rpt), fp64 and complex
 template <typename T> constexpr int cgs_tile() { return 24; }
@@ -1316,6 +1517,8 @@ static int cgs_dispatch(int mode, int64_t n, const void* Vv, int64_t ldv, int nc
   auto hc = static_cast<T*>(hcv);
   auto hs = static_cast<T*>(hsv);
   int launches = 0;
+  if (cgs_use_flat(n, rs.max_blocks, ncols, TILE))
+    return cgs_flat<T>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, rs.max_blocks / 4, st);
   if (ncols <= TILE) {
     if (mode == 0)
       cgs_nc<T, F_PROJ>(n, V, ldv, ncols, w, nullptr, co, nullptr, nullptr, nullptr, rs, grid, st);
