@@ -158,13 +158,17 @@ def compute(key: str, log=print) -> dict:
     x2 = r2.x.real if (not np.iscomplexobj(b) and np.iscomplexobj(r2.x)) else r2.x
     xs = out[f"{mode}_x_samples"]
     out["x_gap_oracle"] = float(np.linalg.norm(x2[idx] - xs) / np.linalg.norm(xs))
+    p1, p2 = out[f"{mode}_x_proj"], probe_projections(x2, PROBE_K, PROBE_SEED)
+    out["x_proj_gap_oracle"] = float(np.linalg.norm(p2 - p1) / np.linalg.norm(p1))
+    out["x_norm_gap_oracle"] = float(abs(np.linalg.norm(x2) - out[f"{mode}_x_norm"]) /
+                                     out[f"{mode}_x_norm"])
     out["beta0_gap_oracle"] = float(abs(r2.beta0 - out[f"{mode}_beta0"]) / out[f"{mode}_beta0"])
     e1 = {int(mm_): e for mm_, e in zip(out[f"{mode}_hist_m"], out[f"{mode}_hist_est"])}
     gaps = [abs(h["est"] - e1[h["m"]]) / e1[h["m"]] for h in r2.history
             if h["est"] is not None and h["m"] in e1 and not np.isnan(e1[h["m"]])]
     out["est_gap_oracle"] = float(max(gaps)) if gaps else 0.0
     log(f"{key}: oracle-vs-oracle H gap ({how}) {out['h_gap_oracle']:.3e}, "
-        f"x gap {out['x_gap_oracle']:.3e}, beta0 gap {out['beta0_gap_oracle']:.3e}, "
+        f"x gap {out['x_gap_oracle']:.3e} (projected {out['x_proj_gap_oracle']:.3e}), beta0 gap {out['beta0_gap_oracle']:.3e}, "
         f"estimate gap {out['est_gap_oracle']:.3e} "
         f"({time.perf_counter() - t0:.1f} s)")
     return out

@@ -79,7 +79,15 @@ def _b_bar(g):
 
 
 def _compare_x(g, mode, x, tag):
+    # each measure against its own oracle-vs-oracle gap (C7: the entries the
+    # rounding moves most are the few of largest magnitude, which the sample
+    # rarely contains but the projections and the norm weigh fully)
     xb = _x_bar(g)
+    # (the projections estimate ||dx|| within a chi-square spread: against the
+    # absolute 1e-10 bar they are held to half of it; against a measured
+    # oracle-vs-oracle gap, taken through the same projections, to 10x it)
+    xb_p = max(0.5 * X_TOL, 10.0 * g.get("x_proj_gap_oracle", 0.0))
+    xb_n = max(X_TOL, 10.0 * g.get("x_norm_gap_oracle", 0.0))
     idx = g["idx"]
     xs = g[f"{mode}_x_samples"]
     e_s = np.linalg.norm(x[idx] - xs) / np.linalg.norm(xs)
@@ -87,11 +95,13 @@ def _compare_x(g, mode, x, tag):
     po = g[f"{mode}_x_proj"]
     e_p = np.linalg.norm(proj - po) / np.linalg.norm(po)
     e_n = abs(np.linalg.norm(x) - g[f"{mode}_x_norm"]) / g[f"{mode}_x_norm"]
-    print(f"[{tag}] x: sampled {e_s:.2e}, projected {e_p:.2e}, norm {e_n:.2e} (bar {xb:.1e}; "
-          f"oracle-vs-oracle {g.get('x_gap_oracle', float('nan')):.1e})")
+    print(f"[{tag}] x: sampled {e_s:.2e} (bar {xb:.1e}), projected {e_p:.2e} (bar {xb_p:.1e}), "
+          f"norm {e_n:.2e} (bar {xb_n:.1e}); oracle-vs-oracle sampled "
+          f"{g.get('x_gap_oracle', float('nan')):.1e}, projected "
+          f"{g.get('x_proj_gap_oracle', float('nan')):.1e}")
     assert e_s <= xb, e_s
-    assert e_p <= 0.5 * xb, e_p
-    assert e_n <= xb, e_n
+    assert e_p <= xb_p, e_p
+    assert e_n <= xb_n, e_n
 
 
 def _compare_run(ctx, g, mode, rep, x, cplx, tag, h_bar, fixed=False):
