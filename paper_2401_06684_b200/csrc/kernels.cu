@@ -363,13 +363,18 @@ __global__ void __launch_bounds__(256) csr_kernel(int64_t n, const int64_t* __re
 }
 
 // halo: out[rows[i]] += s_ax * sum val * recv[col]
+// recv_sel (peer memory): the receive slot is chosen on the device, slot
+// (*recv_sel & 1) at recv + slot * slot_elems -- so a captured graph replays
+// correctly whatever the exchange count
 template <typename T>
 __global__ void halo_apply_kernel(int64_t nrows, const int32_t* __restrict__ rows,
                                   const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                                   const T* __restrict__ val, const T* __restrict__ recv,
-                                  T* __restrict__ out, T s_ax) {
+                                  T* __restrict__ out, T s_ax, const unsigned* recv_sel,
+                                  int64_t slot_elems) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
+  if (recv_sel) recv += int64_t(*reinterpret_cast<const volatile unsigned*>(recv_sel) & 1u) * slot_elems;
   T acc = s_zero<T>();
   for (int64_t k = rp[i]; k < rp[i + 1]; ++k) acc = s_fma(ldg(val + k), ldg(recv + col[k]), acc);
   const int64_t r = rows[i];
@@ -1163,7 +1168,7 @@ void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st) {
 }
 
 void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st,
-                       const void* recv) {
+                       const void* recv, const unsigned* recv_sel) {
   if (A->halo_rows == 0) return;
   if (!recv) recv = A->d_recv;
   const int blocks = int((A->halo_rows + 255) / 256);
@@ -1171,12 +1176,12 @@ void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t s
     halo_apply_kernel<double><<<blocks, 256, 0, st>>>(
         A->halo_rows, A->d_halo_rows, A->d_halo_ptr, A->d_halo_col,
         static_cast<const double*>(A->d_halo_val), static_cast<const double*>(recv),
-        static_cast<double*>(out), s_ax[0]);
+        static_cast<double*>(out), s_ax[0], recv_sel, A->halo_total);
   else
     halo_apply_kernel<cplx><<<blocks, 256, 0, st>>>(
         A->halo_rows, A->d_halo_rows, A->d_halo_ptr, A->d_halo_col,
         static_cast<const cplx*>(A->d_halo_val), static_cast<const cplx*>(recv),
-        static_cast<cplx*>(out), cplx{s_ax[0], s_ax[1]});
+        static_cast<cplx*>(out), cplx{s_ax[0], s_ax[1]}, recv_sel, A->halo_total);
   post_launch("halo_apply_kernel");
 }
 

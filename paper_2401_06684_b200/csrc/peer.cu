@@ -4,28 +4,33 @@
 // NCCL launch latency"; include/ppf.h: ppf_mat_peer_window / _connect).
 //
 // Window of rank r (cudaMalloc, exported with CUDA IPC; byte offsets):
-//   OFF_READY_H  u32[p]  halo arrivals from sender p: +1 per push of p into r
-//   OFF_FREED_H  u32[q]  +1 per push of receiver q ("I consumed epoch E-1")
+//   OFF_READY_H  u32[p]  semaphore: pushes of sender p into r not yet consumed
+//   OFF_FREED_H  u32[q]  semaphore: free receive slots of receiver q for r's
+//                        pushes (starts at 2: the receive slots are double-buffered)
 //   OFF_READY_R  u32     reduction arrivals: +1 per peer partial stored into r
 //   OFF_BLK      u32  last-block ticket of r's own push kernel (local only)
+//   OFF_XCOUNT   u32  halo exchanges r has completed (local only); slot = parity
 //   OFF_RED      2 slots x nranks x RCAP doubles (slot E&1, row = source rank)
-//   halo_off     2 slots x halo_total scalars (slot E&1; per-peer segments at
+//   halo_off     2 slots x halo_total scalars (slot XCOUNT&1; per-peer segments at
 //                r's recv_off, the same layout as the NCCL receive buffer)
-// Epochs are counted per matrix from 1 and advance identically on every rank
-// because every rank issues the same exchanges in the same order.
+// Every rank issues the same exchanges in the same order, so the sender's and
+// the receiver's exchange counts -- and with them the slot parity -- agree.
 //
-// Halo exchange E on rank r (one per sharded SpMV):
-//   stream:  [ev_pack] ...... diag-block SpMV .. wait ev_halo, wait READY_H[p] >= E (each sender p) .. halo block
-//   comm:    wait ev_pack, wait FREED_H[q] >= E-1 (each receiver q), push kernel [ev_halo]
-// The push kernel stores x[send_idx] into each receiver's slot E&1 (NVLink
-// stores), then -- after every block's __threadfence_system() -- its last block
-// adds 1 to READY_H[r] of each receiver and to FREED_H[r] of each rank that
-// sends to r.  The counters are per peer: neighbours are not all-to-all, so a
-// fast neighbour can run an epoch ahead of a slow one and an aggregate count
-// could be reached with one epoch's data missing.  Receiver slot reuse: slot
-// E&1 was last filled at epoch E-2; a receiver signals "consumed E-2" with its
-// own push of epoch E-1, which its stream orders after its halo block of E-2,
-// hence the FREED_H wait above.
+// Halo exchange on rank r (one per sharded SpMV), all comparison values FIXED
+// (semaphores instead of epochs), so a captured CUDA graph of the step's
+// SpMV chain replays correctly (round 2):
+//   stream:  [ev_pack] .. diag-block SpMV .. wait ev_halo, wait READY_H[p] >= 1 (each sender p)
+//            .. halo block (slot XCOUNT&1) .. consume kernel
+//   comm:    wait ev_pack, wait FREED_H[q] >= 1 (each receiver q), push kernel [ev_halo]
+// The push kernel stores x[send_idx] into each receiver's slot XCOUNT&1
+// (NVLink stores); its last block, after every block's __threadfence_system(),
+// takes one slot from each FREED_H[q] and adds 1 to READY_H[r] of each
+// receiver.  The consume kernel (after the halo block read the slot) gives the
+// arrivals back (READY_H[p] -= 1), returns the slot to each sender (+1 on
+// FREED_H[r] in its window) and advances XCOUNT.  The counters are per peer:
+// neighbours are not all-to-all, so a fast neighbour can run an exchange ahead
+// of a slow one and an aggregate count could be met with one exchange's data
+// missing.
 //
 // Reduction E (allreduce of the rank-local partial sums a reduction kernel left
 // in RedScratch::raw): one block stores raw into slot E&1 / row r of every
@@ -57,6 +62,7 @@ namespace {
 
 constexpr size_t OFF_READY_H = 0, OFF_FREED_H = 4 * PPF_PEER_MAX_RANKS;
 constexpr size_t OFF_READY_R = 8 * PPF_PEER_MAX_RANKS, OFF_BLK = OFF_READY_R + 64;
+constexpr size_t OFF_XCOUNT = OFF_BLK + 64;
 constexpr size_t OFF_RED = 1024;
 // reduction row: up to (m_max + 1) complex coefficients (m_max <= 1024) + slack
 constexpr int RCAP = 2 * (1024 + 2) + 16;
@@ -166,8 +172,9 @@ void preload_module(const void* sym) {
 template <typename T>
 __global__ void __launch_bounds__(256) peer_push_kernel(
     const T* __restrict__ x, const int32_t* __restrict__ idx, const PushEnt* __restrict__ ent,
-    int nent, int64_t total, int slot, unsigned* const* __restrict__ sig, int nready, int nsig,
+    int nent, int64_t total, const unsigned* xcount, unsigned* const* __restrict__ sig, int nto,
     unsigned* blk) {
+  const int slot = int(*reinterpret_cast<const volatile unsigned*>(xcount) & 1u);
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
     int e = 0;
@@ -181,14 +188,25 @@ __global__ void __launch_bounds__(256) peer_push_kernel(
     if (atomicAdd(blk, 1u) == gridDim.x - 1) {
       *blk = 0;  // the next push is stream-ordered after this one
       __threadfence_system();
-      // "consumed" signals first, then (after a fence) the arrivals: a rank
-      // that has seen this push arrive has also received every signal of it,
-      // so once its run is over no write of ours is still headed for its
-      // window (it may free the window at teardown)
-      for (int k = nready; k < nsig; ++k) atomicAdd_system(sig[k], 1u);
-      __threadfence_system();
-      for (int k = 0; k < nready; ++k) atomicAdd_system(sig[k], 1u);
+      // sig[0, nto): READY_H[r] in each receiver's window; sig[nto, 2 nto):
+      // this rank's FREED_H[q] of the same receivers (a slot now in use)
+      for (int k = 0; k < nto; ++k) atomicSub(sig[nto + k], 1u);
+      for (int k = 0; k < nto; ++k) atomicAdd_system(sig[k], 1u);
     }
+  }
+}
+
+// after the halo block read the receive slot: the arrivals are consumed
+// (READY_H[p] -= 1, this rank's window), the slot goes back to every sender
+// (FREED_H[r] += 1 in its window), the exchange count advances
+__global__ void peer_consume_kernel(unsigned* const* __restrict__ sig, int nfrom,
+                                    unsigned* xcount) {
+  if (threadIdx.x == 0) {
+    // sig[0, nfrom): own READY_H[p]; sig[nfrom, 2 nfrom): FREED_H[r] at each sender p
+    for (int k = 0; k < nfrom; ++k) atomicSub(sig[k], 1u);
+    __threadfence_system();
+    for (int k = 0; k < nfrom; ++k) atomicAdd_system(sig[nfrom + k], 1u);
+    *xcount += 1u;
   }
 }
 
@@ -233,7 +251,8 @@ struct PeerState {
   // device tables: push entries, push signals, reduction destinations + signals
   void* d_tab = nullptr;
   PushEnt* d_ent = nullptr;
-  unsigned** d_push_sig = nullptr;
+  unsigned** d_push_sig = nullptr;   // push: READY_H at receivers, own FREED_H
+  unsigned** d_cons_sig = nullptr;   // consume: own READY_H, FREED_H at senders
   double** d_red_dst = nullptr;
   unsigned** d_red_sig = nullptr;
   int nent = 0, n_to = 0, n_from = 0, push_blocks = 1;
@@ -251,9 +270,9 @@ void peer_destroy(PeerState* p) {
   // freeing the window under it (all ranks run the same exchanges).
   if (p->connected && p->halo_epoch > 0) {
     const auto t0 = std::chrono::steady_clock::now();
-    for (unsigned* f : p->wait_freed) {
+    for (unsigned* f : p->wait_freed) {   // both slots back from every receiver
       uint32_t v = 0;
-      while (cudaMemcpy(&v, f, 4, cudaMemcpyDeviceToHost) == cudaSuccess && v < p->halo_epoch &&
+      while (cudaMemcpy(&v, f, 4, cudaMemcpyDeviceToHost) == cudaSuccess && v < 2u &&
              std::chrono::steady_clock::now() - t0 < std::chrono::seconds(10))
         std::this_thread::sleep_for(std::chrono::milliseconds(1));
     }
@@ -283,39 +302,46 @@ static void ensure_comm_objects(ppf_ctx* ctx) {
 }
 
 // comm stream: push this rank's boundary entries of x into the receivers
-void peer_halo_begin(ppf_ctx* ctx, ppf_mat* A, const void* x) {
+// (`st`: the stream the SpMV runs on -- the context's, or a capture stream)
+void peer_halo_begin(ppf_ctx* ctx, ppf_mat* A, const void* x, cudaStream_t st) {
   PeerState* P = A->peer;
-  cudaStream_t st = ctx->stream, cs = ctx->comm_stream;
-  const uint32_t E = ++P->halo_epoch;
+  cudaStream_t cs = ctx->comm_stream;
+  ++P->halo_epoch;  // host count (teardown only)
   PPF_CUDA(cudaEventRecord(ctx->ev_pack, st));
   PPF_CUDA(cudaStreamWaitEvent(cs, ctx->ev_pack, 0));
-  if (E > 1)
-    for (unsigned* f : P->wait_freed) stream_wait_geq(cs, f, E - 1);
-  const int slot = int(E & 1u);
+  for (unsigned* f : P->wait_freed) stream_wait_geq(cs, f, 1u);
   unsigned* blk = reinterpret_cast<unsigned*>(P->win + OFF_BLK);
-  const int nsig = P->n_to + P->n_from;
+  const unsigned* xc = reinterpret_cast<const unsigned*>(P->win + OFF_XCOUNT);
   if (A->dtype == PPF_R64)
     peer_push_kernel<double><<<P->push_blocks, 256, 0, cs>>>(
-        static_cast<const double*>(x), A->d_send_idx, P->d_ent, P->nent, A->send_total, slot,
-        P->d_push_sig, P->n_to, nsig, blk);
+        static_cast<const double*>(x), A->d_send_idx, P->d_ent, P->nent, A->send_total, xc,
+        P->d_push_sig, P->n_to, blk);
   else
     peer_push_kernel<double2><<<P->push_blocks, 256, 0, cs>>>(
-        static_cast<const double2*>(x), A->d_send_idx, P->d_ent, P->nent, A->send_total, slot,
-        P->d_push_sig, P->n_to, nsig, blk);
+        static_cast<const double2*>(x), A->d_send_idx, P->d_ent, P->nent, A->send_total, xc,
+        P->d_push_sig, P->n_to, blk);
   check_launch("peer_push_kernel");
   PPF_CUDA(cudaEventRecord(ctx->ev_halo, cs));
 }
 
-// compute stream: this rank's push has read x, every sender's entries have
-// arrived; returns the receive slot of this epoch for the halo block
-const void* peer_halo_wait(ppf_ctx* ctx, ppf_mat* A) {
+// stream `st`: this rank's push has read x, every sender's entries have
+// arrived; returns the receive slots' base (the halo block picks slot
+// XCOUNT&1 on the device through *sel)
+const void* peer_halo_wait(ppf_ctx* ctx, ppf_mat* A, cudaStream_t st, const unsigned** sel) {
   PeerState* P = A->peer;
-  cudaStream_t st = ctx->stream;
-  const uint32_t E = P->halo_epoch;
   PPF_CUDA(cudaStreamWaitEvent(st, ctx->ev_halo, 0));
-  for (unsigned* f : P->wait_ready) stream_wait_geq(st, f, E);
-  const size_t sc = A->dtype == PPF_R64 ? 8 : 16;
-  return P->win + P->hoff + size_t(E & 1u) * size_t(A->halo_total) * sc;
+  for (unsigned* f : P->wait_ready) stream_wait_geq(st, f, 1u);
+  *sel = reinterpret_cast<const unsigned*>(P->win + OFF_XCOUNT);
+  return P->win + P->hoff;
+}
+
+// stream `st`, after the halo block: arrivals consumed, slots returned
+void peer_halo_done(ppf_ctx* ctx, ppf_mat* A, cudaStream_t st) {
+  (void)ctx;
+  PeerState* P = A->peer;
+  peer_consume_kernel<<<1, 32, 0, st>>>(P->d_cons_sig, P->n_from,
+                                        reinterpret_cast<unsigned*>(P->win + OFF_XCOUNT));
+  check_launch("peer_consume_kernel");
 }
 
 // allreduce(sum) of raw[0:nv] over the ranks, deterministic (rank order)
@@ -450,22 +476,31 @@ ppf_status ppf_mat_peer_connect(ppf_mat* A, const void* descs) {
   // push entries (receivers in peer order = this rank's send-list order) and
   // signal targets: READY_H of each receiver, then FREED_H of each sender
   std::vector<PushEnt> ent;
-  std::vector<unsigned*> psig;
+  std::vector<unsigned*> psig, pown, csig, cown;
   for (int q = 0; q < R; ++q)
     if (q != me && A->send_count[q]) {
       const size_t qh = halo_off(R);
       ent.push_back({P->peer[q] + qh + size_t(D[q].recv_off[me]) * sc,
                      int64_t(D[q].halo_total) * int64_t(sc), A->send_off[q], A->send_count[q]});
       psig.push_back(reinterpret_cast<unsigned*>(P->peer[q] + OFF_READY_H) + me);
+      pown.push_back(reinterpret_cast<unsigned*>(P->win + OFF_FREED_H) + q);
       P->wait_freed.push_back(reinterpret_cast<unsigned*>(P->win + OFF_FREED_H) + q);
     }
   P->n_to = int(ent.size());
   for (int q = 0; q < R; ++q)
     if (q != me && A->recv_count[q]) {
-      psig.push_back(reinterpret_cast<unsigned*>(P->peer[q] + OFF_FREED_H) + me);
+      cown.push_back(reinterpret_cast<unsigned*>(P->win + OFF_READY_H) + q);
+      csig.push_back(reinterpret_cast<unsigned*>(P->peer[q] + OFF_FREED_H) + me);
       P->wait_ready.push_back(reinterpret_cast<unsigned*>(P->win + OFF_READY_H) + q);
     }
-  P->n_from = int(psig.size()) - P->n_to;
+  P->n_from = int(cown.size());
+  psig.insert(psig.end(), pown.begin(), pown.end());
+  cown.insert(cown.end(), csig.begin(), csig.end());
+  // both receive slots of every receiver start free
+  {
+    std::vector<unsigned> two(size_t(R), 2u);
+    PPF_CUDA(cudaMemcpy(P->win + OFF_FREED_H, two.data(), size_t(R) * 4, cudaMemcpyHostToDevice));
+  }
   P->nent = int(ent.size());
   if (ent.empty()) ent.push_back({nullptr, 0, 0, 0});
   std::vector<double*> rdst(R);
@@ -475,14 +510,18 @@ ppf_status ppf_mat_peer_connect(ppf_mat* A, const void* descs) {
     if (q != me) rsig.push_back(reinterpret_cast<unsigned*>(P->peer[q] + OFF_READY_R));
   }
   const size_t b_ent = ent.size() * sizeof(PushEnt), b_ps = (psig.size() + 1) * sizeof(void*),
-               b_rd = rdst.size() * sizeof(void*), b_rs = (rsig.size() + 1) * sizeof(void*);
+               b_rd = rdst.size() * sizeof(void*), b_rs = (rsig.size() + 1) * sizeof(void*),
+               b_cs = (cown.size() + 1) * sizeof(void*);
   if (P->d_tab) PPF_CUDA(cudaFree(P->d_tab));
-  PPF_CUDA(cudaMalloc(&P->d_tab, b_ent + b_ps + b_rd + b_rs));
+  PPF_CUDA(cudaMalloc(&P->d_tab, b_ent + b_ps + b_rd + b_rs + b_cs));
   char* t = static_cast<char*>(P->d_tab);
   P->d_ent = reinterpret_cast<PushEnt*>(t);
   P->d_push_sig = reinterpret_cast<unsigned**>(t + b_ent);
   P->d_red_dst = reinterpret_cast<double**>(t + b_ent + b_ps);
   P->d_red_sig = reinterpret_cast<unsigned**>(t + b_ent + b_ps + b_rd);
+  P->d_cons_sig = reinterpret_cast<unsigned**>(t + b_ent + b_ps + b_rd + b_rs);
+  if (!cown.empty())
+    PPF_CUDA(cudaMemcpy(P->d_cons_sig, cown.data(), cown.size() * sizeof(void*), cudaMemcpyHostToDevice));
   PPF_CUDA(cudaMemcpy(P->d_ent, ent.data(), b_ent, cudaMemcpyHostToDevice));
   if (!psig.empty())
     PPF_CUDA(cudaMemcpy(P->d_push_sig, psig.data(), psig.size() * sizeof(void*), cudaMemcpyHostToDevice));

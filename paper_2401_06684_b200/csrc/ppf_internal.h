@@ -275,7 +275,7 @@ void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
 void launch_acc(ppf_mat* A, const void* x, const void* out, const Epi& e, cudaStream_t st);
 // recv: the receive buffer to read (null: A->d_recv)
 void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st,
-                       const void* recv = nullptr);
+                       const void* recv = nullptr, const unsigned* recv_sel = nullptr);
 const void* kernels_module_symbol();
 // peer.cu: the peer-memory exchange (ppf_mat_peer_window / _connect)
 void peer_destroy(PeerState* p);
@@ -284,11 +284,14 @@ bool peer_active(const ppf_mat* A);
 // module loading a first launch waits for the device, which a rank blocked in
 // a collective or a peer wait would turn into a cross-rank stall
 void preload_kernels();
-void peer_halo_begin(ppf_ctx* ctx, ppf_mat* A, const void* x);
-const void* peer_halo_wait(ppf_ctx* ctx, ppf_mat* A);
+void peer_halo_begin(ppf_ctx* ctx, ppf_mat* A, const void* x, cudaStream_t st);
+// returns the receive slots' base; *sel = the device word whose parity picks the slot
+const void* peer_halo_wait(ppf_ctx* ctx, ppf_mat* A, cudaStream_t st, const unsigned** sel);
+void peer_halo_done(ppf_ctx* ctx, ppf_mat* A, cudaStream_t st);
 void peer_allreduce(ppf_ctx* ctx, ppf_mat* A, double* raw, int nv, cudaStream_t st);
 // run.cpp: the sharded SpMV with communication/compute overlap
-void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e);
+void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e,
+               cudaStream_t st = nullptr);
 bool poly_fits(const ppf_poly* q, ppf_dtype dt);
 
 struct RedScratch {   // reduction scratch (device)

@@ -193,17 +193,22 @@ static void halo_transport(ppf_ctx* ctx, ppf_mat* A, const void* x) {
   PPF_CUDA(cudaStreamSynchronize(st));  // the staging is reused by the next call
 }
 
-void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e) {
-  cudaStream_t st = ctx->stream;
+void halo_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* out, const Epi& e,
+               cudaStream_t st_in) {
+  // st_in: the stream of the caller's SpMV sequence (a capture stream while the
+  // step's chain is recorded as a CUDA graph), else the context's
+  cudaStream_t st = st_in ? st_in : ctx->stream;
   if (peer_active(A)) {
     // peer memory (peer.cu): push on the comm stream || diagonal block here
     const bool comm = A->send_total || A->halo_total;
-    if (comm) peer_halo_begin(ctx, A, x);
+    if (comm) peer_halo_begin(ctx, A, x, st);
     Epi ed = e;
     ed.acc = nullptr;
     launch_spmv(A, x, out, ed, st);
-    const void* recv = comm ? peer_halo_wait(ctx, A) : nullptr;
-    if (A->halo_rows) launch_halo_apply(A, out, e.s_ax, st, recv);
+    const unsigned* sel = nullptr;
+    const void* recv = comm ? peer_halo_wait(ctx, A, st, &sel) : nullptr;
+    if (A->halo_rows) launch_halo_apply(A, out, e.s_ax, st, recv, sel);
+    if (comm) peer_halo_done(ctx, A, st);
     if (e.acc) launch_acc(A, x, out, e, st);
     return;
   }
@@ -396,8 +401,9 @@ struct Runner {
     if (A->nranks > 1) {
       // pack + overlapped exchange + diagonal block + halo block; timed as one
       // unit (its device time includes any exposed communication)
-      launches += (A->send_total ? 1 : 0) + (A->halo_rows ? 1 : 0);
-      timed(0, bytes, [&] { halo_spmv(ctx, A, x, out, e); });
+      launches += (A->send_total ? 1 : 0) + (A->halo_rows ? 1 : 0) +
+                  ((peer_active(A) && (A->send_total || A->halo_total)) ? 1 : 0);
+      timed(0, bytes, [&] { halo_spmv(ctx, A, x, out, e, st); });
       return;
     }
     timed(0, bytes, [&] { launch_spmv(A, x, out, e, st); });
@@ -835,8 +841,12 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
   // graph Laplacian, Table 1's 100^3: C2 deg 20 6.7 -> 4.7 ms) and still trim
   // the inter-kernel gaps at C3/C4 (-0.4..0.6%)
   const bool big = double(A->stored) * double(R.sc + 4) >= 256e6;
+  // sharded: the chain's halo exchanges over peer memory are capturable
+  // (fixed-value semaphores, peer.cu); the NCCL and host-transport paths
+  // launch directly (NCCL's own capture support is not exercised here: the
+  // one-GPU tests run NCCL through a stand-in that is not graph-safe)
   R.use_graph = (ws_shape(q, o) & WS_GRAPH) && ctx->use_graphs && !ctx->profile &&
-                A->nranks == 1;
+                (A->nranks == 1 || (peer_active(A) && !ctx->has_transport));
   const int64_t n = R.n;
   const size_t vb = size_t(n) * R.sc;
   double t_dense = 0.0;
@@ -1368,7 +1378,8 @@ extern "C" ppf_status ppf_spmv(ppf_ctx* ctx, ppf_mat* A, const void* x, void* y)
     e.s_ax[0] = 1.0;
     if (A->nranks > 1) {
       ppf::halo_spmv(ctx, A, x, y, e);
-      ctx->launches += 1 + (A->send_total ? 1 : 0) + (A->halo_rows ? 1 : 0);
+      ctx->launches += 1 + (A->send_total ? 1 : 0) + (A->halo_rows ? 1 : 0) +
+                       ((ppf::peer_active(A) && (A->send_total || A->halo_total)) ? 1 : 0);
       return PPF_OK;
     }
     ppf::launch_spmv(A, x, y, e, ctx->stream);

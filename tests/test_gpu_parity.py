@@ -362,7 +362,11 @@ def test_c5_small_library_ritz(ctx):
     xg, rep = pp.run(ctx, M, q, bd, func="invsqrt", krylov="cgs2", m_max=cfg.m_max,
                      stop="true", tol=cfg.tol, x_ref=dev(xr))
     assert rep.iterations == res_o.m
-    assert np.linalg.norm(host(xg) - res_o.x) <= 1e-8 * np.linalg.norm(res_o.x)
+    # own q on each side: the nodes differ at ~1e-11 (F6), the iterate only at
+    # rounding level -- held to the north_star bar
+    e_x = np.linalg.norm(host(xg) - res_o.x) / np.linalg.norm(res_o.x)
+    print(f"C5s own-Ritz x gap {e_x:.2e} (bar {X_TOL:g})")
+    assert e_x <= X_TOL
 
 
 def test_run_host_matches_device(ctx):
