@@ -56,7 +56,7 @@ def _slab_bounds(cfg, n, world):
     return [c * per for c in cuts]
 
 
-def _worker(rank, world, port, case, out_path, q_path, fake_lib):
+def _worker(rank, world, port, case, out_path, q_path, fake_lib, graphs=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -84,6 +84,7 @@ def _worker(rank, world, port, case, out_path, q_path, fake_lib):
         ctx = pp.Context(0, rank=rank, nranks=world, nccl_id=idl[0])
     else:
         ctx = pp.Context(0, rank=rank, nranks=world)
+    ctx.set_graphs(graphs)
 
     def exchange(send, scount, recv, rcount):
         ops, so, ro = [], 0, 0
@@ -209,3 +210,32 @@ def test_two_rank_run_matches_oracle(case, transport, request):
     ms_r = [int(v) for v in ms[0::2]]
     assert len(ms_r) == world and all(v == res.m for v in ms_r)   # every rank, the oracle's m
     assert np.linalg.norm(x - res.x) <= X_TOL * np.linalg.norm(res.x)
+
+
+@pytest.mark.parametrize("case", ["c4s_cgs2_sqrt", "c3s_lanczos", "c7s_graph_basis", "c5s_ritz"])
+def test_peer_ipc_graph_replay_bitwise(case):
+    """Peer memory between processes (CUDA IPC windows): the sharded step's
+    q(A)q(A) chain captured once as a CUDA graph -- push kernels, stream waits
+    on the peer semaphores, halo blocks, consume kernels (peer.cu) -- and
+    replayed every step gives bitwise the run of direct launches, at the
+    oracle's m on every rank.  (Ranks emulated as threads of ONE process cannot
+    host such graphs: their graphs' internal streams share hardware queues, so
+    a wait node of one rank can sit in front of the push of another -- the
+    one-process tests in test_gpu_peer.py launch directly.)"""
+    import torch.multiprocessing as mp
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    cfg, A, b, iv, qo, res = oracle_case(case)
+    world = WORLD.get(case, 2)
+    got = {}
+    with tempfile.TemporaryDirectory() as td:
+        q_path = os.path.join(td, "q.npy")
+        if cfg.poly == "ritz":
+            np.save(q_path, np.stack([qo.nodes, qo.dd]))
+        for g in (True, False):
+            out = os.path.join(td, f"x{int(g)}.npy")
+            mp.spawn(_worker, args=(world, _free_port(), case, out, q_path, "peer", g), nprocs=world,
+                     join=True)
+            got[g] = (np.load(out), open(out + ".m").read().split())
+    assert np.array_equal(got[True][0], got[False][0])
+    assert got[True][1] == got[False][1]
+    assert all(int(v) == res.m for v in got[True][1][0::2])

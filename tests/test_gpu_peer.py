@@ -95,16 +95,22 @@ def _run_threads(fn, ranks, timeout=240):
         t.join(timeout)
         if t.is_alive():
             print("a rank did not finish (peer exchange stalled)", flush=True)
+            for r, e in enumerate(errs):   # a rank that failed leaves the others waiting
+                if e is not None:
+                    print(f"rank {r} failed: {e!r}", flush=True)
             os._exit(3)   # tear the context down instead of hanging
     for e in errs:
         if e is not None:
             raise e
 
 
-def child_run(case, q_path, out_path, world=None, graphs=True):
-    """Child process: the case on `world` emulated ranks with peer memory
-    (graphs: the step's q(A)q(A) chain, halo exchanges included, replayed as
-    a captured CUDA graph -- ppf_ctx_set_graphs -- or launched directly)."""
+def child_run(case, q_path, out_path, world=None, graphs=False):
+    """Child process: the case on `world` emulated ranks with peer memory,
+    launched directly (graphs=False): ranks emulated as threads of one process
+    cannot replay captured graphs whose stream waits depend on each other --
+    the graphs' internal streams share hardware queues, so one rank's wait node
+    can block another rank's push (measured: a stall).  The graph path is
+    tested between processes (test_gpu_multirank.py::test_peer_ipc_graph_replay_bitwise)."""
     import paper_2401_06684_b200 as pp
     name, deg, kw = CASES[case]
     cfg = configs.CONFIGS[name]
@@ -207,30 +213,6 @@ def test_peer_ranks_match_oracle(case, world, tmp_path):
         per = [float(np.linalg.norm((o["x"] - res.x)[lo:hi]) / np.linalg.norm(res.x[lo:hi]))
                for lo, hi in zip(bounds[:-1], bounds[1:])]
         pytest.fail(f"x rel. error {err:.3g}; per slab {per}")
-
-
-@pytest.mark.parametrize("case,world", [("c4s_cgs2_sqrt", 3), ("c3s_lanczos", 8),
-                                        ("c7s_graph_basis", 2)])
-def test_peer_graph_replay_bitwise(case, world, tmp_path):
-    """The sharded step's chain captured once as a CUDA graph (push kernels,
-    stream waits on the peer semaphores, halo blocks, consume kernels) and
-    replayed every step gives bitwise the run of direct launches: the
-    semaphores' fixed comparison values and the device-side slot parity make
-    the graph independent of the exchange count."""
-    assert torch.cuda.is_available(), "GPU tests need a B200"
-    cfg, A, b, iv, qo, res = oracle_case(case)
-    q_path = str(tmp_path / "q.npy")
-    if cfg.poly == "ritz":
-        np.save(q_path, np.stack([qo.nodes, qo.dd]))
-    outs = {}
-    for g in (True, False):
-        out = str(tmp_path / f"out{int(g)}.npz")
-        _child(f"child_run({case!r}, {q_path!r}, {out!r}, {world}, graphs={g})")
-        outs[g] = np.load(out)
-    assert np.array_equal(outs[True]["x"], outs[False]["x"])
-    assert np.array_equal(outs[True]["H"], outs[False]["H"])
-    assert [int(m) for m in outs[True]["m"]] == [int(m) for m in outs[False]["m"]] == \
-        [res.m] * world
 
 
 def test_peer_spmv_many_epochs(tmp_path):
