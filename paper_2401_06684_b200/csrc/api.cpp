@@ -199,6 +199,7 @@ void ppf_ctx_destroy(ppf_ctx* c) {
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->t_host) cudaFreeHost(c->t_host);
   if (c->ev) cudaEventDestroy(c->ev);
+  if (c->res_ctl) cudaFreeHost(c->res_ctl);
   if (c->ev_t0) cudaEventDestroy(c->ev_t0);
   if (c->ev_t1) cudaEventDestroy(c->ev_t1);
   if (c->ev_pack) cudaEventDestroy(c->ev_pack);

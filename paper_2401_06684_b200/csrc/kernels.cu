@@ -12,6 +12,7 @@
 // Reductions are deterministic: per-block partials, then the last block to
 // arrive sums them in block order (fixed tree), independent of timing.
 #include <atomic>
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -1591,6 +1592,255 @@ void launch_lanczos(ppf_dtype dt, int phase, int64_t n, const void* v, const voi
   }
 #undef PPF_LZ
   post_launch("lanczos_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Resident step loop (small operators, round 2).  For an
+// operator one CTA can hold (n <= RES_MAX_ROWS, SELL-32), launching ~5 kernels
+// and synchronising with the host at every step costs far more than the
+// arithmetic (C1: 1024 rows, 9 SpMVs of 5k entries per step took ~62 us).  One
+// CTA of 1024 threads runs the steps back to back: the plain SpMV v_j -> U,
+// the recorded q(A)q(A) chain (U -> W2, the same epilogues as the graph
+// replays), the orthogonalisation (Lanczos or CGS2) writing v_{j+1} and the
+// H column -- and after each step stores the H column into a mapped host
+// block and bumps a step counter (after __threadfence_system).  The host polls
+// the counter, evaluates f(H_m) and the estimate as in the launched path, and
+// either lets the device run on (at most RES_AHEAD steps past the last step it
+// has decided) or raises `stop`; steps run past the stop are discarded.
+// Block-scope coherence: every vector is written and read by this one CTA
+// (one SM), so plain loads after __syncthreads() see the writes.
+// ---------------------------------------------------------------------------
+template <typename T> struct ResCallT {
+  const T* x;
+  T* out;
+  EpiT<T> e;
+  int has_x;
+};
+
+template <typename T>
+__device__ void res_spmv(int64_t n, const int64_t* __restrict__ sptr, const int32_t* __restrict__ col,
+                         const T* __restrict__ val, const T* x, T* out, const EpiT<T>& e,
+                         bool has_x) {
+  for (int64_t row = threadIdx.x; row < n; row += blockDim.x) {
+    const int64_t base = sptr[row >> 5];
+    const int w = int((sptr[(row >> 5) + 1] - base) >> 5);
+    const int lane = int(row & 31);
+    T acc = s_zero<T>();
+    for (int k = 0; k < w; ++k) acc = s_fma(ldg(val + base + 32 * k + lane), x[__ldg(col + base + 32 * k + lane)], acc);
+    T r = s_mul(e.s_ax, acc);
+    if (has_x) r = s_fma(e.s_x, e.xe[row], r);
+    if (e.z) r = s_fma(e.s_z, e.z[row], r);
+    if (e.u) r = s_fma(e.s_u, e.u[row], r);
+    out[row] = r;
+    if (e.acc) {
+      const T b0 = e.acc_init ? s_mul(e.s_acc0, e.xe[row]) : e.acc[row];
+      e.acc[row] = s_fma(e.s_acc, r, b0);
+    }
+  }
+}
+
+// block-wide sum of a T (one per thread), fixed order; every thread gets it
+template <typename T>
+__device__ __forceinline__ T res_block_sum(T v, double* sm) {
+  constexpr int ND = n_doubles<T>();
+  double* a = reinterpret_cast<double*>(&v);
+  T out;
+  double* o = reinterpret_cast<double*>(&out);
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    o[d] = block_sum(a[d], sm);
+    __syncthreads();
+    if (threadIdx.x == 0) sm[32] = o[d];
+    __syncthreads();
+    o[d] = sm[32];
+    __syncthreads();
+  }
+  return out;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) resident_steps_kernel(
+    int64_t n, const int64_t* __restrict__ sptr, const int32_t* __restrict__ col,
+    const T* __restrict__ val, T* V, int64_t ldv, T* U, T* W, T* H, int ldh, int m_max,
+    int lanczos, const double* beta0_dev, ResCtl* ctl, const ResCallT<T>* calls_host, int ncalls,
+    int ahead) {
+  constexpr int ND = n_doubles<T>();
+  extern __shared__ __align__(16) unsigned char res_smem[];
+  ResCallT<T>* calls = reinterpret_cast<ResCallT<T>*>(res_smem);
+  T* coef = reinterpret_cast<T*>(res_smem + size_t(ncalls) * sizeof(ResCallT<T>));  // 2 (m_max+1)
+  __shared__ double sm[33];
+  __shared__ int s_go;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < ncalls * int(sizeof(ResCallT<T>) / 8); i += blockDim.x)
+    reinterpret_cast<uint64_t*>(calls)[i] = reinterpret_cast<const volatile uint64_t*>(calls_host)[i];
+  if (tid == 0) ctl->beta0 = *beta0_dev;
+  __syncthreads();
+  const EpiT<T> plain{s_from<T>(1.0, 0.0), s_zero<T>(), s_zero<T>(), s_zero<T>(), nullptr, nullptr,
+                      nullptr, nullptr, s_zero<T>(), s_zero<T>(), false};
+  T beta_prev = s_zero<T>();
+  double* Hmap = ctl->H;
+  for (int j = 0; j < m_max; ++j) {
+    if (tid == 0) {
+      // soft throttle: wait for the host to catch up to RES_AHEAD steps, but
+      // never longer than RES_WAIT_NS -- a host that cannot answer (a tool
+      // that serialises the launch, e.g. a profiler replaying the kernel)
+      // must not stall the device: it then runs on to m_max, bounded work
+      int go = 1;
+      uint64_t t0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        if (*reinterpret_cast<volatile int*>(&ctl->stop)) {
+          go = 0;
+          break;
+        }
+        if (j < *reinterpret_cast<volatile int*>(&ctl->acked) + ahead) break;
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > RES_WAIT_NS) break;
+        __nanosleep(500);
+      }
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) break;
+    T* vj = V + int64_t(j) * ldv;
+    T* vn = V + int64_t(j + 1) * ldv;
+    // u = A v_j, then the chain U -> ... -> W
+    res_spmv(n, sptr, col, val, vj, U, plain, false);
+    for (int c = 0; c < ncalls; ++c) {
+      __syncthreads();
+      const ResCallT<T>& cl = calls[c];
+      res_spmv(n, sptr, col, val, cl.x, cl.out, cl.e, cl.has_x != 0);
+    }
+    __syncthreads();
+    if (lanczos) {
+      const T* vp = j > 0 ? V + int64_t(j - 1) * ldv : nullptr;
+      T part = s_zero<T>();
+      for (int64_t i = tid; i < n; i += blockDim.x) {
+        T wi = W[i];
+        if (vp) wi = s_sub(wi, s_mul(beta_prev, vp[i]));
+        W[i] = wi;
+        part = s_cfma(vj[i], wi, part);
+      }
+      const T alpha = res_block_sum(part, sm);
+      double nr = 0.0;
+      for (int64_t i = tid; i < n; i += blockDim.x) {
+        const T wi = s_sub(W[i], s_mul(alpha, vj[i]));
+        W[i] = wi;
+        nr += s_abs2(wi);
+      }
+      const double beta = sqrt(res_block_sum<double>(nr, sm));
+      __syncthreads();
+      const double inv = 1.0 / beta;
+      for (int64_t i = tid; i < n; i += blockDim.x) vn[i] = s_scale(W[i], inv);
+      if (tid == 0) {
+        H[j + size_t(j) * ldh] = alpha;
+        H[j + 1 + size_t(j) * ldh] = s_from<T>(beta, 0.0);
+        if (j + 1 < m_max + 1) H[j + size_t(j + 1) * ldh] = s_from<T>(beta, 0.0);
+      }
+      beta_prev = s_from<T>(beta, 0.0);
+    } else {
+      // CGS2: h = V^H w; w -= V h; g = V^H w; w -= V g; H(0:j, j) = h + g
+      const int nc = j + 1, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+      for (int pass = 0; pass < 2; ++pass) {
+        T* cf = coef + pass * (m_max + 1);
+        for (int c = warp; c < nc; c += nw) {
+          const T* vc = V + int64_t(c) * ldv;
+          T s = s_zero<T>();
+          for (int64_t i = lane; i < n; i += 32) s = s_cfma(vc[i], W[i], s);
+          double* a = reinterpret_cast<double*>(&s);
+#pragma unroll
+          for (int d = 0; d < ND; ++d) a[d] = warp_sum(a[d]);
+          if (lane == 0) cf[c] = s;
+        }
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += blockDim.x) {
+          T s = s_zero<T>();
+          for (int c = 0; c < nc; ++c) s = s_fma(V[int64_t(c) * ldv + i], cf[c], s);
+          W[i] = s_sub(W[i], s);
+        }
+        __syncthreads();
+      }
+      double nr = 0.0;
+      for (int64_t i = tid; i < n; i += blockDim.x) nr += s_abs2(W[i]);
+      const double beta = sqrt(res_block_sum<double>(nr, sm));
+      __syncthreads();
+      const double inv = 1.0 / beta;
+      for (int64_t i = tid; i < n; i += blockDim.x) vn[i] = s_scale(W[i], inv);
+      for (int c = tid; c < nc; c += blockDim.x) H[c + size_t(j) * ldh] = s_add(coef[c], coef[m_max + 1 + c]);
+      if (tid == 0) H[j + 1 + size_t(j) * ldh] = s_from<T>(beta, 0.0);
+    }
+    __syncthreads();
+    // column j (rows 0..j+1) to the host, then the step count
+    for (int r = tid; r <= j + 1; r += blockDim.x) {
+      const double* hv = reinterpret_cast<const double*>(&H[r + size_t(j) * ldh]);
+#pragma unroll
+      for (int d = 0; d < ND; ++d) Hmap[(size_t(r) + size_t(j) * ldh) * ND + d] = hv[d];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) *reinterpret_cast<volatile int*>(&ctl->done) = j + 1;
+  }
+}
+
+int resident_max_rows() { return RES_MAX_ROWS; }
+
+// eligible layouts: one rank, SELL-32 without sorting
+bool resident_fits(const ppf_mat* A) {
+  return A->nranks == 1 && A->fmt == PPF_FMT_SELL && A->C == 32 && A->d_perm == nullptr &&
+         A->n_local <= RES_MAX_ROWS;
+}
+
+size_t resident_call_bytes(ppf_dtype dt) {
+  return dt == PPF_R64 ? sizeof(ResCallT<double>) : sizeof(ResCallT<cplx>);
+}
+
+// write the recorded chain (x, out, epilogue per SpMV) into `dst` (host)
+void resident_pack_calls(ppf_dtype dt, const std::vector<ResCallSpec>& spec, void* dst) {
+  for (size_t i = 0; i < spec.size(); ++i) {
+    if (dt == PPF_R64) {
+      ResCallT<double> c;
+      std::memset(&c, 0, sizeof(c));
+      c.x = static_cast<const double*>(spec[i].x);
+      c.out = static_cast<double*>(spec[i].out);
+      c.e = to_epi<double>(spec[i].e, spec[i].x);
+      c.has_x = (spec[i].e.s_x[0] != 0.0 || spec[i].e.s_x[1] != 0.0) ? 1 : 0;
+      std::memcpy(static_cast<char*>(dst) + i * sizeof(c), &c, sizeof(c));
+    } else {
+      ResCallT<cplx> c;
+      std::memset(&c, 0, sizeof(c));
+      c.x = static_cast<const cplx*>(spec[i].x);
+      c.out = static_cast<cplx*>(spec[i].out);
+      c.e = to_epi<cplx>(spec[i].e, spec[i].x);
+      c.has_x = (spec[i].e.s_x[0] != 0.0 || spec[i].e.s_x[1] != 0.0) ? 1 : 0;
+      std::memcpy(static_cast<char*>(dst) + i * sizeof(c), &c, sizeof(c));
+    }
+  }
+}
+
+void launch_resident(ppf_mat* A, void* V, int64_t ldv, void* U, void* W, void* H, int ldh,
+                     int m_max, int lanczos, const double* beta0_dev, ResCtl* ctl_dev,
+                     const void* calls_dev, int ncalls, int ahead, cudaStream_t st) {
+  const size_t cb = resident_call_bytes(A->dtype);
+  const size_t sc = A->dtype == PPF_R64 ? 8 : 16;
+  const size_t smem = size_t(ncalls) * cb + 2 * size_t(m_max + 1) * sc;
+#define PPF_RES(T)                                                                              \
+  {                                                                                             \
+    auto kfn = resident_steps_kernel<T>;                                                        \
+    if (smem > 48 * 1024)                                                                       \
+      cuda_check(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                      int(smem)), "cudaFuncSetAttribute(resident)");           \
+    kfn<<<1, 1024, smem, st>>>(A->n_local, A->d_ptr, A->d_col, static_cast<const T*>(A->d_val), \
+                               static_cast<T*>(V), ldv, static_cast<T*>(U), static_cast<T*>(W), \
+                               static_cast<T*>(H), ldh, m_max, lanczos, beta0_dev, ctl_dev,     \
+                               static_cast<const ResCallT<T>*>(calls_dev), ncalls, ahead);      \
+  }
+  if (A->dtype == PPF_R64)
+    PPF_RES(double)
+  else
+    PPF_RES(cplx)
+#undef PPF_RES
+  post_launch("resident_steps_kernel");
 }
 
 // a kernel of this translation unit (its module is force-loaded by peer.cu)

@@ -197,6 +197,8 @@ struct ppf_ctx {
   size_t h_pinned_bytes;
   cudaEvent_t ev;
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // timing events: ppf_report.seconds_device
+  void* res_ctl = nullptr;     // mapped pinned control block of the resident step loop
+  size_t res_ctl_bytes = 0;
   // last run
   std::vector<ppf::HistRec> hist;
   std::vector<double> lastH;  // (m+1) x m, n_doubles per entry, column-major ld = m+1
@@ -315,6 +317,29 @@ void launch_norm(ppf_dtype dt, int64_t n, const void* v, double* nrm_out, RedScr
 //   mode 0: coef_out[0:ncols] = V^H w
 //   mode 1: w -= V coef_in ; coef_out = V^H w ; H[:,j] = coef_in + coef_out
 //   mode 2: w -= V coef_in ; H[j+1,j] = ||w||, inv[0] = 1/||w||
+// resident step loop (kernels.cu): mapped host control block and the chain
+constexpr int RES_MAX_ROWS = 4096;
+constexpr int RES_AHEAD = 4;
+constexpr unsigned long long RES_WAIT_NS = 200000;  // the device's longest wait for the host
+struct ResCtl {
+  int stop;      // host -> device: stop before the next step
+  int acked;     // host -> device: steps the host has decided (the device runs <= RES_AHEAD past)
+  int done;      // device -> host: steps completed (H columns 0..done-1 written)
+  int pad;
+  double beta0;  // device -> host: ||c||
+  double H[1];   // device -> host: H columns, (ldh x (m_max+1)) scalars, column-major
+};
+struct ResCallSpec {
+  const void* x;
+  void* out;
+  Epi e;
+};
+bool resident_fits(const ppf_mat* A);
+size_t resident_call_bytes(ppf_dtype dt);
+void resident_pack_calls(ppf_dtype dt, const std::vector<ResCallSpec>& spec, void* dst);
+void launch_resident(ppf_mat* A, void* V, int64_t ldv, void* U, void* W, void* H, int ldh,
+                     int m_max, int lanczos, const double* beta0_dev, ResCtl* ctl_dev,
+                     const void* calls_dev, int ncalls, int ahead, cudaStream_t st);
 int launch_cgs(ppf_dtype dt, int mode, int64_t n, const void* V, int64_t ldv, int ncols, void* w,
                 const void* coef_in, void* coef_out, void* Hcol, void* Hsub, double* inv,
                 RedScratch& rs, int grid, cudaStream_t st);

@@ -11,6 +11,8 @@
 // true error) and at the end.  q(A) is the Clenshaw recurrence (P:332,
 // reading Q4) or the Newton-Horner scheme, each SpMV's epilogue
 // carrying the recurrence's vector updates.
+#include <atomic>
+#include <thread>
 #include <nccl.h>
 
 #include <algorithm>
@@ -998,6 +1000,128 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
     pend.pop_front();
     return stop;
   };
+  // Resident step loop (small operators; kernels.cu: resident_steps_kernel):
+  // one CTA runs the steps back to back while the host decides the
+  // checkpoints from H columns it reads out of a mapped block.
+  const bool resident = [&] {
+    const char* e = std::getenv("PPF_RESIDENT");
+    if (e && e[0] == '0') return false;
+    return resident_fits(A) && q && q->deg >= 1 && !right && !twopass && power == 1 &&
+           (o->stop == PPF_STOP_EST || o->stop == PPF_STOP_FIXED_M) && !ctx->profile;
+  }();
+  bool resident_done = false;
+  if (resident) {
+    // the step's q(A)q(A) chain, U -> Y -> W2, as recorded SpMV calls
+    std::vector<Runner::Call> chain;
+    R.rec = &chain;
+    R.apply_q(R.vec(R.L.U), R.vec(R.L.Y));
+    R.apply_q(R.vec(R.L.Y), R.vec(R.L.W2));
+    R.rec = nullptr;
+    bool ok = true;
+    std::vector<ResCallSpec> spec;
+    for (auto& c : chain) {
+      if (c.scale || c.graph) ok = false;
+      spec.push_back({c.x, c.out, c.e});
+    }
+    if (ok) {
+      const size_t cb = resident_call_bytes(R.dt);
+      const size_t hbytes = size_t(R.L.ldh) * size_t(m_max + 1) * R.sc;
+      const size_t calls_off = (sizeof(ResCtl) + hbytes + 255) & ~size_t(255);
+      const size_t need = calls_off + spec.size() * cb + 256;
+      if (ctx->res_ctl_bytes < need) {
+        PPF_CUDA(cudaStreamSynchronize(R.st));
+        if (ctx->res_ctl) PPF_CUDA(cudaFreeHost(ctx->res_ctl));
+        ctx->res_ctl = nullptr;
+        ctx->res_ctl_bytes = 0;
+        PPF_CUDA(cudaHostAlloc(&ctx->res_ctl, need, cudaHostAllocMapped));
+        ctx->res_ctl_bytes = need;
+      }
+      char* blk = static_cast<char*>(ctx->res_ctl);
+      void* blk_dev = nullptr;
+      PPF_CUDA(cudaHostGetDevicePointer(&blk_dev, blk, 0));
+      auto* ctl = reinterpret_cast<ResCtl*>(blk);
+      volatile int* v_stop = &ctl->stop;
+      volatile int* v_acked = &ctl->acked;
+      volatile int* v_done = &ctl->done;
+      *v_stop = 0;
+      *v_done = 0;
+      *v_acked = o->stop == PPF_STOP_FIXED_M ? m_max : 0;
+      resident_pack_calls(R.dt, spec, blk + calls_off);
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      R.timed(0, 0.0, [&] {
+        launch_resident(A, R.V(0), R.L.ldv, R.vec(R.L.U), R.vec(R.L.W2), R.Hp(0, 0), R.L.ldh,
+                        m_max, lanczos ? 1 : 0, R.scal(S_BETA0), reinterpret_cast<ResCtl*>(blk_dev),
+                        static_cast<char*>(blk_dev) + calls_off, int(spec.size()), RES_AHEAD, R.st);
+      });
+      const int nd = int(R.sc / 8);
+      if (o->stop == PPF_STOP_FIXED_M) {
+        m = m_max;
+      } else {
+        int decided = 0;
+        bool stopped = false;
+        while (!stopped && decided < m_max) {
+          const int d = *v_done;
+          std::atomic_thread_fence(std::memory_order_acquire);
+          if (d <= decided) {
+            // the kernel ended early only if it failed: report, do not spin
+            const cudaError_t qs = cudaStreamQuery(R.st);
+            if (qs != cudaErrorNotReady && *v_done <= decided) {
+              PPF_CUDA(qs);
+              fail(PPF_ECUDA, "resident step kernel ended before the host's decision");
+            }
+            std::this_thread::yield();
+            continue;
+          }
+          for (int mm = decided + 1; mm <= d && !stopped; ++mm) {
+            m = mm;
+            mvms = mvms_start + (long long)mm * per_step;
+            decided = mm;
+            if (!(mm % k == 0 || mm == m_max)) {
+              *v_acked = mm;
+              continue;
+            }
+            beta0 = ctl->beta0;
+            Hh.assign(size_t(mm + 1) * mm, zc(0.0, 0.0));
+            for (int jj = 0; jj < mm; ++jj)
+              for (int i = 0; i <= std::min(mm, jj + 1); ++i) {
+                const size_t oo = (size_t(i) + size_t(jj) * R.L.ldh) * nd;
+                Hh[size_t(i) + size_t(jj) * (mm + 1)] = zc(ctl->H[oo], nd == 2 ? ctl->H[oo + 1] : 0.0);
+              }
+            const double hsub = std::abs(Hh[size_t(mm) + size_t(mm - 1) * (mm + 1)]);
+            int mb = mm;
+            for (int jj = std::max(0, mm - k); jj < mm; ++jj)
+              if (std::abs(Hh[size_t(jj + 1) + size_t(jj) * (mm + 1)]) <= brt * beta0) {
+                mb = jj + 1;
+                break;
+              }
+            std::vector<zc> Hs = Hh;
+            if (mb != mm) {
+              std::vector<zc> H2(size_t(mb + 1) * mb);
+              for (int jj = 0; jj < mb; ++jj)
+                for (int i = 0; i <= mb; ++i) H2[size_t(i) + size_t(jj) * (mb + 1)] = Hh[size_t(i) + size_t(jj) * (mm + 1)];
+              Hs = H2;
+            }
+            auto td = std::chrono::steady_clock::now();
+            std::vector<zc> yy = dense_y(Hs, mb + 1, mb, beta0, lanczos);
+            t_dense += std::chrono::duration<double>(std::chrono::steady_clock::now() - td).count();
+            if (decide(mm, mb, hsub, mvms, yy)) {
+              m = mb;
+              y = std::move(yy);
+              stopped = true;
+              *v_stop = 1;
+              break;
+            }
+            *v_acked = mm;
+          }
+        }
+        if (!stopped) *v_stop = 1;
+      }
+      PPF_CUDA(cudaStreamSynchronize(R.st));
+      mvms = mvms_start + (long long)m * per_step;
+      resident_done = true;
+    }
+  }
+  if (!resident_done) {
   std::vector<Runner::Call> calls = R.record_step(0);
   size_t played = 0;
   for (int j = 0; j < m_max; ++j) {
@@ -1096,6 +1220,7 @@ ppf_status run_impl(ppf_ctx* ctx, ppf_mat* A, const ppf_poly* q, const ppf_opts*
       m = mb;
       break;
     }
+  }
   }
   // final H, y_m
   R.fetch_H(m + 1, m, Hh, beta0);
