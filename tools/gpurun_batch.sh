@@ -1,5 +1,7 @@
 python -c "import __graft_entry__ as g; g.build()"
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_c1_launches.csv python bench.py --config C1 --steps 2 --warmup 3 --no-cpu-baseline --no-profile > gpurun_out/r2_c1_ncu.log 2>&1; echo ncu=$?
-tail -3 gpurun_out/r2_c1_ncu.log
-timeout 300 python bench.py --config C1 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r2_c1.json 2>&1; python -c "import json;d=json.load(open('gpurun_out/r2_c1.json'));print('C1',round(d['value']*1e3,4),'ms m',d['config']['m'])"
-timeout 600 python -m pytest tests/test_gpu_resident.py -m gpu -q -p no:cacheprovider 2>&1 | tail -2
+( time timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf ) > gpurun_out/r2_gpu_suite2.log 2>&1; echo pytest_rc=$?
+tail -6 gpurun_out/r2_gpu_suite2.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()"; echo smoke_rc=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_smoke_launches.csv python -c "import __graft_entry__ as g; g.smoke()" > /dev/null 2>&1; echo ncu_smoke_rc=$?
+timeout 900 python bench.py > gpurun_out/r2_bench_default.json 2> gpurun_out/r2_bench_default.err; echo bench_rc=$?
+python -c "import json;d=json.load(open('gpurun_out/r2_bench_default.json'));print(d['value'],d['e2e']['value'],d['roofline']['frac'],d['cpu_baseline']['value'],d['clocks'])"
