@@ -12,7 +12,10 @@
 // Reductions are deterministic: per-block partials, then the last block to
 // arrive sums them in block order (fixed tree), independent of timing.
 #include <atomic>
+#include <set>
+#include <mutex>
 #include <cstring>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -1458,6 +1461,323 @@ __global__ void __launch_bounds__(FLAT_THREADS) cgs_flat_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// "Wide" CGS2 sweeps (round 2): ALL columns of V per stage, for bases wider
+// than one 24-column tile (C7: m = 114, C2 deg 5: m = 76).  A stage holds a
+// chunk of WIDE_R rows (512 B per column segment) of every column, fetched by
+// 2-D tensor-map bulk copies (boxes of WIDE_R rows x WIDE_CB columns, rows
+// past n and columns past ncols zero-filled by the copy engine) plus one 1-D
+// bulk copy of w; a producer warp keeps the ring full.  Consumers (8 warps):
+//   UPD   one thread per (row, quarter of the columns): lanes on consecutive
+//         rows of one column (conflict-free), the quarters added in order;
+//         the updated w goes back to the stage and to global memory;
+//   PROJ  one thread per column, accumulating over the whole sweep in a
+//         register; row order skewed by lane (row (i + lane) mod WIDE_R) so
+//         the 32 lanes of a warp hit distinct banks.
+// So every sweep is ONE launch reading V once, whatever the column count (the
+// tiled sweeps issue one launch per 24-column tile and the UPD+PROJ sweep two
+// passes); per-CTA partials, the last CTA sums them in CTA order.
+// ---------------------------------------------------------------------------
+constexpr int WIDE_CB = 32;                    // columns per tensor box
+constexpr int WIDE_THREADS = 256;              // consumer threads
+constexpr int WIDE_MAX_COLS = 192;
+// rows per chunk: SEG bytes per column segment (512 B or 1 KB -- longer
+// segments keep the DRAM row buffers busier; 1 KB when three stages still fit)
+template <typename T, int SEG> __host__ __device__ constexpr int wide_rows() { return SEG / int(sizeof(T)); }
+template <typename T, int SEG> __host__ __device__ inline int wide_stage_bytes(int ncols) {
+  const int ncp = (ncols + WIDE_CB - 1) / WIDE_CB * WIDE_CB;
+  return (ncp + 1) * SEG;
+}
+template <typename T, int SEG> __host__ __device__ inline int wide_stages(int ncols) {
+  int S = (CGS_SMEM - 32 * 8) / wide_stage_bytes<T, SEG>(ncols);
+  return S > 8 ? 8 : S;
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int c0, int c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(WIDE_THREADS) : "memory");
+}
+
+template <typename T, int FL, int SEG>
+__global__ void __launch_bounds__(WIDE_THREADS + 32, 1) cgs_wide_kernel(
+    const __grid_constant__ CUtensorMap tmV, int64_t n, int ncols, T* __restrict__ w,
+    const T* __restrict__ coef_in, T* __restrict__ coef_out, T* __restrict__ Hcol,
+    T* __restrict__ Hsub, double* __restrict__ inv, double* partials, unsigned* counter,
+    double* raw) {
+  constexpr int ND = n_doubles<T>();
+  constexpr int R = wide_rows<T, SEG>();
+  constexpr int DPE = int(sizeof(T)) / 8;   // doubles per element (tensor inner unit)
+  constexpr bool UPD = FL & F_UPD, PROJ = FL & F_PROJ, NRM = FL & F_NRM;
+  constexpr int NW = WIDE_THREADS / 32;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ T cin[WIDE_MAX_COLS];
+  __shared__ T part[WIDE_THREADS / R][R];
+  __shared__ double red[NW + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int S = wide_stages<T, SEG>(ncols);
+  const int ncp = (ncols + WIDE_CB - 1) / WIDE_CB * WIDE_CB;
+  const int nbox = ncp / WIDE_CB;
+  const uint32_t stage_bytes = uint32_t(wide_stage_bytes<T, SEG>(ncols));
+  const uint32_t ring = smem_u32(smem);
+  const uint32_t full0 = ring + uint32_t(S) * stage_bytes;
+  const uint32_t empty0 = full0 + 8 * 8;
+  const int64_t nchunks = (n + R - 1) / R;
+  const int64_t nloc = blockIdx.x < nchunks ? (nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (UPD)
+    for (int c = tid; c < ncols; c += blockDim.x) cin[c] = coef_in[c];
+  __syncthreads();
+  T acc = s_zero<T>();
+  double nrm = 0.0;
+  // projection threads per column: 8, 4, 2 or 1 (a power of two dividing R)
+  const int PG = ncols * 8 <= WIDE_THREADS ? 8 : ncols * 4 <= WIDE_THREADS ? 4
+                 : ncols * 2 <= WIDE_THREADS ? 2 : 1;
+  if (warp == NW) {
+    // ---- producer ----
+    if (lane == 0) {
+      for (int64_t i = 0; i < nloc; ++i) {
+        const int s = int(i % S);
+        if (i >= S) mbar_wait(empty0 + 8 * s, uint32_t(((i / S) - 1) & 1));
+        const int64_t r0 = (int64_t(blockIdx.x) + i * gridDim.x) * R;
+        const uint32_t st = ring + uint32_t(s) * stage_bytes;
+        const int64_t rows = n - r0 < R ? n - r0 : R;
+        const uint32_t wbytes = uint32_t((rows * int64_t(sizeof(T)) + 15) & ~int64_t(15));
+        mbar_expect_tx(full0 + 8 * s, uint32_t(nbox) * uint32_t(WIDE_CB * R * sizeof(T)) + wbytes);
+        for (int bx = 0; bx < nbox; ++bx)
+          tma_load_2d(st + uint32_t(bx * WIDE_CB * R * sizeof(T)), &tmV, int(r0 * DPE),
+                      bx * WIDE_CB, full0 + 8 * s);
+        bulk_g2s(st + uint32_t(ncp * R * sizeof(T)), w + r0, wbytes, full0 + 8 * s);
+      }
+    }
+  } else {
+    // ---- consumers ----
+    const int lr = tid % R, p = tid / R;                  // UPD: row, quarter (fp64: 4 x 64)
+    constexpr int PARTS = WIDE_THREADS / R;               // 4 (fp64) or 8 (complex)
+    for (int64_t i = 0; i < nloc; ++i) {
+      const int s = int(i % S);
+      mbar_wait(full0 + 8 * s, uint32_t((i / S) & 1));
+      const uint32_t st = ring + uint32_t(s) * stage_bytes;
+      const uint32_t wseg = st + uint32_t(ncp * R * sizeof(T));
+      const int64_t r0 = (int64_t(blockIdx.x) + i * gridDim.x) * R;
+      if (UPD) {
+        // four chains over this thread's columns c = p, p + PARTS, ...
+        T s4[4] = {s_zero<T>(), s_zero<T>(), s_zero<T>(), s_zero<T>()};
+        int c = p;
+        for (; c + 3 * PARTS < ncols; c += 4 * PARTS) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int cu = c + u * PARTS;
+            s4[u] = s_fma(lds_s<T>(st + uint32_t((cu * R + lr) * sizeof(T))), cin[cu], s4[u]);
+          }
+        }
+        for (; c < ncols; c += PARTS)
+          s4[0] = s_fma(lds_s<T>(st + uint32_t((c * R + lr) * sizeof(T))), cin[c], s4[0]);
+        part[p][lr] = s_add(s_add(s4[0], s4[1]), s_add(s4[2], s4[3]));
+        consumers_sync();
+        if (p == 0) {
+          T sum = part[0][lr];
+#pragma unroll
+          for (int q2 = 1; q2 < PARTS; ++q2) sum = s_add(sum, part[q2][lr]);
+          const bool valid = r0 + lr < n;
+          const T wr = valid ? s_sub(lds_s<T>(wseg + uint32_t(lr * sizeof(T))), sum) : s_zero<T>();
+          if (valid) w[r0 + lr] = wr;
+          if (NRM) nrm += s_abs2(wr);
+          if (PROJ) {   // the updated w back into the stage for the projection
+            if constexpr (ND == 1) {
+              asm volatile("st.shared.f64 [%0], %1;" ::"r"(wseg + uint32_t(lr * 8)), "d"(wr) : "memory");
+            } else {
+              const cplx z = reinterpret_cast<const cplx&>(wr);
+              asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(wseg + uint32_t(lr * 16)), "d"(z.re),
+                           "d"(z.im) : "memory");
+            }
+          }
+        }
+        if (PROJ) consumers_sync();
+      }
+      if (PROJ && tid < ncols * PG) {
+        // G = PG threads per column (c = tid / PG) take the rows r = g mod PG
+        // (g = tid % PG), visited from row (tid * ... ) on: rr = (i PG + tid)
+        // mod R keeps each thread's residue class and gives the lanes of a
+        // half-warp distinct banks
+        const int c = tid / PG;
+        const uint32_t col = st + uint32_t(c * R * sizeof(T));
+        const int64_t rem = n - r0;
+        const int nit = R / PG;               // 8 .. 64, a multiple of 4 for PG <= 16
+        // four independent chains (the single FMA chain through shared-memory
+        // loads was latency-bound), combined in a fixed order
+        T a4[4] = {s_zero<T>(), s_zero<T>(), s_zero<T>(), s_zero<T>()};
+        if (rem >= R) {
+          for (int i = 0; i < nit; i += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rr = ((i + u) * PG + tid) & (R - 1);
+              a4[u] = s_cfma(lds_s<T>(col + uint32_t(rr * sizeof(T))),
+                             lds_s<T>(wseg + uint32_t(rr * sizeof(T))), a4[u]);
+            }
+          }
+        } else {
+          for (int i = 0; i < nit; i += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int rr = ((i + u) * PG + tid) & (R - 1);
+              if (rr < rem)
+                a4[u] = s_cfma(lds_s<T>(col + uint32_t(rr * sizeof(T))),
+                               lds_s<T>(wseg + uint32_t(rr * sizeof(T))), a4[u]);
+            }
+          }
+        }
+        acc = s_add(acc, s_add(s_add(a4[0], a4[1]), s_add(a4[2], a4[3])));
+      }
+      consumers_sync();   // the stage (and part[]) are free again
+      if (lane == 0) mbar_arrive(empty0 + 8 * s);
+    }
+  }
+  // per-CTA partials: the PG partial sums of a column added in group order
+  if (PROJ) {
+    T* gsum = &part[0][0];   // WIDE_THREADS entries, free after the loop
+    __syncthreads();
+    if (warp < NW) gsum[tid] = acc;
+    __syncthreads();
+    for (int c = tid; c < ncols; c += blockDim.x) {
+      T s = gsum[c * PG];
+      for (int g = 1; g < PG; ++g) s = s_add(s, gsum[c * PG + g]);
+      const double* a = reinterpret_cast<const double*>(&s);
+      for (int d = 0; d < ND; ++d) partials[(int64_t(blockIdx.x) * ncols + c) * ND + d] = a[d];
+    }
+  }
+  if (NRM) {
+    const double v = block_sum(nrm, red);
+    if (tid == 0) partials[blockIdx.x] = v;
+  }
+  if (last_block(counter)) {
+    if (PROJ) {
+      reduce_partials_wide(partials, gridDim.x, ncols * ND, ncols * ND, [&](int q, double v) {
+        if (raw) {
+          raw[q] = v;
+          return;
+        }
+        reinterpret_cast<double*>(coef_out)[q] = v;
+        if (Hcol) reinterpret_cast<double*>(Hcol)[q] = reinterpret_cast<const double*>(coef_in)[q] + v;
+      });
+    }
+    if (NRM) {
+      reduce_partials_wide(partials, gridDim.x, 1, 1, [&](int, double v) {
+        if (raw) {
+          raw[0] = v;
+          return;
+        }
+        const double nr = sqrt(v);
+        double* hs = reinterpret_cast<double*>(Hsub);
+        hs[0] = nr;
+        if (ND == 2) hs[1] = 0.0;
+        inv[0] = 1.0 / nr;
+      });
+    }
+    __syncthreads();
+    if (tid == 0) *counter = 0;
+  }
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiled encode_tiled() {
+  static EncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// wide sweeps: ncols beyond one tile, up to WIDE_MAX_COLS (two stages fit)
+static bool cgs_use_wide(int ncols, int tile) {
+  const char* e = std::getenv("PPF_CGS_WIDE");
+  if (e && e[0] == '0') return false;
+  return ncols > tile && ncols <= WIDE_MAX_COLS && encode_tiled() != nullptr;
+}
+
+template <typename T, int SEG>
+static int cgs_wide_seg(int mode, int64_t n, const T* V, int64_t ldv, int ncols, T* w, const T* ci,
+                        T* co, T* hc, T* hs, double* inv, RedScratch& rs, int grid, cudaStream_t st) {
+  constexpr int R = wide_rows<T, SEG>();
+  constexpr int DPE = int(sizeof(T)) / 8;
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {cuuint64_t(n) * DPE, cuuint64_t(ncols)};
+  const cuuint64_t strides[1] = {cuuint64_t(ldv) * sizeof(T)};
+  const cuuint32_t box[2] = {cuuint32_t(R * DPE), cuuint32_t(WIDE_CB)};
+  const cuuint32_t estr[2] = {1, 1};
+  if (encode_tiled()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<T*>(V), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    fail(PPF_ECUDA, "cuTensorMapEncodeTiled failed");
+  const int S = wide_stages<T, SEG>(ncols);
+  const size_t smem = size_t(S) * size_t(wide_stage_bytes<T, SEG>(ncols)) + 2 * 8 * 8;
+  const int64_t chunks = (n + R - 1) / R;
+  int blocks = int(chunks < grid ? chunks : grid);
+  if (blocks < 1) blocks = 1;
+  auto go = [&](auto kfn, const T* cin, T* cout, T* hcol, T* hsub, double* iv) {
+    // the attribute is per kernel and per device (the three sweep kernels
+    // share one function-pointer type, so the key is the pointer itself)
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (done.insert({reinterpret_cast<const void*>(kfn), dev}).second)
+        cuda_check(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CGS_SMEM),
+                   "cudaFuncSetAttribute(cgs_wide_kernel)");
+    }
+    kfn<<<blocks, WIDE_THREADS + 32, smem, st>>>(tm, n, ncols, w, cin, cout, hcol, hsub, iv,
+                                                 rs.partials, rs.counter, rs.raw);
+    const cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kfn);
+      fail(PPF_ECUDA, std::string("cgs_wide_kernel: ") + cudaGetErrorString(le) + " (blocks " +
+                          std::to_string(blocks) + ", smem " + std::to_string(smem) + ", ncols " +
+                          std::to_string(ncols) + ", maxdyn " + std::to_string(fa.maxDynamicSharedSizeBytes) +
+                          ", static " + std::to_string(fa.sharedSizeBytes) + ", regs " +
+                          std::to_string(fa.numRegs) + ", maxthr " + std::to_string(fa.maxThreadsPerBlock) + ")");
+    }
+  };
+  if (mode == 0)
+    go(cgs_wide_kernel<T, F_PROJ, SEG>, nullptr, co, nullptr, nullptr, nullptr);
+  else if (mode == 1)
+    go(cgs_wide_kernel<T, F_UPD | F_PROJ, SEG>, ci, co, hc, nullptr, nullptr);
+  else
+    go(cgs_wide_kernel<T, F_UPD | F_NRM, SEG>, ci, nullptr, nullptr, hs, inv);
+  return 1;
+}
+
+template <typename T>
+static int cgs_wide(int mode, int64_t n, const T* V, int64_t ldv, int ncols, T* w, const T* ci,
+                    T* co, T* hc, T* hs, double* inv, RedScratch& rs, int grid, cudaStream_t st) {
+  const char* e = std::getenv("PPF_CGS_WIDE_SEG");
+  const bool big = e ? e[0] == '1' : wide_stages<T, 1024>(ncols) >= 3;
+  if (big) return cgs_wide_seg<T, 1024>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+  return cgs_wide_seg<T, 512>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
+}
+
 // rows below which the flat sweeps replace the tiled TMA ones (per rank):
 // ~2 chunks of a full 24-column tile per SM
 static bool cgs_use_flat(int64_t n, int num_sms_cap, int ncols, int tile) {
@@ -1525,6 +1845,8 @@ static int cgs_dispatch(int mode, int64_t n, const void* Vv, int64_t ldv, int nc
   int launches = 0;
   if (cgs_use_flat(n, rs.max_blocks, ncols, TILE))
     return cgs_flat<T>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, rs.max_blocks / 4, st);
+  if (cgs_use_wide(ncols, TILE))
+    return cgs_wide<T>(mode, n, V, ldv, ncols, w, ci, co, hc, hs, inv, rs, grid, st);
   if (ncols <= TILE) {
     if (mode == 0)
       cgs_nc<T, F_PROJ>(n, V, ldv, ncols, w, nullptr, co, nullptr, nullptr, nullptr, rs, grid, st);

@@ -56,7 +56,8 @@ def _guards_intact(buf, segs):
 
 
 CASES = [
-    ("C2", 5, 30, "sell", 32, "0"),     # tiled CGS2 (TMA ring), 2 column tiles
+    ("C2", 5, 30, "sell", 32, "0"),     # wide CGS2 (2-D tensor-map ring), 31 columns
+    ("C2", 5, 30, "sell", 32, "w0"),    # tiled CGS2 (TMA ring), 2 column tiles
     ("C2", 5, 30, "sell", 32, "1"),     # flat CGS2
     ("C4s", 20, 12, "sell", 64, "0"),   # sell2 (C = 64, prefetch, PDL), sqrt
     ("C3s", 10, 20, "csr", 32, None),   # CSR kernel, Lanczos
@@ -78,7 +79,8 @@ def _problem(name, deg):
 @pytest.mark.parametrize("name,deg,m,fmt,C_,flat", CASES)
 def test_guard_bands(ctx_dev, monkeypatch, name, deg, m, fmt, C_, flat):
     if flat is not None:
-        monkeypatch.setenv("PPF_CGS_FLAT", flat)
+        monkeypatch.setenv("PPF_CGS_FLAT", flat[-1])
+        monkeypatch.setenv("PPF_CGS_WIDE", "0" if flat.startswith("w") else "1")
     cfg, A, b, iv = _problem(name, deg)
     ctx = pp.Context(0)
     plan = pp.Plan.from_csr(A, fmt=fmt, C_=C_)
@@ -134,12 +136,14 @@ def ctx_dev():
 
 
 @pytest.mark.parametrize("name,deg,m,C_,flat", [("C2", 5, 40, 32, "0"), ("C2", 5, 40, 32, "1"),
+                                                ("C2", 5, 40, 32, "w0"),
                                                 ("C4s", 20, 14, 64, "0"), ("C5s", 16, 4, 32, None)])
 def test_bitwise_repeatable(ctx_dev, monkeypatch, name, deg, m, C_, flat):
     """Ten runs of the same problem: x and H bitwise identical (a shared-memory
     race in the bulk-copy ring or an early stage release would show here)."""
     if flat is not None:
-        monkeypatch.setenv("PPF_CGS_FLAT", flat)
+        monkeypatch.setenv("PPF_CGS_FLAT", flat[-1])
+        monkeypatch.setenv("PPF_CGS_WIDE", "0" if flat.startswith("w") else "1")
     cfg = configs.CONFIGS[name]
     A, b, iv = configs.build(name)
     ctx = pp.Context(0)

@@ -264,11 +264,12 @@ CASES = [("C1", 4), ("C2", 5), ("C2", 10), ("C2", 20), ("C3s", 10), ("C3s", 20),
 
 
 @pytest.mark.parametrize("name,deg", CASES)
-@pytest.mark.parametrize("cgs", ["flat", "tiled"])
+@pytest.mark.parametrize("cgs", ["flat", "wide", "tiled"])
 def test_run_parity_true_error(ctx, name, deg, cgs, monkeypatch):
     """End to end at the same m*: both sides stop at the first m whose true
     error (vs the closed form) is <= tol (reading Q11)."""
     monkeypatch.setenv("PPF_CGS_FLAT", "1" if cgs == "flat" else "0")
+    monkeypatch.setenv("PPF_CGS_WIDE", "1" if cgs == "wide" else "0")
     cfg = configs.CONFIGS[name]
     A, b, iv = configs.build(name)
     xr = _reference(cfg, A, b)
@@ -289,11 +290,12 @@ def test_run_parity_true_error(ctx, name, deg, cgs, monkeypatch):
 
 @pytest.mark.parametrize("name,deg,C_", [("C2", 10, 64), ("C2", 5, 32), ("C2", 20, 32), ("C3s", 10, 64),
                                          ("C4s", 20, 64)])
-@pytest.mark.parametrize("cgs", ["flat", "tiled"])
+@pytest.mark.parametrize("cgs", ["flat", "wide", "tiled"])
 def test_run_parity_estimate_stop(ctx, name, deg, C_, cgs, monkeypatch):
     """The paper's practical criterion: both stop at the same m
     (C2 also in SELL-32, the layout bench.py times it in)."""
     monkeypatch.setenv("PPF_CGS_FLAT", "1" if cgs == "flat" else "0")
+    monkeypatch.setenv("PPF_CGS_WIDE", "1" if cgs == "wide" else "0")
     cfg = configs.CONFIGS[name]
     A, b, iv = configs.build(name)
     qo = chebyshev.coefficients(*iv, deg)
@@ -444,12 +446,13 @@ def test_graph_replay_bitwise(ctx, name, deg, kry):
 
 @pytest.mark.parametrize("n", [1, 2, 3, 7, 65, 257])
 @pytest.mark.parametrize("kry", ["lanczos", "cgs2"])
-@pytest.mark.parametrize("cgs", ["flat", "tiled"])
+@pytest.mark.parametrize("cgs", ["flat", "wide", "tiled"])
 def test_tiny_and_ragged_sizes(ctx, n, kry, cgs, monkeypatch):
     """Sizes below one SELL slice (64 rows), one CGS2 chunk (256 rows) and
     ragged tails just past them: the run must match the oracle, including the
     bulk-copy tail of the CGS2 sweeps (one padding element for odd n)."""
     monkeypatch.setenv("PPF_CGS_FLAT", "1" if cgs == "flat" else "0")
+    monkeypatch.setenv("PPF_CGS_WIDE", "1" if cgs == "wide" else "0")
     rng = np.random.default_rng(n)
     main = 2.0 + rng.random(n)
     off = 0.3 * rng.random(max(n - 1, 0))
