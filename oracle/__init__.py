@@ -22,8 +22,8 @@ Modules (each function cites the passage it follows):
   reference  R1-R4  closed-form / reference f(A)b
 
 Parity status: every function is pinned by a ``-m "not gpu"`` test in
-tests/test_oracle_*.py except the numerical VALUES of Ritz nodes built from a
-finite Arnoldi run (rounding-dependent at ~1e-11): "parity unpinned"
-for ``newton.ritz_values`` node values themselves -- only their invariants
-(interpolation property, multiset agreement to 1e-8) are checked.
+tests/test_oracle_*.py, including the Ritz node VALUES of a finite Arnoldi run
+(closed forms: the 1D Laplacian from e_1, invariant subspaces).  For generic
+inputs those values carry ~1e-11 of rounding, so the GPU parity
+tests compare nodes as multisets at 1e-8 and import the oracle's q for H/x.
 """

@@ -205,7 +205,7 @@ def test_two_rank_run_matches_oracle(case, transport, request):
         x = np.load(out)
         ms = open(out + ".m").read().split()
         nodes = np.load(out + ".nodes.npy") if cfg.poly == "ritz" else None
-    if nodes is not None:  # the sharded Ritz setup (parity unpinned at ~1e-11, F6)
+    if nodes is not None:  # the sharded Ritz setup (rounding-dependent at ~1e-11, F6)
         assert np.abs(np.sort_complex(nodes) - np.sort_complex(qo.nodes)).max() < 1e-8
     ms_r = [int(v) for v in ms[0::2]]
     assert len(ms_r) == world and all(v == res.m for v in ms_r)   # every rank, the oracle's m

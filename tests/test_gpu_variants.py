@@ -212,7 +212,7 @@ def test_sign_function_shared_q(ctx, func, stop):
 
 def test_sign_function_library_ritz_and_invariant(ctx):
     """The library's own Ritz construction for Q^2 (power 2) agrees with
-    the oracle's nodes as multisets (parity unpinned at ~1e-10, F6), and the
+    the oracle's nodes as multisets (rounding-dependent at ~1e-10, F6), and the
     GPU sign satisfies sign(Q)(sign(Q) b) = b."""
     cfg, A, b, op, qo = _c6s()
     M = pp.Matrix(ctx, pp.Plan.from_csr(A))
@@ -433,7 +433,7 @@ def test_graph_laplacian_forward_basis_run(ctx):
 
 def test_harmonic_ritz_wilson(ctx):
     """Harmonic Ritz nodes from the device Arnoldi run
-    against the oracle's (multisets, parity unpinned at ~1e-10 like the Ritz
+    against the oracle's (multisets, rounding-dependent at ~1e-10 like the Ritz
     nodes, F6), and the run with the oracle's harmonic q imported."""
     from oracle import newton
     cfg = configs.CONFIGS["C5s"]

@@ -215,6 +215,42 @@ def test_contour_ls_wilson_converges():
     assert res.term == "converged" and res.m <= 6
 
 
+def test_ritz_values_closed_form_partial_krylov():
+    """Ritz node VALUES from a finite (d < n) Arnoldi run, pinned by closed
+    forms (PAPER.md:338-354):
+    (i) the 1D Dirichlet Laplacian T_N = tridiag(-1, 2, -1) started from e_1:
+        the Arnoldi/Lanczos basis is e_1..e_d, H_d = T_d, so the Ritz values are
+        2 - 2 cos(k pi/(d+1)), k = 1..d, and ritz_newton's nodes are exactly
+        those, Leja-ordered, with divided differences of z^{-1/2};
+    (ii) b in a d-dimensional invariant subspace of a diagonal A: the d Ritz
+        values are those d eigenvalues (the Krylov space is exhausted)."""
+    import scipy.sparse as sp
+    N, d = 200, 9
+    T = sp.diags([-np.ones(N - 1), 2 * np.ones(N), -np.ones(N - 1)], [-1, 0, 1]).tocsr()
+    e1 = np.zeros(N)
+    e1[0] = 1.0
+    H, _ = newton.arnoldi_plain(Operator(T), e1, d)
+    theta = np.sort(newton.ritz_values(H[:d, :d]).real)
+    exact = np.sort(2 - 2 * np.cos(np.arange(1, d + 1) * np.pi / (d + 1)))
+    assert np.abs(theta - exact).max() < 1e-13
+    q, mv, _ = newton.ritz_newton(Operator(T), e1, d - 1)
+    assert mv == d
+    assert np.abs(np.sort(q.nodes.real) - exact).max() < 1e-13
+    assert np.abs(q.nodes.imag).max() < 1e-13
+    assert abs(q.nodes[0].real - exact.max()) < 1e-13           # Leja: max modulus first
+    # the interpolation property at the closed-form nodes (z^{-1/2} there)
+    assert np.abs(newton.evaluate(q, exact) - exact ** -0.5).max() < 1e-10
+    # (ii) invariant subspace
+    lam = np.arange(1.0, 101.0)
+    A = sp.diags(lam).tocsr()
+    pick = np.array([3, 17, 42, 88]) - 1
+    b = np.zeros(100)
+    b[pick] = [1.0, -2.0, 0.5, 3.0]
+    H2, _ = newton.arnoldi_plain(Operator(A), b, len(pick))
+    th2 = np.sort(newton.ritz_values(H2[:len(pick), :len(pick)]).real)
+    assert np.abs(th2 - lam[pick]).max() < 1e-10
+
+
 def test_harmonic_ritz_values_closed_forms():
     """Harmonic Ritz values: (i) they are the reciprocals of
     the Ritz values of A^{-1} on A K_d(A, b), i.e. the eigenvalues of the
