@@ -1,5 +1,6 @@
 // C ABI entry points (include/ppf.h): errors, context, operator planning and
 // upload, polynomial objects, the host dense kernel.  ppf_run lives in run.cpp.
+#include <climits>
 #include <nccl.h>
 
 #include <algorithm>
@@ -368,6 +369,54 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
         for (; k < w; ++k) B.col[B.ptr[s] + k * C + lane] = pad_col;
       }
     }
+    // 16-bit column deltas (SELL-64, fp64, no sorting): per (slice s, column k)
+    // a base offset b = min over the slice's real entries of (col - row); each
+    // entry stores col - row - b in 16 bits.  Relative to the row, a stencil's
+    // k-th entries of one slice differ only by where the boundary shifts them
+    // (C4, N = 256: offsets within one (s, k) span at most N^2 - 1 = 65535),
+    // so the index stream shrinks from 4 to 2 + 4/64 bytes per entry (C4: 12
+    // -> 10.06 bytes per stored entry).  If any (s, k) spans more than 65535
+    // the plan keeps 32-bit indices.  PPF_IDX16=0 keeps them always.
+    const char* e16 = std::getenv("PPF_IDX16");
+    if (C == 64 && p->dtype == PPF_R64 && p->sigma <= 1 && !(e16 && e16[0] == '0') && stored > 0) {
+      std::vector<int32_t> cb(size_t(stored / 64));
+      std::vector<uint16_t> d16(size_t(stored), 0);
+      bool ok = true;
+      for (int64_t s = 0; s < B.nslices && ok; ++s) {
+        const int64_t w = (B.ptr[s + 1] - B.ptr[s]) / C;
+        for (int64_t k = 0; k < w && ok; ++k) {
+          int64_t lo = INT64_MAX, hi = INT64_MIN;
+          for (int lane = 0; lane < C; ++lane) {
+            const int64_t pp = s * C + lane;
+            if (pp >= n_local || k >= dlen[pp]) continue;   // padding
+            const int64_t off = int64_t(B.col[B.ptr[s] + k * C + lane]) - pp;
+            lo = std::min(lo, off);
+            hi = std::max(hi, off);
+          }
+          if (lo == INT64_MAX) lo = hi = 0;   // all padding (delta 0: col = row)
+          if (hi - lo > 65535) {
+            ok = false;
+            break;
+          }
+          cb[size_t(B.ptr[s] / 64 + k)] = int32_t(lo);
+          for (int lane = 0; lane < C && ok; ++lane) {
+            const int64_t pp = s * C + lane;
+            const size_t idx = size_t(B.ptr[s] + k * C + lane);
+            if (pp < n_local && k < dlen[pp]) {
+              d16[idx] = uint16_t(int64_t(B.col[idx]) - pp - lo);
+              continue;
+            }
+            // padding (val 0): delta 0; the kernel clamps every decoded column
+            // to [0, n), so the x it reads there is in bounds
+            d16[idx] = 0;
+          }
+        }
+      }
+      if (ok) {
+        B.cb.swap(cb);
+        B.d16.swap(d16);
+      }
+    }
   }
   p->sends_set = (nranks == 1);
   *out = guard.release();
@@ -404,7 +453,7 @@ ppf_status ppf_plan_set_halo_send(ppf_plan* p, int peer, int64_t count, const in
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t ptr, col, val, perm, hrows, hptr, hcol, hval, recv, send, sidx, total;
+  size_t ptr, col, cb, val, perm, hrows, hptr, hcol, hval, recv, send, sidx, total;
 };
 
 static Layout layout_of(const ppf_plan* p) {
@@ -413,8 +462,15 @@ static Layout layout_of(const ppf_plan* p) {
   size_t o = 0;
   L.ptr = o;
   o += al256(p->diag.ptr.size() * 8);
-  L.col = o;
-  o += al256(p->diag.col.size() * 4);
+  L.col = o;   // 32-bit indices, or the 16-bit deltas + per-(slice, column) bases
+  if (p->diag.d16.empty()) {
+    o += al256(p->diag.col.size() * 4);
+    L.cb = o;
+  } else {
+    o += al256(p->diag.d16.size() * 2);
+    L.cb = o;
+    o += al256(p->diag.cb.size() * 4);
+  }
   L.val = o;
   o += al256(p->diag.col.size() * sc);
   L.perm = o;
@@ -476,7 +532,12 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     if (n) PPF_CUDA(cudaMemcpyAsync(b + off, src, n, cudaMemcpyHostToDevice, st));
   };
   up(L.ptr, p->diag.ptr.data(), p->diag.ptr.size() * 8);
-  up(L.col, p->diag.col.data(), p->diag.col.size() * 4);
+  if (p->diag.d16.empty()) {
+    up(L.col, p->diag.col.data(), p->diag.col.size() * 4);
+  } else {
+    up(L.col, p->diag.d16.data(), p->diag.d16.size() * 2);
+    up(L.cb, p->diag.cb.data(), p->diag.cb.size() * 4);
+  }
   up(L.val, p->diag.val.data(), p->diag.col.size() * sc);
   up(L.perm, p->diag.perm.data(), p->diag.perm.size() * 4);
   up(L.hrows, p->halo.rows.data(), p->halo.rows.size() * 4);
@@ -511,7 +572,13 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
   m->rank = p->rank;
   m->nslices = p->diag.nslices;
   m->d_ptr = reinterpret_cast<const int64_t*>(b + L.ptr);
-  m->d_col = reinterpret_cast<const int32_t*>(b + L.col);
+  if (p->diag.d16.empty()) {
+    m->d_col = reinterpret_cast<const int32_t*>(b + L.col);
+  } else {
+    m->d_col = nullptr;
+    m->d_d16 = reinterpret_cast<const uint16_t*>(b + L.col);
+    m->d_cb = reinterpret_cast<const int32_t*>(b + L.cb);
+  }
   m->d_val = b + L.val;
   m->d_perm = p->diag.perm.empty() ? nullptr : reinterpret_cast<const int32_t*>(b + L.perm);
   {

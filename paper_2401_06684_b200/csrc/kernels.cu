@@ -228,14 +228,15 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
 
 // two rows per lane, 128-bit loads of (val, val) and (col, col); C = 64, fp64;
 // KS warps per slice as in sell1_kernel
-template <int KS, bool ACC = false>
+template <int KS, bool ACC = false, bool IDX16 = false>
 __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
                                                     const double* __restrict__ val,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ out, EpiT<double> e,
-                                                    bool has_x) {
+                                                    bool has_x, const uint16_t* __restrict__ d16,
+                                                    const int32_t* __restrict__ cbase) {
   pdl_release();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
@@ -256,8 +257,16 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
     // 128-B line per 8 lanes of values (16 B each) / 16 lanes of indices.
     if ((lane & 7) == 0)
       for (int k = k0; k < k1; ++k) prefetch_l2(val + base + 64 * k + 2 * lane);
-    if ((lane & 15) == 0)
-      for (int k = k0; k < k1; ++k) prefetch_l2(col + base + 64 * k + 2 * lane);
+    if constexpr (IDX16) {
+      // 16-bit deltas: 128 B per column of the slice; the bases: 4 B per column
+      if (lane == 0) {
+        for (int k = k0; k < k1; ++k) prefetch_l2(d16 + base + 64 * k);
+        prefetch_l2(cbase + (base >> 6) + k0);
+      }
+    } else {
+      if ((lane & 15) == 0)
+        for (int k = k0; k < k1; ++k) prefetch_l2(col + base + 64 * k + 2 * lane);
+    }
   }
   pdl_wait();
   // the slice's rows of the epilogue vectors and of x (its own rows: the
@@ -272,17 +281,39 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
     }
   }
   if (live) {
-    const int2* cp = reinterpret_cast<const int2*>(col + base) + lane;
     const double2* vp = reinterpret_cast<const double2*>(val + base) + lane;
     // (measured: the compiler's own schedule of this loop, at 32 registers
     // and full occupancy, streams C3/C4 at 97-98% of the measured copy
     // bandwidth; the forced batching of sell1_kernel drops it to 72%)
+    if constexpr (IDX16) {
+      // column = row + base(s, k) + 16-bit delta (the plan's encoding),
+      // clamped to [0, n): padding slots (val 0, delta 0) of rows near the
+      // ends, and of the lanes past n in the last slice, then read in bounds
+      const ushort2* dp = reinterpret_cast<const ushort2*>(d16 + base) + lane;
+      const int32_t* cbp = cbase + (base >> 6);
+      const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
+      // (measured and dropped: the slice's bases loaded once and taken by
+      // shuffles in the loop -- C4 273 -> 290 ms; the broadcast load per step
+      // stays)
 #pragma unroll 4
-    for (int k = k0; k < k1; ++k) {
-      const int2 c = __ldg(cp + 32 * k);
-      const double2 v = __ldg(vp + 32 * k);
-      a0 = fma(v.x, __ldg(x + c.x), a0);
-      a1 = fma(v.y, __ldg(x + c.y), a1);
+      for (int k = k0; k < k1; ++k) {
+        const ushort2 d = __ldg(dp + 32 * k);
+        const int cb = __ldg(cbp + k) + r0i;
+        const double2 v = __ldg(vp + 32 * k);
+        const int c0 = min(max(cb + int(d.x), 0), nm1);
+        const int c1 = min(max(cb + 1 + int(d.y), 0), nm1);
+        a0 = fma(v.x, __ldg(x + c0), a0);
+        a1 = fma(v.y, __ldg(x + c1), a1);
+      }
+    } else {
+      const int2* cp = reinterpret_cast<const int2*>(col + base) + lane;
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const int2 c = __ldg(cp + 32 * k);
+        const double2 v = __ldg(vp + 32 * k);
+        a0 = fma(v.x, __ldg(x + c.x), a0);
+        a1 = fma(v.y, __ldg(x + c.y), a1);
+      }
     }
   }
   if constexpr (KS > 1) {
@@ -1060,10 +1091,18 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
       const int64_t spb2 = (bt / 32) / KS;
       const int b2 = int((A->nslices + spb2 - 1) / spb2);
 #define PPF_S2(K)                                                                            \
-  launch_pdl(sell2_kernel<K, ACC>, b2, bt, st, A->nslices, A->n_local, A->d_ptr, A->d_col, \
-             reinterpret_cast<const double*>(val), xt, ot, et, has_x)
-      PPF_KS(PPF_S2)
+  launch_pdl(sell2_kernel<K, ACC, false>, b2, bt, st, A->nslices, A->n_local, A->d_ptr, A->d_col, \
+             reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb)
+#define PPF_S2D(K)                                                                           \
+  launch_pdl(sell2_kernel<K, ACC, true>, b2, bt, st, A->nslices, A->n_local, A->d_ptr, A->d_col, \
+             reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb)
+      if (A->d_d16) {
+        PPF_KS(PPF_S2D)
+      } else {
+        PPF_KS(PPF_S2)
+      }
 #undef PPF_S2
+#undef PPF_S2D
       post_launch("sell2_kernel");
       return;
     }

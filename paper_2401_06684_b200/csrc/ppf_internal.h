@@ -99,6 +99,12 @@ struct HostBlock {
   std::vector<int32_t> col;
   std::vector<double> val;     // n_doubles per entry
   std::vector<int32_t> perm;   // SELL sigma > 1: perm[pos] = original local row
+  // SELL-64 fp64 with 16-bit column deltas (round 2): column of entry (slice s,
+  // column k, lane slot t, row r = 64 s + t) = r + cb[ptr[s]/64 + k] +
+  // d16[ptr[s] + 64 k + t]; padding entries carry delta 0 (val 0).  Empty
+  // unless every (s, k) spans <= 65535 in (col - row).
+  std::vector<uint16_t> d16;
+  std::vector<int32_t> cb;
 };
 
 struct HostHalo {
@@ -141,6 +147,8 @@ struct ppf_mat {
   const int32_t* d_col;
   const void* d_val;
   const int32_t* d_perm;    // null unless sigma > 1
+  const uint16_t* d_d16 = nullptr;  // 16-bit column deltas (SELL-64 fp64), with d_cb
+  const int32_t* d_cb = nullptr;    // per (slice, column) base offset (col - row)
   int csr_group;            // lanes per row for the CSR kernel
   int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks
   int64_t sell_heavy = 0;   // leading slices given a whole block each (see sell_heavy_prefix)

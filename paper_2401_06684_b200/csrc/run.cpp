@@ -398,7 +398,9 @@ struct Runner {
   void spmv_now(const void* x, void* out, const Epi& e) {
     // algorithmic bytes: values + column indices once, x gathered once, out
     // written once, z and u streamed once
-    const double bytes = double(sc + 4) * double(A->nnz) +
+    // (index bytes per entry: 4, or 2 + 4/64 with the 16-bit column deltas)
+    const double idxb = A->d_d16 ? 2.0 + 4.0 / 64.0 : 4.0;
+    const double bytes = (double(sc) + idxb) * double(A->nnz) +
                          double(sc) * double(n) * (2 + (e.z ? 1 : 0) + (e.u ? 1 : 0));
     if (A->nranks > 1) {
       // pack + overlapped exchange + diagonal block + halo block; timed as one

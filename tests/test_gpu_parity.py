@@ -55,9 +55,17 @@ def ragged_matrix(n, seed, complex_=False):
 FORMATS = [("sell", 32, 1), ("sell", 64, 1), ("sell", 32, 128), ("csr", 32, 1)]
 
 
+@pytest.mark.parametrize("idx", ["16", "32"])
 @pytest.mark.parametrize("fmt,C_,sig", FORMATS)
-@pytest.mark.parametrize("which", ["lap3", "convdiff3", "ragged", "ragged_c", "wilson"])
-def test_spmv_parity(ctx, fmt, C_, sig, which):
+@pytest.mark.parametrize("which", ["lap3", "convdiff3", "ragged", "ragged_c", "wilson", "wide_cols"])
+def test_spmv_parity(ctx, fmt, C_, sig, which, idx, monkeypatch):
+    """Every format against SciPy; SELL-64 (fp64) with the 16-bit column
+    deltas (PPF_IDX16, the default where every (slice, column) spans <= 65535
+    columns) and with 32-bit indices; "wide_cols" has columns spread over
+    200,000 so the plan must fall back to 32-bit indices."""
+    monkeypatch.setenv("PPF_IDX16", "1" if idx == "16" else "0")
+    if idx == "16" and not (fmt == "sell" and C_ == 64):
+        pytest.skip("16-bit deltas exist for SELL-64 only")
     if which == "lap3":
         A = ops.laplacian(13, 3)            # 2197 rows: ragged tail for C = 32 and 64
     elif which == "convdiff3":
@@ -66,6 +74,8 @@ def test_spmv_parity(ctx, fmt, C_, sig, which):
         A = ragged_matrix(3001, 1)
     elif which == "ragged_c":
         A = ragged_matrix(1999, 2, complex_=True)
+    elif which == "wide_cols":
+        A = ragged_matrix(200_000, 5)
     else:
         A = ops.wilson_dirac(3, -1.0, seed=4)
     if np.iscomplexobj(A.val) and C_ == 64:
