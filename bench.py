@@ -445,6 +445,7 @@ def main():
         plan = pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1], sigma=sigma)
         ctx = pp.Context(local, stream=stream)
     info = plan.info()
+    index_bits = plan.index_bits()
     if args.no_graphs:
         ctx.set_graphs(False)
     M = pp.Matrix(ctx, plan)
@@ -617,15 +618,19 @@ def main():
         "config": workload_config(args, cfg, name, deg, A.n, A.nnz, m_iter, reps[-1].mvms, world,
                                   cplx_run, krylov_m, newton_eval),
         "layout": {"format": args.fmt, "sell_sigma": sigma, "sell_split": split,
-                   "stored_entries": info["stored"], "ranks_joined": ranks_joined},
+                   "stored_entries": info["stored"], "column_index_bits": index_bits,
+                   "ranks_joined": ranks_joined},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "fused SELL SpMV + Clenshaw/Newton epilogue (spmv class)",
                      "peak_source": peak_src,
                      "peak_note": "hbm_gbs is a 1:1 read/write copy (torch b.copy_(a)); the SpMV stream is "
-                                  "~90% reads, which the HBM sustains slightly faster, so frac can reach 1.0; "
-                                  "ncu puts the C4 SpMV at 80% of the DRAM's theoretical peak "
+                                  "~92% reads, which the HBM sustains slightly faster, so frac can reach 1.0; "
+                                  "ncu puts the C4 SpMV at 83% of the DRAM's theoretical peak "
                                   "(profiles/ncu_summary.json)",
+                     "bytes_per_unit": ("per SpMV launch: (s + i) per nonzero + s per row for x, out and "
+                                        "each epilogue vector (s = 8 or 16 bytes per scalar; i = 4, or "
+                                        f"2 + 4/64 with 16-bit column deltas -- here {index_bits}-bit)"),
                      "launches_timed": sp["launches"],
                      "share_of_device_time": sp["ms"] / tot_ms if tot_ms else None,
                      "traffic_note": traffic_note},

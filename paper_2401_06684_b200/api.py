@@ -160,6 +160,12 @@ class Plan:
         check(_lib().ppf_plan_info(self.h, C.byref(n), C.byref(z), C.byref(s), C.byref(h)))
         return dict(n_local=n.value, nnz=z.value, stored=s.value, halo_total=h.value)
 
+    def index_bits(self) -> int:
+        """ppf_plan_index_bits: 16 (SELL-64 fp64 column deltas) or 32."""
+        b = C.c_int()
+        check(_lib().ppf_plan_index_bits(self.h, C.byref(b)))
+        return b.value
+
     def halo_recv(self, peer: int) -> np.ndarray:
         cnt = C.c_int64()
         check(_lib().ppf_plan_halo_count(self.h, peer, C.byref(cnt)))

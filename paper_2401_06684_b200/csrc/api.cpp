@@ -423,6 +423,13 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
   PPF_API_END
 }
 
+ppf_status ppf_plan_index_bits(const ppf_plan* p, int* bits) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p && bits, "NULL argument");
+  *bits = p->diag.d16.empty() ? 32 : 16;
+  PPF_API_END
+}
+
 ppf_status ppf_plan_halo_count(const ppf_plan* p, int peer, int64_t* count) {
   PPF_API_BEGIN
   PPF_REQUIRE(p && count && peer >= 0 && peer < p->nranks, "bad arguments");

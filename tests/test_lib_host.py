@@ -261,7 +261,12 @@ def test_plan_sell_layout_sizes():
             assert info["stored"] == A.nnz
         else:
             assert A.nnz <= info["stored"] <= 7 * (A.n + C_)
-        assert p.device_bytes() >= info["stored"] * 12
+        # 8-byte values + 4-byte indices, or 2-byte deltas (+ a 4-byte base per
+        # 64 entries) where the SELL-64 plan encodes them in 16 bits
+        ib = p.index_bits()
+        assert ib == (16 if (fmt, C_) == ("sell", 64) else 32)
+        per = 12 if ib == 32 else 10
+        assert p.device_bytes() >= info["stored"] * per
 
 
 def test_plan_rejects_bad_input():
@@ -371,3 +376,27 @@ int main(void) {
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert "EINVAL" in r.stdout.upper() or "INVAL" in r.stdout.upper()
+
+
+def test_plan_index_bits_choice(monkeypatch):
+    """ppf_plan_index_bits: the SELL-64 fp64 plan stores 16-bit column deltas
+    relative to the row when every slice-column spans <= 65535 (stencils,
+    including the 256^3 conv-diff of C4 whose offsets reach N^2 = 65536 but
+    span at most N^2 - 1 within one slice-column), 32-bit indices otherwise
+    (columns spread over 200,000) or when PPF_IDX16=0."""
+    A = ops.convdiff(40, 3, (10.0, 10.0, 10.0))
+    assert Plan.from_csr(A, fmt="sell", C_=64).index_bits() == 16
+    assert Plan.from_csr(A, fmt="sell", C_=32).index_bits() == 32
+    monkeypatch.setenv("PPF_IDX16", "0")
+    assert Plan.from_csr(A, fmt="sell", C_=64).index_bits() == 32
+    monkeypatch.delenv("PPF_IDX16")
+    n = 200_000
+    i = np.arange(n, dtype=np.int64)
+    cols = np.sort(np.stack([i, (i * 7919) % n, (i * 104729 + 17) % n], axis=1), axis=1)
+    keep = np.ones_like(cols, dtype=bool)
+    keep[:, 1:] = cols[:, 1:] != cols[:, :-1]            # distinct, sorted per row
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(keep.sum(axis=1), out=rp[1:])
+    from inputs.operators import CSR
+    R = CSR(n, rp, cols[keep], np.ones(int(rp[-1])))
+    assert Plan.from_csr(R, fmt="sell", C_=64).index_bits() == 32

@@ -1,5 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()"
-timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -rf -x -k "spmv" > gpurun_out/r2_idx16.log 2>&1; echo pytest_rc=$?
-tail -2 gpurun_out/r2_idx16.log
-for i in 1 2; do timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_i.json 2>/dev/null; python -c "import json;d=json.load(open('gpurun_out/r2_i.json'));print('C4',round(d['value']*1e3,3),'ms m',d['config']['m'],{k:round(v,2) for k,v in d['breakdown_ms_per_step'].items()},{k:round(v or 0) for k,v in d['breakdown_gbs'].items()}, d['roofline']['frac'], d['clocks'])"; done
-timeout 600 python bench.py --config C3 --deg 20 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r2_i.json 2>/dev/null; python -c "import json;d=json.load(open('gpurun_out/r2_i.json'));print('C3 deg 20',round(d['value']*1e3,3),'ms m',d['config']['m'],{k:round(v,2) for k,v in d['breakdown_ms_per_step'].items()},{k:round(v or 0) for k,v in d['breakdown_gbs'].items()})"
+mkdir -p gpurun_out/r02
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r02/ncu_launches_c4_idx16.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-profile > /dev/null 2>&1; echo ncu_rc=$?
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled --kernel-name 'regex:sell2_kernel' --launch-skip 200 --launch-count 1 -o gpurun_out/r02/sell2_c4_idx16 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-profile > /dev/null 2>&1; echo ncu2_rc=$?
