@@ -167,8 +167,9 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
 ppf_status ppf_plan_device_bytes(const ppf_plan* plan, size_t* bytes);
 ppf_status ppf_plan_info(const ppf_plan* plan, int64_t* n_local, int64_t* nnz,
                          int64_t* stored_entries, int64_t* halo_total);
-/* ppf_plan_index_bits: 32, or 16 when the SELL-64 fp64 diagonal block stores its
- * column indices as 16-bit deltas relative to the row (per slice-column base;
+/* ppf_plan_index_bits: 32, or 16 when the SELL diagonal block (complex C = 32,
+ * fp64 C = 64; no sigma sorting) stores its column indices as 16-bit deltas
+ * relative to the row (per slice-column base;
  * chosen by ppf_plan_create whenever every slice-column spans <= 65535 --
  * stencils do -- unless the environment sets PPF_IDX16=0). */
 ppf_status ppf_plan_index_bits(const ppf_plan* plan, int* bits);

@@ -378,8 +378,12 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
     // -> 10.06 bytes per stored entry).  If any (s, k) spans more than 65535
     // the plan keeps 32-bit indices.  PPF_IDX16=0 keeps them always.
     const char* e16 = std::getenv("PPF_IDX16");
-    if (C == 64 && p->dtype == PPF_R64 && p->sigma <= 1 && !(e16 && e16[0] == '0') && stored > 0) {
-      std::vector<int32_t> cb(size_t(stored / 64));
+    // (complex SELL-32 and fp64 SELL-64: the bandwidth-bound layouts; on the
+    // fp64 SELL-32 operators -- small, L2-resident, latency-bound -- the extra
+    // base load per entry cost more than the bytes saved: C2 deg 5 8.8 -> 9.6 ms)
+    if (((C == 32 && p->dtype == PPF_C128) || (C == 64 && p->dtype == PPF_R64)) &&
+        p->sigma <= 1 && !(e16 && e16[0] == '0') && stored > 0) {
+      std::vector<int32_t> cb(size_t(stored / C));
       std::vector<uint16_t> d16(size_t(stored), 0);
       bool ok = true;
       for (int64_t s = 0; s < B.nslices && ok; ++s) {
@@ -398,7 +402,7 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
             ok = false;
             break;
           }
-          cb[size_t(B.ptr[s] / 64 + k)] = int32_t(lo);
+          cb[size_t(B.ptr[s] / C + k)] = int32_t(lo);
           for (int lane = 0; lane < C && ok; ++lane) {
             const int64_t pp = s * C + lane;
             const size_t idx = size_t(B.ptr[s] + k * C + lane);

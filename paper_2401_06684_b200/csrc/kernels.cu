@@ -71,6 +71,11 @@ __device__ __forceinline__ int ld_stream(const int32_t* p) {
   asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
+__device__ __forceinline__ int ld_stream(const uint16_t* p) {
+  unsigned short r;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return int(r);
+}
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
@@ -147,7 +152,7 @@ __device__ __forceinline__ void acc_update(const EpiT<T>& e, int64_t row, T r) {
 // latency-bound at 5.2 TB/s (ncu: 36% "mem busy", 60 warps/SM active) instead
 // of 6.5 TB/s.
 // ---------------------------------------------------------------------------
-template <typename T, int KS, bool PERM, bool ACC = false>
+template <typename T, int KS, bool PERM, bool ACC = false, bool IDX16 = false>
 __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
@@ -155,7 +160,9 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
                                                     const T* __restrict__ x, T* __restrict__ out,
                                                     EpiT<T> e, bool has_x,
                                                     const int32_t* __restrict__ perm,
-                                                    int64_t nheavy) {
+                                                    int64_t nheavy,
+                                                    const uint16_t* __restrict__ d16 = nullptr,
+                                                    const int32_t* __restrict__ cbase = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // the first nheavy slices (the longest rows after a whole-matrix sigma sort)
   // get a whole block each, 8 warps splitting their entry columns; the rest
@@ -174,7 +181,32 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
     const int k0 = part * w / parts, k1 = (part + 1) * w / parts;
     const int32_t* cp = col + base + lane;
     const T* vp = val + base + lane;
-    if constexpr (sizeof(T) == 8) {
+    if constexpr (IDX16) {
+      // column = row + base(s, k) + 16-bit delta, clamped to [0, n) (padding;
+      // see the plan's encoding and sell2_kernel)
+      const uint16_t* dp = d16 + base + lane;
+      const int32_t* cbp = cbase + (base >> 5);
+      const int ri = int(slice * 32 + lane), nm1 = int(n - 1);
+      constexpr int U = sizeof(T) == 8 ? 2 : 4;
+      int k = k0;
+      for (; k + U <= k1; k += U) {
+        int c[U];
+        T v[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          c[u] = min(max(ri + __ldg(cbp + k + u) + ld_stream(dp + 32 * (k + u)), 0), nm1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_stream(vp + 32 * (k + u));
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = ld_gather(x + c[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc = s_fma(v[u], xv[u], acc);
+      }
+      for (; k < k1; ++k) {
+        const int c0 = min(max(ri + __ldg(cbp + k) + ld_stream(dp + 32 * k), 0), nm1);
+        acc = s_fma(ldg(vp + 32 * k), ldg(x + c0), acc);
+      }
+    } else if constexpr (sizeof(T) == 8) {
       // fp64: ptxas' own 32-register schedule at full occupancy is faster
       // (as for sell2_kernel; batching measured 4.2 vs 6.2 TB/s on C3, and
       // 3.4 vs 6.1 TB/s on C3 in this C = 32 layout; on C7's gathers: equal)
@@ -1113,11 +1145,18 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
 #define PPF_S1(K)                                                                                    \
   sell1_kernel<T, K, false, ACC><<<blocks, t1, 0, st>>>(A->nslices, A->n_local, A->d_ptr, A->d_col, \
                                                          val, xt, ot, et, has_x, nullptr, nh)
+#define PPF_S1D(K)                                                                                   \
+  sell1_kernel<T, K, false, ACC, true><<<blocks, t1, 0, st>>>(A->nslices, A->n_local, A->d_ptr,     \
+                                                              A->d_col, val, xt, ot, et, has_x,      \
+                                                              nullptr, nh, A->d_d16, A->d_cb)
   if (A->d_perm) {
     PPF_KS(PPF_S1P)
+  } else if (A->d_d16) {
+    PPF_KS(PPF_S1D)
   } else {
     PPF_KS(PPF_S1)
   }
+#undef PPF_S1D
 #undef PPF_S1P
 #undef PPF_S1
 #undef PPF_KS
@@ -1981,13 +2020,24 @@ template <typename T> struct ResCallT {
 template <typename T>
 __device__ void res_spmv(int64_t n, const int64_t* __restrict__ sptr, const int32_t* __restrict__ col,
                          const T* __restrict__ val, const T* x, T* out, const EpiT<T>& e,
-                         bool has_x) {
+                         bool has_x, const uint16_t* __restrict__ d16,
+                         const int32_t* __restrict__ cbase) {
   for (int64_t row = threadIdx.x; row < n; row += blockDim.x) {
     const int64_t base = sptr[row >> 5];
     const int w = int((sptr[(row >> 5) + 1] - base) >> 5);
     const int lane = int(row & 31);
     T acc = s_zero<T>();
-    for (int k = 0; k < w; ++k) acc = s_fma(ldg(val + base + 32 * k + lane), x[__ldg(col + base + 32 * k + lane)], acc);
+    if (d16) {   // 16-bit column deltas (plan encoding), clamped
+      const int32_t* cbp = cbase + (base >> 5);
+      for (int k = 0; k < w; ++k) {
+        const int c = min(max(int(row) + __ldg(cbp + k) + int(__ldg(d16 + base + 32 * k + lane)), 0),
+                          int(n - 1));
+        acc = s_fma(ldg(val + base + 32 * k + lane), x[c], acc);
+      }
+    } else {
+      for (int k = 0; k < w; ++k)
+        acc = s_fma(ldg(val + base + 32 * k + lane), x[__ldg(col + base + 32 * k + lane)], acc);
+    }
     T r = s_mul(e.s_ax, acc);
     if (has_x) r = s_fma(e.s_x, e.xe[row], r);
     if (e.z) r = s_fma(e.s_z, e.z[row], r);
@@ -2024,7 +2074,7 @@ __global__ void __launch_bounds__(1024, 1) resident_steps_kernel(
     int64_t n, const int64_t* __restrict__ sptr, const int32_t* __restrict__ col,
     const T* __restrict__ val, T* V, int64_t ldv, T* U, T* W, T* H, int ldh, int m_max,
     int lanczos, const double* beta0_dev, ResCtl* ctl, const ResCallT<T>* calls_host, int ncalls,
-    int ahead) {
+    int ahead, const uint16_t* __restrict__ d16, const int32_t* __restrict__ cbase) {
   constexpr int ND = n_doubles<T>();
   extern __shared__ __align__(16) unsigned char res_smem[];
   ResCallT<T>* calls = reinterpret_cast<ResCallT<T>*>(res_smem);
@@ -2067,11 +2117,11 @@ __global__ void __launch_bounds__(1024, 1) resident_steps_kernel(
     T* vj = V + int64_t(j) * ldv;
     T* vn = V + int64_t(j + 1) * ldv;
     // u = A v_j, then the chain U -> ... -> W
-    res_spmv(n, sptr, col, val, vj, U, plain, false);
+    res_spmv(n, sptr, col, val, vj, U, plain, false, d16, cbase);
     for (int c = 0; c < ncalls; ++c) {
       __syncthreads();
       const ResCallT<T>& cl = calls[c];
-      res_spmv(n, sptr, col, val, cl.x, cl.out, cl.e, cl.has_x != 0);
+      res_spmv(n, sptr, col, val, cl.x, cl.out, cl.e, cl.has_x != 0, d16, cbase);
     }
     __syncthreads();
     if (lanczos) {
@@ -2194,7 +2244,8 @@ void launch_resident(ppf_mat* A, void* V, int64_t ldv, void* U, void* W, void* H
     kfn<<<1, 1024, smem, st>>>(A->n_local, A->d_ptr, A->d_col, static_cast<const T*>(A->d_val), \
                                static_cast<T*>(V), ldv, static_cast<T*>(U), static_cast<T*>(W), \
                                static_cast<T*>(H), ldh, m_max, lanczos, beta0_dev, ctl_dev,     \
-                               static_cast<const ResCallT<T>*>(calls_dev), ncalls, ahead);      \
+                               static_cast<const ResCallT<T>*>(calls_dev), ncalls, ahead,       \
+                               A->d_d16, A->d_cb);                                              \
   }
   if (A->dtype == PPF_R64)
     PPF_RES(double)

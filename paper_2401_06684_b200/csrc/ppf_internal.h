@@ -99,10 +99,10 @@ struct HostBlock {
   std::vector<int32_t> col;
   std::vector<double> val;     // n_doubles per entry
   std::vector<int32_t> perm;   // SELL sigma > 1: perm[pos] = original local row
-  // SELL-64 fp64 with 16-bit column deltas (round 2): column of entry (slice s,
-  // column k, lane slot t, row r = 64 s + t) = r + cb[ptr[s]/64 + k] +
-  // d16[ptr[s] + 64 k + t]; padding entries carry delta 0 (val 0).  Empty
-  // unless every (s, k) spans <= 65535 in (col - row).
+  // SELL (C = 32, or C = 64 fp64; no sorting) with 16-bit column deltas
+  // (round 2): column of entry (slice s, column k, slot t, row r = C s + t) =
+  // r + cb[ptr[s]/C + k] + d16[ptr[s] + C k + t]; padding entries carry delta 0
+  // (val 0).  Empty unless every (s, k) spans <= 65535 in (col - row).
   std::vector<uint16_t> d16;
   std::vector<int32_t> cb;
 };
@@ -147,7 +147,7 @@ struct ppf_mat {
   const int32_t* d_col;
   const void* d_val;
   const int32_t* d_perm;    // null unless sigma > 1
-  const uint16_t* d_d16 = nullptr;  // 16-bit column deltas (SELL-64 fp64), with d_cb
+  const uint16_t* d_d16 = nullptr;  // 16-bit column deltas (SELL), with d_cb
   const int32_t* d_cb = nullptr;    // per (slice, column) base offset (col - row)
   int csr_group;            // lanes per row for the CSR kernel
   int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks

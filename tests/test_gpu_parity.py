@@ -59,13 +59,13 @@ FORMATS = [("sell", 32, 1), ("sell", 64, 1), ("sell", 32, 128), ("csr", 32, 1)]
 @pytest.mark.parametrize("fmt,C_,sig", FORMATS)
 @pytest.mark.parametrize("which", ["lap3", "convdiff3", "ragged", "ragged_c", "wilson", "wide_cols"])
 def test_spmv_parity(ctx, fmt, C_, sig, which, idx, monkeypatch):
-    """Every format against SciPy; SELL-64 (fp64) with the 16-bit column
-    deltas (PPF_IDX16, the default where every (slice, column) spans <= 65535
+    """Every format against SciPy; SELL-32/64 with the 16-bit column deltas
+    (PPF_IDX16, the default where every (slice, column) spans <= 65535
     columns) and with 32-bit indices; "wide_cols" has columns spread over
     200,000 so the plan must fall back to 32-bit indices."""
     monkeypatch.setenv("PPF_IDX16", "1" if idx == "16" else "0")
-    if idx == "16" and not (fmt == "sell" and C_ == 64):
-        pytest.skip("16-bit deltas exist for SELL-64 only")
+    if idx == "16" and not (fmt == "sell" and sig == 1):
+        pytest.skip("16-bit deltas exist for SELL without sorting")
     if which == "lap3":
         A = ops.laplacian(13, 3)            # 2197 rows: ragged tail for C = 32 and 64
     elif which == "convdiff3":

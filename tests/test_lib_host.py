@@ -264,7 +264,7 @@ def test_plan_sell_layout_sizes():
         # 8-byte values + 4-byte indices, or 2-byte deltas (+ a 4-byte base per
         # 64 entries) where the SELL-64 plan encodes them in 16 bits
         ib = p.index_bits()
-        assert ib == (16 if (fmt, C_) == ("sell", 64) else 32)
+        assert ib == (16 if (fmt, C_, sig) == ("sell", 64, 1) else 32)   # fp64 operator
         per = 12 if ib == 32 else 10
         assert p.device_bytes() >= info["stored"] * per
 
@@ -386,7 +386,10 @@ def test_plan_index_bits_choice(monkeypatch):
     (columns spread over 200,000) or when PPF_IDX16=0."""
     A = ops.convdiff(40, 3, (10.0, 10.0, 10.0))
     assert Plan.from_csr(A, fmt="sell", C_=64).index_bits() == 16
-    assert Plan.from_csr(A, fmt="sell", C_=32).index_bits() == 32
+    assert Plan.from_csr(A, fmt="sell", C_=32).index_bits() == 32          # fp64 SELL-32: no
+    W = ops.wilson_dirac(4, -1.0, seed=5)                                   # complex SELL-32: yes
+    assert Plan.from_csr(W, fmt="sell", C_=32).index_bits() == 16
+    assert Plan.from_csr(W, fmt="sell", C_=32, sigma=64).index_bits() == 32
     monkeypatch.setenv("PPF_IDX16", "0")
     assert Plan.from_csr(A, fmt="sell", C_=64).index_bits() == 32
     monkeypatch.delenv("PPF_IDX16")
