@@ -79,6 +79,9 @@ def parse():
     p.add_argument("--m-max", type=int, default=None, help="override the config's m_max")
     p.add_argument("--check-every", type=int, default=1,
                    help="k of the stopping check (PAPER.md:424 uses 64/d)")
+    p.add_argument("--encoding", default="auto", choices=["auto", "explicit", "delta16", "pair8"],
+                   help="device layout of the matrix entries (ppf_plan_encoding); auto = the "
+                        "narrowest lossless one the plan finds")
     p.add_argument("--split", type=int, default=0,
                    help="warps per SELL slice (ppf_mat_set_split; 0 = automatic)")
     p.add_argument("--no-profile", action="store_true",
@@ -444,8 +447,12 @@ def main():
         bounds = [0, A.n]
         plan = pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1], sigma=sigma)
         ctx = pp.Context(local, stream=stream)
+    if args.encoding != "auto":
+        plan.set_encoding(args.encoding)
     info = plan.info()
     index_bits = plan.index_bits()
+    encoding, pair_table = plan.encoding()
+    matrix_bytes = plan.device_bytes()
     if args.no_graphs:
         ctx.set_graphs(False)
     M = pp.Matrix(ctx, plan)
@@ -619,6 +626,8 @@ def main():
                                   cplx_run, krylov_m, newton_eval),
         "layout": {"format": args.fmt, "sell_sigma": sigma, "sell_split": split,
                    "stored_entries": info["stored"], "column_index_bits": index_bits,
+                   "encoding": encoding, "pair_table_entries": pair_table,
+                   "device_matrix_bytes": matrix_bytes,
                    "ranks_joined": ranks_joined},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
@@ -628,9 +637,10 @@ def main():
                                   "~92% reads, which the HBM sustains slightly faster, so frac can reach 1.0; "
                                   "ncu puts the C4 SpMV at 83% of the DRAM's theoretical peak "
                                   "(profiles/ncu_summary.json)",
-                     "bytes_per_unit": ("per SpMV launch: (s + i) per nonzero + s per row for x, out and "
-                                        "each epilogue vector (s = 8 or 16 bytes per scalar; i = 4, or "
-                                        f"2 + 4/64 with 16-bit column deltas -- here {index_bits}-bit)"),
+                     "bytes_per_unit": ("per SpMV launch: e per nonzero + s per row for x, out and "
+                                        "each epilogue vector (s = 8 or 16 bytes per scalar; e = s + 4 "
+                                        "(explicit), s + 2 + 4/64 (16-bit column deltas) or 1 (pair "
+                                        f"codes) -- here {encoding})"),
                      "launches_timed": sp["launches"],
                      "share_of_device_time": sp["ms"] / tot_ms if tot_ms else None,
                      "traffic_note": traffic_note},

@@ -84,6 +84,12 @@ typedef enum { PPF_STOP_FIXED_M = 0, PPF_STOP_EST = 1, PPF_STOP_TRUE_ERR = 2 } p
 typedef enum { PPF_CONVERGED = 0, PPF_MAX_ITER = 1, PPF_BREAKDOWN = 2 } ppf_term;
 typedef enum { PPF_POLY_CHEBYSHEV = 0, PPF_POLY_NEWTON = 1 } ppf_poly_kind;
 typedef enum { PPF_FMT_SELL = 0, PPF_FMT_CSR = 1 } ppf_format;
+/* device layout of the diagonal block's entries (ppf_plan_encoding) */
+typedef enum {
+  PPF_ENC_EXPLICIT = 0, /* 32-bit column indices + dtype values */
+  PPF_ENC_DELTA16 = 1,  /* 16-bit column deltas + per-slice-column base + dtype values */
+  PPF_ENC_PAIR8 = 2     /* one 8-bit code per entry into a table of <= 256 (col - row, value) pairs */
+} ppf_encoding;
 
 typedef struct ppf_ctx ppf_ctx;
 typedef struct ppf_plan ppf_plan;
@@ -173,6 +179,26 @@ ppf_status ppf_plan_info(const ppf_plan* plan, int64_t* n_local, int64_t* nnz,
  * chosen by ppf_plan_create whenever every slice-column spans <= 65535 --
  * stencils do -- unless the environment sets PPF_IDX16=0). */
 ppf_status ppf_plan_index_bits(const ppf_plan* plan, int* bits);
+/* ppf_plan_encoding: the layout ppf_mat_create will upload (ppf_encoding) and,
+ * for PPF_ENC_PAIR8, the table size (*ntab, else 0; either pointer may be
+ * NULL).  ppf_plan_create picks the narrowest lossless layout available:
+ *   PPF_ENC_PAIR8 for SELL-64 fp64 without sorting (sell_C = 64,
+ *     sell_sigma = 1) when the diagonal block's stored entries, padding
+ *     included, take at most 256 distinct (column - row, value) pairs -- a
+ *     banded matrix with constant diagonals, i.e. a constant-coefficient
+ *     stencil (the paper's Laplacian and convection-diffusion operators,
+ *     P:419): 1 byte per entry instead of 10-12 (an entry-dictionary
+ *     generalisation of value-indexed CSR; the multiply-adds are the same, in
+ *     the same order, as with the explicit layout);
+ *   else PPF_ENC_DELTA16 where ppf_plan_index_bits reports 16;
+ *   else PPF_ENC_EXPLICIT.
+ * The environment variable PPF_PAIR8=0 (PPF_IDX16=0) at plan time disables
+ * the pair codes (the deltas).  ppf_plan_set_encoding selects a wider layout
+ * than the one chosen (PPF_EINVAL if `enc` is not available for this plan);
+ * call it before ppf_plan_device_bytes / ppf_mat_create.  ppf_plan_index_bits
+ * reports the layout in force: 8 (pair codes), 16 or 32. */
+ppf_status ppf_plan_encoding(const ppf_plan* plan, int* enc, int* ntab);
+ppf_status ppf_plan_set_encoding(ppf_plan* plan, int enc);
 ppf_status ppf_plan_halo_count(const ppf_plan* plan, int peer, int64_t* count);
 ppf_status ppf_plan_halo_recv(const ppf_plan* plan, int peer, int64_t* global_idx);
 ppf_status ppf_plan_set_halo_send(ppf_plan* plan, int peer, int64_t count,

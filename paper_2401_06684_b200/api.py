@@ -161,10 +161,23 @@ class Plan:
         return dict(n_local=n.value, nnz=z.value, stored=s.value, halo_total=h.value)
 
     def index_bits(self) -> int:
-        """ppf_plan_index_bits: 16 (SELL-64 fp64 column deltas) or 32."""
+        """ppf_plan_index_bits: 8 (pair codes), 16 (column deltas) or 32."""
         b = C.c_int()
         check(_lib().ppf_plan_index_bits(self.h, C.byref(b)))
         return b.value
+
+    ENCODINGS = ("explicit", "delta16", "pair8")
+
+    def encoding(self) -> tuple[str, int]:
+        """ppf_plan_encoding: (layout name, pair-table size or 0)."""
+        e, t = C.c_int(), C.c_int()
+        check(_lib().ppf_plan_encoding(self.h, C.byref(e), C.byref(t)))
+        return self.ENCODINGS[e.value], t.value
+
+    def set_encoding(self, enc: str) -> "Plan":
+        """ppf_plan_set_encoding: select a wider layout than the one chosen."""
+        check(_lib().ppf_plan_set_encoding(self.h, self.ENCODINGS.index(enc)))
+        return self
 
     def halo_recv(self, peer: int) -> np.ndarray:
         cnt = C.c_int64()

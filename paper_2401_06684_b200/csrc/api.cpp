@@ -419,6 +419,70 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
       if (ok) {
         B.cb.swap(cb);
         B.d16.swap(d16);
+        p->enc = PPF_ENC_DELTA16;
+      }
+    }
+    // Pair codes (SELL-64 fp64, no sorting): every stored entry, padding
+    // included, becomes an 8-bit index into a table of (col - row, value)
+    // pairs when there are at most 256 distinct pairs -- the constant
+    // diagonals of a constant-coefficient stencil (C3: 7 pairs + the padding
+    // pair, C4: 7 + 1).  1 byte per entry instead of 10.06 (deltas) or 12
+    // (explicit); the kernel takes the pair from shared memory and does the
+    // same multiply-adds in the same order.  Padding is the pair (0, +0.0):
+    // column = row (clamped to the last row in the kernel), value 0, as the
+    // delta layout's padding.  PPF_PAIR8=0 keeps the wider layouts.
+    const char* ep = std::getenv("PPF_PAIR8");
+    if (C == 64 && p->dtype == PPF_R64 && p->sigma <= 1 && !(ep && ep[0] == '0') && stored > 0) {
+      // open-addressing table keyed by (offset, value bits); 1024 slots for
+      // at most 256 keys
+      constexpr int SLOTS = 1024;
+      std::vector<int> slot(SLOTS, -1);
+      std::vector<int32_t> toff;
+      std::vector<double> tval;
+      std::vector<uint64_t> tbits;
+      std::vector<uint8_t> code(size_t(stored), 0);
+      bool ok = true;
+      auto code_of = [&](int64_t off, double v) -> int {
+        uint64_t bits;
+        std::memcpy(&bits, &v, 8);
+        uint64_t h = (uint64_t(off) * 0x9E3779B97F4A7C15ull) ^ (bits * 0xC2B2AE3D27D4EB4Full);
+        h ^= h >> 29;
+        for (int probe = 0; probe < SLOTS; ++probe) {
+          const int sl = int((h + uint64_t(probe)) & (SLOTS - 1));
+          const int c = slot[sl];
+          if (c < 0) {
+            if (toff.size() == 256) return -1;
+            slot[sl] = int(toff.size());
+            toff.push_back(int32_t(off));
+            tval.push_back(v);
+            tbits.push_back(bits);
+            return slot[sl];
+          }
+          if (toff[c] == off && tbits[c] == bits) return c;
+        }
+        return -1;
+      };
+      for (int64_t s = 0; s < B.nslices && ok; ++s) {
+        const int64_t w = (B.ptr[s + 1] - B.ptr[s]) / C;
+        for (int64_t k = 0; k < w && ok; ++k) {
+          for (int lane = 0; lane < C; ++lane) {
+            const int64_t pp = s * C + lane;
+            const size_t idx = size_t(B.ptr[s] + k * C + lane);
+            const bool real = pp < n_local && k < dlen[pp];
+            const int c = real ? code_of(int64_t(B.col[idx]) - pp, B.val[idx]) : code_of(0, 0.0);
+            if (c < 0) {
+              ok = false;
+              break;
+            }
+            code[idx] = uint8_t(c);
+          }
+        }
+      }
+      if (ok) {
+        B.code8.swap(code);
+        B.tab_off.swap(toff);
+        B.tab_val.swap(tval);
+        p->enc = PPF_ENC_PAIR8;
       }
     }
   }
@@ -430,7 +494,26 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
 ppf_status ppf_plan_index_bits(const ppf_plan* p, int* bits) {
   PPF_API_BEGIN
   PPF_REQUIRE(p && bits, "NULL argument");
-  *bits = p->diag.d16.empty() ? 32 : 16;
+  *bits = p->enc == PPF_ENC_PAIR8 ? 8 : p->enc == PPF_ENC_DELTA16 ? 16 : 32;
+  PPF_API_END
+}
+
+ppf_status ppf_plan_encoding(const ppf_plan* p, int* enc, int* ntab) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p, "NULL plan");
+  if (enc) *enc = p->enc;
+  if (ntab) *ntab = p->enc == PPF_ENC_PAIR8 ? int(p->diag.tab_off.size()) : 0;
+  PPF_API_END
+}
+
+ppf_status ppf_plan_set_encoding(ppf_plan* p, int enc) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p, "NULL plan");
+  const bool avail = enc == PPF_ENC_EXPLICIT ||
+                     (enc == PPF_ENC_DELTA16 && !p->diag.d16.empty()) ||
+                     (enc == PPF_ENC_PAIR8 && !p->diag.code8.empty());
+  PPF_REQUIRE(avail, "encoding not available for this plan");
+  p->enc = enc;
   PPF_API_END
 }
 
@@ -473,17 +556,26 @@ static Layout layout_of(const ppf_plan* p) {
   size_t o = 0;
   L.ptr = o;
   o += al256(p->diag.ptr.size() * 8);
-  L.col = o;   // 32-bit indices, or the 16-bit deltas + per-(slice, column) bases
-  if (p->diag.d16.empty()) {
-    o += al256(p->diag.col.size() * 4);
+  L.col = o;   // 32-bit indices, or the 16-bit deltas + per-(slice, column) bases,
+               // or the pair codes + the pair table's offsets (L.cb) and values (L.val)
+  if (p->enc == PPF_ENC_PAIR8) {
+    o += al256(p->diag.code8.size());
     L.cb = o;
+    o += al256(p->diag.tab_off.size() * 4);
+    L.val = o;
+    o += al256(p->diag.tab_val.size() * 8);
   } else {
-    o += al256(p->diag.d16.size() * 2);
-    L.cb = o;
-    o += al256(p->diag.cb.size() * 4);
+    if (p->enc == PPF_ENC_EXPLICIT) {
+      o += al256(p->diag.col.size() * 4);
+      L.cb = o;
+    } else {
+      o += al256(p->diag.d16.size() * 2);
+      L.cb = o;
+      o += al256(p->diag.cb.size() * 4);
+    }
+    L.val = o;
+    o += al256(p->diag.col.size() * sc);
   }
-  L.val = o;
-  o += al256(p->diag.col.size() * sc);
   L.perm = o;
   o += al256(p->diag.perm.size() * 4);
   L.hrows = o;
@@ -543,13 +635,19 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     if (n) PPF_CUDA(cudaMemcpyAsync(b + off, src, n, cudaMemcpyHostToDevice, st));
   };
   up(L.ptr, p->diag.ptr.data(), p->diag.ptr.size() * 8);
-  if (p->diag.d16.empty()) {
-    up(L.col, p->diag.col.data(), p->diag.col.size() * 4);
+  if (p->enc == PPF_ENC_PAIR8) {
+    up(L.col, p->diag.code8.data(), p->diag.code8.size());
+    up(L.cb, p->diag.tab_off.data(), p->diag.tab_off.size() * 4);
+    up(L.val, p->diag.tab_val.data(), p->diag.tab_val.size() * 8);
   } else {
-    up(L.col, p->diag.d16.data(), p->diag.d16.size() * 2);
-    up(L.cb, p->diag.cb.data(), p->diag.cb.size() * 4);
+    if (p->enc == PPF_ENC_EXPLICIT) {
+      up(L.col, p->diag.col.data(), p->diag.col.size() * 4);
+    } else {
+      up(L.col, p->diag.d16.data(), p->diag.d16.size() * 2);
+      up(L.cb, p->diag.cb.data(), p->diag.cb.size() * 4);
+    }
+    up(L.val, p->diag.val.data(), p->diag.col.size() * sc);
   }
-  up(L.val, p->diag.val.data(), p->diag.col.size() * sc);
   up(L.perm, p->diag.perm.data(), p->diag.perm.size() * 4);
   up(L.hrows, p->halo.rows.data(), p->halo.rows.size() * 4);
   up(L.hptr, p->halo.ptr.data(), p->halo.ptr.size() * 8);
@@ -583,14 +681,22 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
   m->rank = p->rank;
   m->nslices = p->diag.nslices;
   m->d_ptr = reinterpret_cast<const int64_t*>(b + L.ptr);
-  if (p->diag.d16.empty()) {
-    m->d_col = reinterpret_cast<const int32_t*>(b + L.col);
+  m->d_col = nullptr;
+  m->d_val = nullptr;
+  if (p->enc == PPF_ENC_PAIR8) {
+    m->d_code8 = reinterpret_cast<const uint8_t*>(b + L.col);
+    m->d_tab_off = reinterpret_cast<const int32_t*>(b + L.cb);
+    m->d_tab_val = reinterpret_cast<const double*>(b + L.val);
+    m->ntab = int(p->diag.tab_off.size());
   } else {
-    m->d_col = nullptr;
-    m->d_d16 = reinterpret_cast<const uint16_t*>(b + L.col);
-    m->d_cb = reinterpret_cast<const int32_t*>(b + L.cb);
+    if (p->enc == PPF_ENC_EXPLICIT) {
+      m->d_col = reinterpret_cast<const int32_t*>(b + L.col);
+    } else {
+      m->d_d16 = reinterpret_cast<const uint16_t*>(b + L.col);
+      m->d_cb = reinterpret_cast<const int32_t*>(b + L.cb);
+    }
+    m->d_val = b + L.val;
   }
-  m->d_val = b + L.val;
   m->d_perm = p->diag.perm.empty() ? nullptr : reinterpret_cast<const int32_t*>(b + L.perm);
   {
     const double avg = double(m->stored) / double(std::max<int64_t>(1, p->n_local));

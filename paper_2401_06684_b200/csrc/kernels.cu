@@ -260,7 +260,13 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
 
 // two rows per lane, 128-bit loads of (val, val) and (col, col); C = 64, fp64;
 // KS warps per slice as in sell1_kernel
-template <int KS, bool ACC = false, bool IDX16 = false>
+//
+// ENC (the plan's ppf_encoding): 0 explicit 32-bit columns + values, 1 16-bit
+// column deltas + values, 2 pair codes: one byte per entry indexing a table of
+// (col - row, value) pairs held in shared memory (the table is plan data,
+// read before the PDL wait).  The pair-code loop does the same multiply-adds
+// in the same order as the explicit layout.
+template <int KS, bool ACC = false, int ENC = 0>
 __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
@@ -268,7 +274,13 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ out, EpiT<double> e,
                                                     bool has_x, const uint16_t* __restrict__ d16,
-                                                    const int32_t* __restrict__ cbase) {
+                                                    const int32_t* __restrict__ cbase,
+                                                    const uint8_t* __restrict__ code8,
+                                                    const int32_t* __restrict__ tab_off,
+                                                    const double* __restrict__ tab_val, int ntab) {
+  constexpr bool IDX16 = ENC == 1;
+  __shared__ double s_tv[ENC == 2 ? 256 : 1];
+  __shared__ int s_to[ENC == 2 ? 256 : 1];
   pdl_release();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
@@ -287,9 +299,14 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
     // time by the unrolled loop (C4 309 -> 302 ms, C3 SpMV 6.15 -> 6.30 TB/s;
     // in sell1_kernel it cost C5 13% and C7 9%, so it is sell2-only).  One
     // 128-B line per 8 lanes of values (16 B each) / 16 lanes of indices.
-    if ((lane & 7) == 0)
+    if constexpr (ENC == 2) {
+      // the codes: 64 B per column of the slice
+      for (int o = 128 * lane; o < 64 * (k1 - k0); o += 32 * 128) prefetch_l2(code8 + base + 64 * k0 + o);
+    } else if ((lane & 7) == 0) {
       for (int k = k0; k < k1; ++k) prefetch_l2(val + base + 64 * k + 2 * lane);
-    if constexpr (IDX16) {
+    }
+    if constexpr (ENC == 2) {
+    } else if constexpr (IDX16) {
       // 16-bit deltas: 128 B per column of the slice; the bases: 4 B per column
       if (lane == 0) {
         for (int k = k0; k < k1; ++k) prefetch_l2(d16 + base + 64 * k);
@@ -299,6 +316,13 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
       if ((lane & 15) == 0)
         for (int k = k0; k < k1; ++k) prefetch_l2(col + base + 64 * k + 2 * lane);
     }
+  }
+  if constexpr (ENC == 2) {
+    for (int i = threadIdx.x; i < ntab; i += blockDim.x) {
+      s_tv[i] = __ldg(tab_val + i);
+      s_to[i] = __ldg(tab_off + i);
+    }
+    __syncthreads();
   }
   pdl_wait();
   // the slice's rows of the epilogue vectors and of x (its own rows: the
@@ -317,7 +341,22 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
     // (measured: the compiler's own schedule of this loop, at 32 registers
     // and full occupancy, streams C3/C4 at 97-98% of the measured copy
     // bandwidth; the forced batching of sell1_kernel drops it to 72%)
-    if constexpr (IDX16) {
+    if constexpr (ENC == 2) {
+      // two codes per lane (rows r0, r0 + 1: low, high byte); column =
+      // row + offset, clamped to the last row for the padding pair of the
+      // lanes past n in the last slice
+      const uint16_t* cp = reinterpret_cast<const uint16_t*>(code8 + base) + lane;
+      const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const unsigned cc = __ldg(cp + 32 * k);
+        const int e0 = int(cc & 0xffu), e1 = int(cc >> 8);
+        const int c0 = min(r0i + s_to[e0], nm1);
+        const int c1 = min(r0i + 1 + s_to[e1], nm1);
+        a0 = fma(s_tv[e0], __ldg(x + c0), a0);
+        a1 = fma(s_tv[e1], __ldg(x + c1), a1);
+      }
+    } else if constexpr (IDX16) {
       // column = row + base(s, k) + 16-bit delta (the plan's encoding),
       // clamped to [0, n): padding slots (val 0, delta 0) of rows near the
       // ends, and of the lanes past n in the last slice, then read in bounds
@@ -1122,19 +1161,24 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
       const int bt = KS > 4 ? 256 : 128;
       const int64_t spb2 = (bt / 32) / KS;
       const int b2 = int((A->nslices + spb2 - 1) / spb2);
-#define PPF_S2(K)                                                                            \
-  launch_pdl(sell2_kernel<K, ACC, false>, b2, bt, st, A->nslices, A->n_local, A->d_ptr, A->d_col, \
-             reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb)
-#define PPF_S2D(K)                                                                           \
-  launch_pdl(sell2_kernel<K, ACC, true>, b2, bt, st, A->nslices, A->n_local, A->d_ptr, A->d_col, \
-             reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb)
-      if (A->d_d16) {
+#define PPF_S2E(K, E)                                                                         \
+  launch_pdl(sell2_kernel<K, ACC, E>, b2, bt, st, A->nslices, A->n_local, A->d_ptr, A->d_col,   \
+             reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb,         \
+             A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab)
+#define PPF_S2(K) PPF_S2E(K, 0)
+#define PPF_S2D(K) PPF_S2E(K, 1)
+#define PPF_S2P(K) PPF_S2E(K, 2)
+      if (A->d_code8) {
+        PPF_KS(PPF_S2P)
+      } else if (A->d_d16) {
         PPF_KS(PPF_S2D)
       } else {
         PPF_KS(PPF_S2)
       }
 #undef PPF_S2
 #undef PPF_S2D
+#undef PPF_S2P
+#undef PPF_S2E
       post_launch("sell2_kernel");
       return;
     }

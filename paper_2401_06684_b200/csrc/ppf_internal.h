@@ -105,6 +105,15 @@ struct HostBlock {
   // (val 0).  Empty unless every (s, k) spans <= 65535 in (col - row).
   std::vector<uint16_t> d16;
   std::vector<int32_t> cb;
+  // SELL-64 fp64 (no sorting) with dictionary-coded entries (round 2, "pair
+  // codes"): entry (s, k, t) of row r = C s + t is the pair
+  // (tab_off[c], tab_val[c]) with c = code8[ptr[s] + C k + t]: column
+  // r + tab_off[c] (clamped to the last row for the padding pair (0, +0.0)),
+  // value tab_val[c].  Empty unless the block's entries (padding included)
+  // take <= 256 distinct (col - row, value bits) pairs.
+  std::vector<uint8_t> code8;
+  std::vector<int32_t> tab_off;
+  std::vector<double> tab_val;
 };
 
 struct HostHalo {
@@ -123,6 +132,7 @@ struct ppf_plan {
   std::vector<int64_t> bounds;
   ppf_format fmt;
   int C, sigma;
+  int enc = PPF_ENC_EXPLICIT;   // device layout of the diagonal block (ppf_encoding)
   ppf::HostBlock diag;
   ppf::HostHalo halo;
   std::vector<std::vector<int64_t>> recv;   // per peer: global indices received (sorted)
@@ -149,6 +159,10 @@ struct ppf_mat {
   const int32_t* d_perm;    // null unless sigma > 1
   const uint16_t* d_d16 = nullptr;  // 16-bit column deltas (SELL), with d_cb
   const int32_t* d_cb = nullptr;    // per (slice, column) base offset (col - row)
+  const uint8_t* d_code8 = nullptr; // pair codes (SELL-64 fp64), with d_tab_off / d_tab_val
+  const int32_t* d_tab_off = nullptr;
+  const double* d_tab_val = nullptr;
+  int ntab = 0;
   int csr_group;            // lanes per row for the CSR kernel
   int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks
   int64_t sell_heavy = 0;   // leading slices given a whole block each (see sell_heavy_prefix)

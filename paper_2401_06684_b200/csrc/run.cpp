@@ -398,9 +398,11 @@ struct Runner {
   void spmv_now(const void* x, void* out, const Epi& e) {
     // algorithmic bytes: values + column indices once, x gathered once, out
     // written once, z and u streamed once
-    // (index bytes per entry: 4, or 2 + 4/C with the 16-bit column deltas)
+    // (index bytes per entry: 4, or 2 + 4/C with the 16-bit column deltas;
+    // with the pair codes one byte per entry carries column and value)
     const double idxb = A->d_d16 ? 2.0 + 4.0 / double(A->C) : 4.0;
-    const double bytes = (double(sc) + idxb) * double(A->nnz) +
+    const double entb = A->d_code8 ? 1.0 : double(sc) + idxb;
+    const double bytes = entb * double(A->nnz) +
                          double(sc) * double(n) * (2 + (e.z ? 1 : 0) + (e.u ? 1 : 0));
     if (A->nranks > 1) {
       // pack + overlapped exchange + diagonal block + halo block; timed as one

@@ -55,17 +55,22 @@ def ragged_matrix(n, seed, complex_=False):
 FORMATS = [("sell", 32, 1), ("sell", 64, 1), ("sell", 32, 128), ("csr", 32, 1)]
 
 
-@pytest.mark.parametrize("idx", ["16", "32"])
+@pytest.mark.parametrize("idx", ["8", "16", "32"])
 @pytest.mark.parametrize("fmt,C_,sig", FORMATS)
 @pytest.mark.parametrize("which", ["lap3", "convdiff3", "ragged", "ragged_c", "wilson", "wide_cols"])
 def test_spmv_parity(ctx, fmt, C_, sig, which, idx, monkeypatch):
-    """Every format against SciPy; SELL-32/64 with the 16-bit column deltas
-    (PPF_IDX16, the default where every (slice, column) spans <= 65535
-    columns) and with 32-bit indices; "wide_cols" has columns spread over
-    200,000 so the plan must fall back to 32-bit indices."""
-    monkeypatch.setenv("PPF_IDX16", "1" if idx == "16" else "0")
-    if idx == "16" and not (fmt == "sell" and sig == 1):
-        pytest.skip("16-bit deltas exist for SELL without sorting")
+    """Every format against SciPy; SELL-64 fp64 with the pair codes (idx 8:
+    PPF_PAIR8, the default for the stencils; the ragged/random matrices fall
+    back), SELL-32/64 with the 16-bit column deltas (PPF_IDX16, the default
+    where every (slice, column) spans <= 65535 columns) and with 32-bit
+    indices; "wide_cols" has columns spread over 200,000 so the plan must
+    fall back to 32-bit indices."""
+    monkeypatch.setenv("PPF_IDX16", "0" if idx == "32" else "1")
+    monkeypatch.setenv("PPF_PAIR8", "1" if idx == "8" else "0")
+    if idx != "32" and not (fmt == "sell" and sig == 1):
+        pytest.skip("16-bit deltas / pair codes exist for SELL without sorting")
+    if idx == "8" and C_ != 64:
+        pytest.skip("pair codes: SELL-64 fp64")
     if which == "lap3":
         A = ops.laplacian(13, 3)            # 2197 rows: ragged tail for C = 32 and 64
     elif which == "convdiff3":
@@ -80,7 +85,10 @@ def test_spmv_parity(ctx, fmt, C_, sig, which, idx, monkeypatch):
         A = ops.wilson_dirac(3, -1.0, seed=4)
     if np.iscomplexobj(A.val) and C_ == 64:
         pytest.skip("C = 64 is the fp64 two-rows-per-lane layout")
-    M = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt=fmt, C_=C_, sigma=sig))
+    plan = pp.Plan.from_csr(A, fmt=fmt, C_=C_, sigma=sig)
+    if idx == "8" and which in ("lap3", "convdiff3"):
+        assert plan.encoding() == ("pair8", 8)
+    M = pp.Matrix(ctx, plan)
     rng = np.random.default_rng(7)
     x = rng.standard_normal(A.n)
     if np.iscomplexobj(A.val):
@@ -92,6 +100,46 @@ def test_spmv_parity(ctx, fmt, C_, sig, which, idx, monkeypatch):
     got = host(yd)
     absA = abs(A.to_scipy()) @ np.abs(x)
     assert np.all(np.abs(got - ref) <= 1e-14 * absA + 1e-300)
+
+
+@pytest.mark.parametrize("ks", [1, 2, 4])
+@pytest.mark.parametrize("shape", [(13, 3, None), (64, 2, None), (19, 3, (10.0, 10.0, 10.0)),
+                                   (47, 3, (10.0, 5.0, 2.5)), (1, 3, None), (2, 2, None)])
+def test_pair_codes_bitwise(ctx, shape, ks):
+    """The pair-code layout does the explicit layout's multiply-adds in the
+    same order on the same values and columns: the SpMV and the fused
+    Clenshaw chain (z, u, x epilogue terms) must be bitwise identical across
+    pair8 / delta16 / explicit, for sizes spanning many 64-row slices with a
+    ragged last slice, a 1-row and a 4-row matrix, warps split per slice, and
+    an anisotropic convection (distinct values per direction)."""
+    N, dim, beta = shape
+    A = ops.laplacian(N, dim) if beta is None else ops.convdiff(N, 3, beta)
+    rng = np.random.default_rng(N * 10 + dim)
+    x = rng.standard_normal(A.n)
+    outs = {}
+    for enc in ("pair8", "delta16", "explicit"):
+        plan = pp.Plan.from_csr(A, fmt="sell", C_=64)
+        if enc != "pair8":
+            try:
+                plan.set_encoding(enc)
+            except RuntimeError:
+                assert enc == "delta16"
+                continue
+        else:
+            assert plan.encoding()[0] == "pair8"
+        M = pp.Matrix(ctx, plan)
+        M.set_split(ks)
+        yd = torch.full_like(dev(x), float("nan"))
+        M.spmv(dev(x), yd)
+        a, b = 0.5, 20.0
+        q = pp.Poly.chebyshev(a, b, 7)
+        outs[enc] = (host(yd), host(q.apply(ctx, M, dev(x))))
+    ref = A.to_scipy() @ x
+    absA = abs(A.to_scipy()) @ np.abs(x)
+    for enc, (y, c) in outs.items():
+        assert np.array_equal(y, outs["explicit"][0]), enc
+        assert np.array_equal(c, outs["explicit"][1]), enc
+    assert np.all(np.abs(outs["pair8"][0] - ref) <= 1e-14 * absA + 1e-300)
 
 
 @pytest.mark.parametrize("ks", [1, 2, 4, 8])

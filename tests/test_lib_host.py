@@ -261,12 +261,14 @@ def test_plan_sell_layout_sizes():
             assert info["stored"] == A.nnz
         else:
             assert A.nnz <= info["stored"] <= 7 * (A.n + C_)
-        # 8-byte values + 4-byte indices, or 2-byte deltas (+ a 4-byte base per
-        # 64 entries) where the SELL-64 plan encodes them in 16 bits
+        # 8-byte values + 4-byte indices, or one byte per entry where the
+        # SELL-64 plan stores the stencil's entries as pair codes
         ib = p.index_bits()
-        assert ib == (16 if (fmt, C_, sig) == ("sell", 64, 1) else 32)   # fp64 operator
-        per = 12 if ib == 32 else 10
+        assert ib == (8 if (fmt, C_, sig) == ("sell", 64, 1) else 32)   # fp64 operator
+        per = {32: 12, 16: 10, 8: 1}[ib]
         assert p.device_bytes() >= info["stored"] * per
+        if ib == 8:
+            assert p.device_bytes() < info["stored"] * 2
 
 
 def test_plan_rejects_bad_input():
@@ -384,6 +386,7 @@ def test_plan_index_bits_choice(monkeypatch):
     including the 256^3 conv-diff of C4 whose offsets reach N^2 = 65536 but
     span at most N^2 - 1 within one slice-column), 32-bit indices otherwise
     (columns spread over 200,000) or when PPF_IDX16=0."""
+    monkeypatch.setenv("PPF_PAIR8", "0")
     A = ops.convdiff(40, 3, (10.0, 10.0, 10.0))
     assert Plan.from_csr(A, fmt="sell", C_=64).index_bits() == 16
     assert Plan.from_csr(A, fmt="sell", C_=32).index_bits() == 32          # fp64 SELL-32: no
@@ -403,3 +406,52 @@ def test_plan_index_bits_choice(monkeypatch):
     from inputs.operators import CSR
     R = CSR(n, rp, cols[keep], np.ones(int(rp[-1])))
     assert Plan.from_csr(R, fmt="sell", C_=64).index_bits() == 32
+
+
+def test_plan_pair_codes_choice(monkeypatch):
+    """ppf_plan_encoding: SELL-64 fp64 without sorting stores each entry as an
+    8-bit code into a table of (col - row, value) pairs when there are at most
+    256 distinct pairs, padding (0, 0.0) included: the constant-coefficient
+    stencils (7 pairs + padding); complex, sorted, SELL-32, CSR and
+    variable-coefficient operators keep the wider layouts.  PPF_PAIR8=0 and
+    ppf_plan_set_encoding select a wider one; an unavailable one is EINVAL."""
+    from inputs.operators import CSR
+    for A in (ops.convdiff(40, 3, (10.0, 10.0, 10.0)), ops.laplacian(30, 3), ops.laplacian(32, 2)):
+        p = Plan.from_csr(A, fmt="sell", C_=64)
+        enc, ntab = p.encoding()
+        nd = 2 * (3 if A.n in (64000, 27000) else 2) + 1     # distinct diagonals
+        assert enc == "pair8" and ntab == nd + 1, (enc, ntab)
+        assert p.index_bits() == 8
+        stored = p.info()["stored"]
+        b8 = p.device_bytes()
+        p.set_encoding("delta16")
+        assert p.encoding() == ("delta16", 0) and p.index_bits() == 16
+        assert p.device_bytes() >= 10 * stored > 5 * b8
+        p.set_encoding("explicit")
+        assert p.index_bits() == 32 and p.device_bytes() >= 12 * stored
+        p.set_encoding("pair8")                      # back: still available
+        assert p.device_bytes() == b8
+    A = ops.convdiff(20, 3, (10.0, 10.0, 10.0))
+    assert Plan.from_csr(A, fmt="sell", C_=32).encoding()[0] == "explicit"
+    assert Plan.from_csr(A, fmt="csr").encoding()[0] == "explicit"
+    W = ops.wilson_dirac(4, -1.0, seed=5)
+    pw = Plan.from_csr(W, fmt="sell", C_=32)
+    assert pw.encoding()[0] == "delta16"
+    with pytest.raises(RuntimeError):
+        pw.set_encoding("pair8")
+    # variable coefficients: 257+ distinct values -> the deltas
+    V = CSR(A.n, A.row_ptr, A.col, A.val * (1.0 + 1e-3 * (np.arange(A.nnz) % 300)))
+    assert Plan.from_csr(V, fmt="sell", C_=64).encoding()[0] == "delta16"
+    # exactly 256 distinct pairs (padding included) still fits; 257 does not
+    n = 64 * 8
+    rp = np.arange(n + 1, dtype=np.int64)
+    for k in (256, 257):
+        vals = 1.0 + (np.arange(n) % k)                  # k values on the diagonal
+        D = CSR(n, rp, np.arange(n, dtype=np.int64), vals)
+        enc = Plan.from_csr(D, fmt="sell", C_=64).encoding()
+        # a diagonal matrix has no padding: k pairs
+        assert (enc[0] == "pair8") == (k <= 256)
+        if enc[0] == "pair8":
+            assert enc[1] == k
+    monkeypatch.setenv("PPF_PAIR8", "0")
+    assert Plan.from_csr(ops.laplacian(30, 3), fmt="sell", C_=64).encoding()[0] == "delta16"
