@@ -260,13 +260,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 16 ? 3 : 1) sell1_kernel(int
 
 // two rows per lane, 128-bit loads of (val, val) and (col, col); C = 64, fp64;
 // KS warps per slice as in sell1_kernel
-//
-// ENC (the plan's ppf_encoding): 0 explicit 32-bit columns + values, 1 16-bit
-// column deltas + values, 2 pair codes: one byte per entry indexing a table of
-// (col - row, value) pairs held in shared memory (the table is plan data,
-// read before the PDL wait).  The pair-code loop does the same multiply-adds
-// in the same order as the explicit layout.
-template <int KS, bool ACC = false, int ENC = 0>
+template <int KS, bool ACC = false, bool IDX16 = false>
 __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const int32_t* __restrict__ col,
@@ -274,13 +268,7 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ out, EpiT<double> e,
                                                     bool has_x, const uint16_t* __restrict__ d16,
-                                                    const int32_t* __restrict__ cbase,
-                                                    const uint8_t* __restrict__ code8,
-                                                    const int32_t* __restrict__ tab_off,
-                                                    const double* __restrict__ tab_val, int ntab) {
-  constexpr bool IDX16 = ENC == 1;
-  __shared__ double s_tv[ENC == 2 ? 256 : 1];
-  __shared__ int s_to[ENC == 2 ? 256 : 1];
+                                                    const int32_t* __restrict__ cbase) {
   pdl_release();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
@@ -299,14 +287,9 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
     // time by the unrolled loop (C4 309 -> 302 ms, C3 SpMV 6.15 -> 6.30 TB/s;
     // in sell1_kernel it cost C5 13% and C7 9%, so it is sell2-only).  One
     // 128-B line per 8 lanes of values (16 B each) / 16 lanes of indices.
-    if constexpr (ENC == 2) {
-      // the codes: 64 B per column of the slice
-      for (int o = 128 * lane; o < 64 * (k1 - k0); o += 32 * 128) prefetch_l2(code8 + base + 64 * k0 + o);
-    } else if ((lane & 7) == 0) {
+    if ((lane & 7) == 0)
       for (int k = k0; k < k1; ++k) prefetch_l2(val + base + 64 * k + 2 * lane);
-    }
-    if constexpr (ENC == 2) {
-    } else if constexpr (IDX16) {
+    if constexpr (IDX16) {
       // 16-bit deltas: 128 B per column of the slice; the bases: 4 B per column
       if (lane == 0) {
         for (int k = k0; k < k1; ++k) prefetch_l2(d16 + base + 64 * k);
@@ -316,13 +299,6 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
       if ((lane & 15) == 0)
         for (int k = k0; k < k1; ++k) prefetch_l2(col + base + 64 * k + 2 * lane);
     }
-  }
-  if constexpr (ENC == 2) {
-    for (int i = threadIdx.x; i < ntab; i += blockDim.x) {
-      s_tv[i] = __ldg(tab_val + i);
-      s_to[i] = __ldg(tab_off + i);
-    }
-    __syncthreads();
   }
   pdl_wait();
   // the slice's rows of the epilogue vectors and of x (its own rows: the
@@ -341,22 +317,7 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
     // (measured: the compiler's own schedule of this loop, at 32 registers
     // and full occupancy, streams C3/C4 at 97-98% of the measured copy
     // bandwidth; the forced batching of sell1_kernel drops it to 72%)
-    if constexpr (ENC == 2) {
-      // two codes per lane (rows r0, r0 + 1: low, high byte); column =
-      // row + offset, clamped to the last row for the padding pair of the
-      // lanes past n in the last slice
-      const uint16_t* cp = reinterpret_cast<const uint16_t*>(code8 + base) + lane;
-      const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
-#pragma unroll 4
-      for (int k = k0; k < k1; ++k) {
-        const unsigned cc = __ldg(cp + 32 * k);
-        const int e0 = int(cc & 0xffu), e1 = int(cc >> 8);
-        const int c0 = min(r0i + s_to[e0], nm1);
-        const int c1 = min(r0i + 1 + s_to[e1], nm1);
-        a0 = fma(s_tv[e0], __ldg(x + c0), a0);
-        a1 = fma(s_tv[e1], __ldg(x + c1), a1);
-      }
-    } else if constexpr (IDX16) {
+    if constexpr (IDX16) {
       // column = row + base(s, k) + 16-bit delta (the plan's encoding),
       // clamped to [0, n): padding slots (val 0, delta 0) of rows near the
       // ends, and of the lanes past n in the last slice, then read in bounds
@@ -385,6 +346,136 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
         a0 = fma(v.x, __ldg(x + c.x), a0);
         a1 = fma(v.y, __ldg(x + c.y), a1);
       }
+    }
+  }
+  if constexpr (KS > 1) {
+    __shared__ double2 red[8][32];
+    red[warp][lane] = make_double2(a0, a1);
+    __syncthreads();
+    if (part != 0) return;
+#pragma unroll
+    for (int p = 1; p < KS; ++p) {
+      const double2 t = red[warp + p][lane];
+      a0 += t.x;
+      a1 += t.y;
+    }
+  }
+  if (!live) return;
+  const int64_t r0 = slice * 64 + 2 * lane;
+  if (r0 + 1 < n) {
+    double2 r;
+    r.x = e.s_ax * a0;
+    r.y = e.s_ax * a1;
+    if (has_x) {
+      const double2 xv = __ldg(reinterpret_cast<const double2*>(e.xe + r0));
+      r.x = fma(e.s_x, xv.x, r.x);
+      r.y = fma(e.s_x, xv.y, r.y);
+    }
+    if (e.z) {
+      const double2 zv = __ldg(reinterpret_cast<const double2*>(e.z + r0));
+      r.x = fma(e.s_z, zv.x, r.x);
+      r.y = fma(e.s_z, zv.y, r.y);
+    }
+    if (e.u) {
+      const double2 uv = __ldg(reinterpret_cast<const double2*>(e.u + r0));
+      r.x = fma(e.s_u, uv.x, r.x);
+      r.y = fma(e.s_u, uv.y, r.y);
+    }
+    *reinterpret_cast<double2*>(out + r0) = r;
+    if constexpr (ACC) {
+      acc_update(e, r0, r.x);
+      acc_update(e, r0 + 1, r.y);
+    }
+  } else if (r0 < n) {
+    const double r = epilogue(e, a0, x, r0, has_x);
+    out[r0] = r;
+    if constexpr (ACC) acc_update(e, r0, r);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SELL-64 fp64 SpMV + fused epilogue on pair codes (PPF_ENC_PAIR8): entry
+// (s, k, t) is the pair (off, val) = table[code8[ptr[s] + 64 k + t]],
+// column = row + off.  Lane i of the slice's warp takes rows 64 s + 2i and
+// 64 s + 2i + 1 (one 16-bit load gives both codes of a column), as in
+// sell2_kernel: the two gathers of a column then fall on the same lines (the
+// second an L1 hit).
+//
+// With 1 byte per entry the matrix is ~18% of the DRAM bytes (C4: 117 of the
+// 654 MB per chain SpMV) and DRAM is no longer the bound: at 155-160 us per
+// C4 SpMV (4.1 TB/s of DRAM traffic, 1.02x the algorithmic bytes) the L1
+// data pipe is 57% busy (a fifth of it the table lookups), DRAM 51%, and
+// long-scoreboard stalls on the x gathers dominate.  Measured on C4 (ncu, per
+// SpMV) and dropped:
+//  * rows i and i + 32 per lane (every warp access 32 consecutive rows,
+//    fewer L1 wavefronts): L1 hit rate 49 -> 24%, 155 -> 168 us;
+//  * one aligned 16-B load of x[c], x[c + 1] where both rows take the same
+//    pair at an even column (5 of C4's 7 columns, fewer L1 sectors): the
+//    branch cost more than it saved, 160 -> 187 us;
+//  * all codes of 8 columns, then all gathers, then the FMAs (64 registers,
+//    half the warps): 195 us;
+//  * a persistent grid, each CTA walking a contiguous range of slices (L1
+//    reuse of the +-1 / +-N neighbours): the far (+-N^2) neighbours' reuse
+//    distance across CTAs outgrew L2 -- DRAM reads 0.52 -> 0.96 GB, 227 us.
+// The table is held as (value, offset bits) pairs: one 16-B shared load per
+// lookup, a broadcast where a column's codes agree.  KS warps per slice as in
+// sell2_kernel.  The multiply-adds are the explicit layout's, in its order
+// (bitwise-identical results).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ int pair_off(double2 p) { return int(__double_as_longlong(p.y)); }
+
+template <int KS, bool ACC = false>
+__global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
+                                                    const int64_t* __restrict__ sptr,
+                                                    const uint8_t* __restrict__ code8,
+                                                    const int32_t* __restrict__ tab_off,
+                                                    const double* __restrict__ tab_val, int ntab,
+                                                    const double* __restrict__ x,
+                                                    double* __restrict__ out, EpiT<double> e,
+                                                    bool has_x) {
+  __shared__ double2 s_tab[256];
+  pdl_release();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
+  const int part = warp % KS;
+  const bool live = slice < nslices;
+  double a0 = 0.0, a1 = 0.0;
+  int64_t base = 0;
+  int k0 = 0, k1 = 0;
+  if (live) {
+    base = sptr[slice];
+    const int w = int((sptr[slice + 1] - base) >> 6);
+    k0 = part * w / KS;
+    k1 = (part + 1) * w / KS;
+    // the slice's codes (64 B per column) into L2 before the PDL wait
+    for (int o = 128 * lane; o < 64 * (k1 - k0); o += 32 * 128) prefetch_l2(code8 + base + 64 * k0 + o);
+  }
+  for (int i = threadIdx.x; i < ntab; i += blockDim.x)
+    s_tab[i] = make_double2(__ldg(tab_val + i), __longlong_as_double((long long)__ldg(tab_off + i)));
+  __syncthreads();
+  pdl_wait();
+  // the slice's rows of the epilogue vectors and of x: one line per 8 lanes
+  if (live && part == 0 && (lane & 7) == 0) {
+    const int64_t r0 = slice * 64 + 2 * lane;
+    if (r0 < n) {
+      prefetch_l2(x + r0);
+      if (e.z) prefetch_l2(e.z + r0);
+      if (e.u) prefetch_l2(e.u + r0);
+      if (has_x && e.xe != x) prefetch_l2(e.xe + r0);
+    }
+  }
+  if (live) {
+    const uint16_t* cp = reinterpret_cast<const uint16_t*>(code8 + base) + lane;
+    const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
+#pragma unroll 4
+    for (int k = k0; k < k1; ++k) {
+      const int cc = ld_stream(cp + 32 * k);
+      const double2 p0 = s_tab[cc & 0xff], p1 = s_tab[cc >> 8];
+      a0 = fma(p0.x, __ldg(x + min(r0i + pair_off(p0), nm1)), a0);
+      a1 = fma(p1.x, __ldg(x + min(r0i + 1 + pair_off(p1), nm1)), a1);
     }
   }
   if constexpr (KS > 1) {
@@ -698,9 +789,6 @@ __global__ void __launch_bounds__(256) combine_kernel(int64_t n, const T* __rest
 constexpr int F_UPD = 1, F_PROJ = 2, F_NRM = 4;
 constexpr int CGS_SMEM = 212 * 1024;  // dynamic shared memory per CTA (ring + barriers)
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -1163,13 +1251,21 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
       const int b2 = int((A->nslices + spb2 - 1) / spb2);
 #define PPF_S2E(K, E)                                                                         \
   launch_pdl(sell2_kernel<K, ACC, E>, b2, bt, st, A->nslices, A->n_local, A->d_ptr, A->d_col,   \
-             reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb,         \
-             A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab)
-#define PPF_S2(K) PPF_S2E(K, 0)
-#define PPF_S2D(K) PPF_S2E(K, 1)
-#define PPF_S2P(K) PPF_S2E(K, 2)
+             reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb)
+#define PPF_S2(K) PPF_S2E(K, false)
+#define PPF_S2D(K) PPF_S2E(K, true)
+#define PPF_SP(K)                                                                              \
+  launch_pdl(sellp_kernel<K, ACC>, bp, tp, st, A->nslices, A->n_local, A->d_ptr, A->d_code8,   \
+             A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x)
       if (A->d_code8) {
-        PPF_KS(PPF_S2P)
+        // 8-warp blocks (measured C4 / C3 deg 20: 4-, 8- and 16-warp blocks
+        // within 2%)
+        const int tp = 256;
+        const int64_t spbp = (tp / 32) / KS;
+        const int bp = int((A->nslices + spbp - 1) / spbp);
+        PPF_KS(PPF_SP)
+        post_launch("sellp_kernel");
+        return;
       } else if (A->d_d16) {
         PPF_KS(PPF_S2D)
       } else {
@@ -1177,7 +1273,7 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
       }
 #undef PPF_S2
 #undef PPF_S2D
-#undef PPF_S2P
+#undef PPF_SP
 #undef PPF_S2E
       post_launch("sell2_kernel");
       return;
