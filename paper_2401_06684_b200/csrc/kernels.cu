@@ -412,6 +412,9 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 //  * one aligned 16-B load of x[c], x[c + 1] where both rows take the same
 //    pair at an even column (5 of C4's 7 columns, fewer L1 sectors): the
 //    branch cost more than it saved, 160 -> 187 us;
+//  * x staged in shared memory over the block's rows +- one block height
+//    (coalesced 16-B loads after the PDL wait), the near pairs' gathers read
+//    there through a generic pointer: 161 -> 233 us;
 //  * all codes of 8 columns, then all gathers, then the FMAs (64 registers,
 //    half the warps): 195 us;
 //  * a persistent grid, each CTA walking a contiguous range of slices (L1
@@ -427,11 +430,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ __forceinline__ int pair_off(double2 p) { return int(__double_as_longlong(p.y)); }
 
-// XS (KS = 1 only): the block stages x over its rows +- one block height
-// into shared memory after the PDL wait (coalesced 16-B loads), and the
-// gathers of the pairs with |offset| <= that height read it there (a generic
-// pointer: shared or global per lane, no branch).
-template <int KS, bool ACC = false, bool XS = false>
+template <int KS, bool ACC = false>
 __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const uint8_t* __restrict__ code8,
@@ -441,7 +440,6 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
                                                     double* __restrict__ out, EpiT<double> e,
                                                     bool has_x) {
   __shared__ double2 s_tab[256];
-  __shared__ __align__(16) double xs[XS ? 3 * 64 * 8 : 2];
   pdl_release();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
@@ -472,38 +470,7 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
       if (has_x && e.xe != x) prefetch_l2(e.xe + r0);
     }
   }
-  if constexpr (XS) {
-    // x[R0 - H, R0 + 2H) with H = the block's rows (clamped to [0, n))
-    const int H = blockDim.x * 2;
-    const int64_t R0 = int64_t(blockIdx.x) * H;
-    for (int i = threadIdx.x; i < 3 * H / 2; i += blockDim.x) {
-      const int64_t r = R0 - H + 2 * i;
-      if (r >= 0 && r + 1 < n) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(x + r));
-        xs[2 * i] = v.x;
-        xs[2 * i + 1] = v.y;
-      } else if (r >= 0 && r < n) {
-        xs[2 * i] = x[r];
-      }
-    }
-    __syncthreads();
-    if (live) {
-      const uint16_t* cp = reinterpret_cast<const uint16_t*>(code8 + base) + lane;
-      const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
-      const int lo = int(R0) - H;            // global row of xs[0]
-#pragma unroll 4
-      for (int k = k0; k < k1; ++k) {
-        const int cc = ld_stream(cp + 32 * k);
-        const double2 p0 = s_tab[cc & 0xff], p1 = s_tab[cc >> 8];
-        const int o0 = pair_off(p0), o1 = pair_off(p1);
-        const int c0 = min(r0i + o0, nm1), c1 = min(r0i + 1 + o1, nm1);
-        const double* q0 = (o0 <= H && o0 >= -H) ? xs + (c0 - lo) : x + c0;
-        const double* q1 = (o1 <= H && o1 >= -H) ? xs + (c1 - lo) : x + c1;
-        a0 = fma(p0.x, *q0, a0);
-        a1 = fma(p1.x, *q1, a1);
-      }
-    }
-  } else if (live) {
+  if (live) {
     const uint16_t* cp = reinterpret_cast<const uint16_t*>(code8 + base) + lane;
     const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
 #pragma unroll 4
@@ -1293,18 +1260,6 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
 #define PPF_SP(K)                                                                              \
   launch_pdl(sellp_kernel<K, ACC>, bp, tp, st, A->nslices, A->n_local, A->d_ptr, A->d_code8,   \
              A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x)
-      static const bool xs_env = [] {
-        const char* v = std::getenv("PPF_SELLP_XS");
-        return v && v[0] == '1';
-      }();
-      if (A->d_code8 && xs_env && KS == 1) {
-        const int tp = 256;
-        const int bp = int((A->nslices + 7) / 8);
-        launch_pdl(sellp_kernel<1, ACC, true>, bp, tp, st, A->nslices, A->n_local, A->d_ptr,
-                   A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x);
-        post_launch("sellp_kernel");
-        return;
-      }
       if (A->d_code8) {
         // 8-warp blocks (measured C4 / C3 deg 20: 4-, 8- and 16-warp blocks
         // within 2%)
