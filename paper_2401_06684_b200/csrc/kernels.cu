@@ -411,7 +411,8 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 //    fewer L1 wavefronts): L1 hit rate 49 -> 24%, 155 -> 168 us;
 //  * one aligned 16-B load of x[c], x[c + 1] where both rows take the same
 //    pair at an even column (5 of C4's 7 columns, fewer L1 sectors): the
-//    branch cost more than it saved, 160 -> 187 us;
+//    branch cost more than it saved, 160 -> 187 us (and 179 us with
+//    diagonal-aligned slots, where the branch never diverges);
 //  * x staged in shared memory over the block's rows +- one block height
 //    (coalesced 16-B loads after the PDL wait), the near pairs' gathers read
 //    there through a generic pointer: 161 -> 233 us;
