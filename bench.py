@@ -633,10 +633,13 @@ def main():
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "fused SELL SpMV + Clenshaw/Newton epilogue (spmv class)",
                      "peak_source": peak_src,
-                     "peak_note": "hbm_gbs is a 1:1 read/write copy (torch b.copy_(a)); the SpMV stream is "
-                                  "~92% reads, which the HBM sustains slightly faster, so frac can reach 1.0; "
-                                  "ncu puts the C4 SpMV at 83% of the DRAM's theoretical peak "
-                                  "(profiles/ncu_summary.json)",
+                     "peak_note": ("hbm_gbs is a 1:1 read/write copy (torch b.copy_(a)); the SpMV stream is "
+                                   "~92% reads, which the HBM sustains slightly faster, so frac can reach 1.0 "
+                                   "(the 16-bit-delta C4 SpMV: 0.96, ncu 83% of the DRAM's theoretical peak)" +
+                                   ("; with pair codes (1 B per entry) the SpMV moves 2.6x fewer bytes and is "
+                                    "bound by its x gathers (L1 data pipe), not DRAM: ncu 51% of DRAM peak, "
+                                    "1.018x algorithmic traffic (profiles/ncu_summary.json, DESIGN.md section 5)"
+                                    if encoding == "pair8" else "")),
                      "bytes_per_unit": ("per SpMV launch: e per nonzero + s per row for x, out and "
                                         "each epilogue vector (s = 8 or 16 bytes per scalar; e = s + 4 "
                                         "(explicit), s + 2 + 4/64 (16-bit column deltas) or 1 (pair "
