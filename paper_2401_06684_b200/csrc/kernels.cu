@@ -413,6 +413,8 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 //    pair at an even column (5 of C4's 7 columns, fewer L1 sectors): the
 //    branch cost more than it saved, 160 -> 187 us (and 179 us with
 //    diagonal-aligned slots, where the branch never diverges);
+//  * two slices per warp (twice the independent loads per loop turn, 40
+//    registers): 161 -> 195 us;
 //  * x staged in shared memory over the block's rows +- one block height
 //    (coalesced 16-B loads after the PDL wait), the near pairs' gathers read
 //    there through a generic pointer: 161 -> 233 us;
