@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(cgs_consumers<T>() + 32, 1)
   constexpr int NCL = NC / 2;                  // columns per lane (c = 2 cc + h)
   constexpr bool UPD = FL & F_UPD, PROJ = FL & F_PROJ, NRM = FL & F_NRM;
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ T cin[NC];
+  __shared__ __align__(16) T cin[NC];
   __shared__ double red[NW][NC * ND + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int S = cgs_stages<T>(nct);
@@ -912,8 +912,10 @@ __global__ void __launch_bounds__(cgs_consumers<T>() + 32, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // fp64: the coefficients of lane parity h (columns h, h + 2, ...) stored
+  // contiguously, read two at a time (16-B shared loads) by the update
   if (UPD)
-    for (int c = tid; c < nct; c += blockDim.x) cin[c] = coef_in[c];
+    for (int c = tid; c < nct; c += blockDim.x) cin[ND == 1 ? (c & 1) * (NC / 2) + (c >> 1) : c] = coef_in[c];
   __syncthreads();
 
   T acc[NCL];
@@ -957,7 +959,7 @@ __global__ void __launch_bounds__(cgs_consumers<T>() + 32, 1)
     const uint32_t ring_u = smem_u32(ring);
     const uint32_t colb = uint32_t(CS * sizeof(T));  // bytes between column segments
     const int ncl_h = (nct - h + 1) >> 1;             // this lane's columns c = 2 cc + h < nct
-    const uint32_t cin_u = smem_u32(cin) + uint32_t(h * sizeof(T));
+    const uint32_t cin_u = smem_u32(cin) + uint32_t(h * sizeof(T) * (ND == 1 ? NC / 2 : 1));
     // the warp releases the stage (its "empty" arrival) as soon as it has
     // read the last row block's operands into registers, before that block's
     // arithmetic: the producer can refill the stage while the FMA chains run
@@ -987,14 +989,27 @@ __global__ void __launch_bounds__(cgs_consumers<T>() + 32, 1)
         if (UPD) {
           // two interleaved partial sums per lane, then the pair's halves
           T s0 = s_zero<T>(), s1 = s_zero<T>();
+          if constexpr (ND == 1) {
 #pragma unroll
-          for (int cc = 0; cc < NCL; ++cc) {
-            if (COLCHK && cc >= ncl_h) continue;
-            const T cf = lds_s<T>(cin_u + uint32_t(2 * cc * sizeof(T)));
-            if (cc & 1)
-              s1 = s_fma(tv[cc], cf, s1);
-            else
-              s0 = s_fma(tv[cc], cf, s0);
+            for (int cc = 0; cc < NCL; cc += 2) {
+              if (COLCHK && cc >= ncl_h) continue;
+              double c0, c1;
+              asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                           : "=d"(c0), "=d"(c1)
+                           : "r"(cin_u + uint32_t(cc * sizeof(T))));
+              s0 = s_fma(tv[cc], c0, s0);
+              if (cc + 1 < NCL && !(COLCHK && cc + 1 >= ncl_h)) s1 = s_fma(tv[cc + 1], c1, s1);
+            }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < NCL; ++cc) {
+              if (COLCHK && cc >= ncl_h) continue;
+              const T cf = lds_s<T>(cin_u + uint32_t(2 * cc * sizeof(T)));
+              if (cc & 1)
+                s1 = s_fma(tv[cc], cf, s1);
+              else
+                s0 = s_fma(tv[cc], cf, s0);
+            }
           }
           T sum = s_add(s0, s1);
           if constexpr (ND == 1) {
