@@ -415,6 +415,10 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 //    diagonal-aligned slots, where the branch never diverges);
 //  * two slices per warp (twice the independent loads per loop turn, 40
 //    registers): 161 -> 195 us;
+//  * a window-staged persistent kernel (producer warp bulk-copying codes,
+//    z, u and x as three contiguous windows per 1024-row stage into a 4-deep
+//    mbarrier ring, 16 consumer warps working from shared memory): 203 us,
+//    consumers waiting on the ring (DRAM 36%);
 //  * x staged in shared memory over the block's rows +- one block height
 //    (coalesced 16-B loads after the PDL wait), the near pairs' gathers read
 //    there through a generic pointer: 161 -> 233 us;
