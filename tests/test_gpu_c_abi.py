@@ -130,9 +130,42 @@ int main(int argc, char** argv) {
   /* a float64 vector starting 8 bytes into an allocation: rejected */
   int mis = ppf_run(ctx, A, q, &o, db, (char*)dx + 8, work, wbytes, &rep_h);
 
+  /* the same operator as SELL-64: the plan stores pair codes (PPF_ENC_PAIR8);
+     its SpMV does the SELL-32 kernel's multiply-adds in the same order */
+  ppf_plan* plan64 = NULL;
+  CK(ppf_plan_create(PPF_R64, n, 1, 0, bounds, row_ptr, col, val, PPF_FMT_SELL, 64, 1, &plan64));
+  int enc = -1, ntab = -1, ibits = 0;
+  CK(ppf_plan_encoding(plan64, &enc, &ntab));
+  CK(ppf_plan_index_bits(plan64, &ibits));
+  size_t mbytes64 = 0;
+  CK(ppf_plan_device_bytes(plan64, &mbytes64));
+  void* mbuf64 = NULL;
+  CU(cudaMalloc(&mbuf64, mbytes64));
+  ppf_mat* A64 = NULL;
+  CK(ppf_mat_create(ctx, plan64, mbuf64, mbytes64, &A64));
+  ppf_plan_destroy(plan64);
+  void *y32 = NULL, *y64 = NULL;
+  CU(cudaMalloc(&y32, (size_t)n * 8));
+  CU(cudaMalloc(&y64, (size_t)n * 8));
+  CK(ppf_spmv(ctx, A, db, y32));
+  CK(ppf_spmv(ctx, A64, db, y64));
+  CU(cudaDeviceSynchronize());
+  double* h32 = (double*)malloc((size_t)n * 8);
+  double* h64 = (double*)malloc((size_t)n * 8);
+  CU(cudaMemcpy(h32, y32, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(h64, y64, (size_t)n * 8, cudaMemcpyDeviceToHost));
+  int spmv_equal = 1;
+  for (int64_t i = 0; i < n; ++i) spmv_equal &= (h32[i] == h64[i]);
+  if (spit(dir, "y_pair.bin", h64, (size_t)n * 8)) return 6;
+  ppf_mat_destroy(A64);
+  cudaFree(y32); cudaFree(y64); cudaFree(mbuf64);
+  free(h32); free(h64);
+
   printf("m=%d term=%d mvms=%lld launches=%lld beta0=%.17g min_q=%.17g hist=%d "
-         "sec_dev=%.9g sec_total=%.9g misaligned=%d\n", rep.iterations, rep.term, rep.mvms,
-         rep.kernel_launches, beta0, min_q, cnt, rep.seconds_device, rep.seconds_total, mis);
+         "sec_dev=%.9g sec_total=%.9g misaligned=%d enc=%d ntab=%d ibits=%d spmv_equal=%d "
+         "mbytes64=%zu\n", rep.iterations, rep.term, rep.mvms,
+         rep.kernel_launches, beta0, min_q, cnt, rep.seconds_device, rep.seconds_total, mis, enc,
+         ntab, ibits, spmv_equal, mbytes64);
   ppf_poly_destroy(q);
   ppf_mat_destroy(A);
   ppf_ctx_destroy(ctx);
@@ -183,3 +216,11 @@ def test_c99_program_runs_c1_on_device(tmp_path):
     assert int(rep["launches"]) > 0
     assert 0.0 < float(rep["sec_dev"]) <= float(rep["sec_total"]) * 1.05
     assert int(rep["misaligned"]) == 1           # PPF_EINVAL
+    # pair codes from C: PPF_ENC_PAIR8 with the 5-point stencil's 5 pairs + padding, 8-bit
+    # codes, the SpMV equal to the SELL-32 one and to SciPy's within fp64 rounding
+    assert int(rep["enc"]) == 2 and int(rep["ibits"]) == 8 and 5 < int(rep["ntab"]) <= 11
+    assert int(rep["spmv_equal"]) == 1
+    assert int(rep["mbytes64"]) < 2 * A.nnz + 16 * 1024
+    y = np.fromfile(tmp_path / "y_pair.bin")
+    yr = A.to_scipy() @ b
+    assert np.all(np.abs(y - yr) <= 1e-14 * (abs(A.to_scipy()) @ np.abs(b)))
