@@ -87,6 +87,9 @@ def parse():
     p.add_argument("--no-profile", action="store_true",
                    help="time without the per-kernel CUDA events (no roofline breakdown)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-alt-layout", action="store_true",
+                   help="skip the second measurement on the 16-bit-delta layout that a pair-code "
+                        "run adds (same steps, the layout that streams the explicit values)")
     p.add_argument("--no-graphs", action="store_true",
                    help="launch the step's q(A)q(A) chain directly instead of replaying a CUDA graph")
     p.add_argument("--comm", default="peer", choices=["peer", "nccl"],
@@ -604,6 +607,38 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
 
+    # With pair codes, the same K steps once more on the 16-bit-delta layout:
+    # the time and roofline of the layout that streams explicit values, so the
+    # line shows both the byte saving and the kernel's bandwidth when it is
+    # DRAM-bound.  Not part of the headline.
+    alt = None
+    if encoding == "pair8" and world == 1 and not args.no_alt_layout:
+        plan2 = pp.Plan.from_csr(A, fmt=fmt[0], C_=fmt[1], sigma=sigma).set_encoding("delta16")
+        M_main, work_main = M, work
+        M = pp.Matrix(ctx, plan2)
+        plan2.close()
+        M.set_split(args.split)
+        work = pp.Workspace(ctx, M, q0, opts)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                one_step()
+        torch.cuda.synchronize()
+        ms_alt, reps_alt, _, _, _ = timed_region(False)
+        _, _, _, prof_alt, _ = timed_region(True)
+        sp_alt = prof_alt["spmv"]
+        ach_alt = ((sp_alt["bytes"] / sp_alt["launches"]) / (sp_alt["ms"] / sp_alt["launches"] * 1e-3)
+                   / 1e9 if sp_alt["ms"] else None)
+        pk, _ = measured_peaks()
+        alt = {"encoding": "delta16", "value": ms_alt / 1e3, "unit": "s",
+               "m": reps_alt[-1].iterations, "spmv_ms_per_step": sp_alt["ms"] / args.steps,
+               "roofline_achieved_gbs": ach_alt, "roofline_frac": (ach_alt / pk) if ach_alt else None,
+               "spmv_bytes_per_step": sp_alt["bytes"] / args.steps,
+               "note": "same workload and steps on the 16-bit-delta layout (10.06 B per entry); "
+                       "the headline uses the pair codes (1 B per entry)"}
+        del M, work
+        M, work = M_main, work_main
+        torch.cuda.synchronize()
+
     peak, peak_src = measured_peaks()
     sp = prof["spmv"]
     achieved = (sp["bytes"] / sp["launches"]) / (sp["ms"] / sp["launches"] * 1e-3) / 1e9 if sp["ms"] else None
@@ -611,7 +646,8 @@ def main():
     traffic = None
     try:
         summ = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        if summ.get("config") == name and summ.get("deg") == deg and world == 1:
+        if (summ.get("config") == name and summ.get("deg") == deg and world == 1
+                and summ.get("encoding", "delta16") == encoding):
             traffic = summ.get("dominant_kernel_dram_bytes_per_launch")
             traffic_note = summ.get("note")
         else:
@@ -653,6 +689,7 @@ def main():
                      "launches_timed": sp["launches"],
                      "share_of_device_time": sp["ms"] / tot_ms if tot_ms else None,
                      "traffic_note": traffic_note},
+        "alt_layout": alt,
         "breakdown_ms_per_step": {k: v["ms"] / args.steps for k, v in prof.items()},
         "breakdown_gbs": {k: (v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] else None)
                           for k, v in prof.items()},
