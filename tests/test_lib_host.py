@@ -304,6 +304,28 @@ def test_plan_halo_lists_two_slabs():
         assert p.info()["halo_total"] == N * N
 
 
+def test_pair_codes_per_slab():
+    """Each rank's plan codes its own diagonal block: the z-slabs of a 3D
+    convection-diffusion stencil both get pair codes (the off-slab neighbours
+    go to the halo block, so a slab may have fewer pairs than the whole
+    matrix), the device layout is ~1 byte per diagonal-block entry, and the
+    halo lists are those of the explicit layout."""
+    N = 12
+    A = ops.convdiff(N, 3, (10.0, 10.0, 10.0))
+    bounds = [0, 5 * N * N, N**3]
+    for rank in (0, 1):
+        lo, hi = bounds[rank], bounds[rank + 1]
+        rp = A.row_ptr[lo:hi + 1] - A.row_ptr[lo]
+        sl = slice(A.row_ptr[lo], A.row_ptr[hi])
+        p = Plan(rp, A.col[sl], A.val[sl], row_bounds=bounds, rank=rank, fmt="sell", C_=64)
+        enc, ntab = p.encoding()
+        assert enc == "pair8" and 7 <= ntab <= 13, (enc, ntab)
+        halo = p.halo_recv(1 - rank)
+        p.set_encoding("explicit")
+        assert np.array_equal(p.halo_recv(1 - rank), halo)
+        assert len(halo) == N * N
+
+
 def test_real_pair_form_same_polynomial():
     """ppf_poly_set_newton_eval("pairs") on a Newton q with conjugate-pair nodes
     (the Ritz values of the real, convection-dominated C8s operator): the
