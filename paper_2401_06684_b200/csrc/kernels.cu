@@ -404,7 +404,8 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 // With 1 byte per entry the matrix is ~18% of the DRAM bytes (C4: 117 of the
 // 654 MB per chain SpMV) and DRAM is no longer the bound: at 155-160 us per
 // C4 SpMV (4.1 TB/s of DRAM traffic, 1.02x the algorithmic bytes) the L1
-// data pipe is 57% busy (a fifth of it the table lookups), DRAM 51%, and
+// data pipe is 76% busy (the x gathers; a fifth of it the table lookups),
+// DRAM 51%, and
 // long-scoreboard stalls on the x gathers dominate.  Measured on C4 (ncu, per
 // SpMV) and dropped:
 //  * rows i and i + 32 per lane (every warp access 32 consecutive rows,
