@@ -50,7 +50,13 @@ def ctx():
 def _matrix(ctx, cfg, A, cplx):
     fmt, sigma = bench.default_layout(cfg, A.n, cplx)
     C_ = 64 if fmt == "sell64" else 32
-    return pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=C_, sigma=sigma))
+    plan = pp.Plan.from_csr(A, fmt="sell", C_=C_, sigma=sigma)
+    enc = plan.encoding()
+    print(f"[layout] {fmt} sigma {sigma}: {enc[0]} ({enc[1]} pairs)")
+    if fmt == "sell64" and cfg.family in ("laplacian", "convdiff"):
+        # the bench layout of C3/C4: full-size parity runs through the pair codes
+        assert enc[0] == "pair8"
+    return pp.Matrix(ctx, plan)
 
 
 def _sampled_spmv(ctx, A, M, rng, nsample=4096):
