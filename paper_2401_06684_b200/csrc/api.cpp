@@ -688,6 +688,10 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     m->d_tab_off = reinterpret_cast<const int32_t*>(b + L.cb);
     m->d_tab_val = reinterpret_cast<const double*>(b + L.val);
     m->ntab = int(p->diag.tab_off.size());
+    for (int i = 0; i < m->ntab && i < 32; ++i) {
+      m->h_tab_val[i] = p->diag.tab_val[size_t(i)];
+      m->h_tab_off[i] = p->diag.tab_off[size_t(i)];
+    }
   } else {
     if (p->enc == PPF_ENC_EXPLICIT) {
       m->d_col = reinterpret_cast<const int32_t*>(b + L.col);

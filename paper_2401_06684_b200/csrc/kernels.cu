@@ -428,8 +428,12 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 //  * a persistent grid, each CTA walking a contiguous range of slices (L1
 //    reuse of the +-1 / +-N neighbours): the far (+-N^2) neighbours' reuse
 //    distance across CTAs outgrew L2 -- DRAM reads 0.52 -> 0.96 GB, 227 us.
-// The table is held as (value, offset bits) pairs: one 16-B shared load per
-// lookup, a broadcast where a column's codes agree.  KS warps per slice as in
+// A table of at most 32 pairs (C3/C4: 8) is passed by value as a
+// __grid_constant__ kernel parameter, so the lookups are indexed constant-
+// cache loads off the L1 data pipe (C4 186.2 -> 177.8 ms, C3 deg 20 97.9 ->
+// 93.8 ms); larger tables are held in shared memory as (value, offset bits)
+// pairs: one 16-B load per lookup, a broadcast where a column's codes agree.
+// PPF_SELLP_CTAB=0 forces the shared-memory table.  KS warps per slice as in
 // sell2_kernel.  The multiply-adds are the explicit layout's, in its order
 // (bitwise-identical results).
 // ---------------------------------------------------------------------------
@@ -438,7 +442,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ __forceinline__ int pair_off(double2 p) { return int(__double_as_longlong(p.y)); }
 
-template <int KS, bool ACC = false>
+struct PairTab32 {
+  double v[32];
+  int o[32];
+};
+
+// CT: the table (<= 32 pairs) comes by value as a kernel parameter, so the
+// lookups are constant-cache loads (uniform across the warp where a column's
+// codes agree) instead of shared-memory loads on the L1 data pipe
+template <int KS, bool ACC = false, bool CT = false>
 __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const uint8_t* __restrict__ code8,
@@ -446,8 +458,8 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
                                                     const double* __restrict__ tab_val, int ntab,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ out, EpiT<double> e,
-                                                    bool has_x) {
-  __shared__ double2 s_tab[256];
+                                                    bool has_x, const __grid_constant__ PairTab32 ct) {
+  __shared__ double2 s_tab[CT ? 1 : 256];
   pdl_release();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
@@ -464,9 +476,11 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
     // the slice's codes (64 B per column) into L2 before the PDL wait
     for (int o = 128 * lane; o < 64 * (k1 - k0); o += 32 * 128) prefetch_l2(code8 + base + 64 * k0 + o);
   }
-  for (int i = threadIdx.x; i < ntab; i += blockDim.x)
-    s_tab[i] = make_double2(__ldg(tab_val + i), __longlong_as_double((long long)__ldg(tab_off + i)));
-  __syncthreads();
+  if constexpr (!CT) {
+    for (int i = threadIdx.x; i < ntab; i += blockDim.x)
+      s_tab[i] = make_double2(__ldg(tab_val + i), __longlong_as_double((long long)__ldg(tab_off + i)));
+    __syncthreads();
+  }
   pdl_wait();
   // the slice's rows of the epilogue vectors and of x: one line per 8 lanes
   if (live && part == 0 && (lane & 7) == 0) {
@@ -484,9 +498,15 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
 #pragma unroll 4
     for (int k = k0; k < k1; ++k) {
       const int cc = ld_stream(cp + 32 * k);
-      const double2 p0 = s_tab[cc & 0xff], p1 = s_tab[cc >> 8];
-      a0 = fma(p0.x, __ldg(x + min(r0i + pair_off(p0), nm1)), a0);
-      a1 = fma(p1.x, __ldg(x + min(r0i + 1 + pair_off(p1), nm1)), a1);
+      if constexpr (CT) {
+        const int e0 = cc & 0xff, e1 = cc >> 8;
+        a0 = fma(ct.v[e0], __ldg(x + min(r0i + ct.o[e0], nm1)), a0);
+        a1 = fma(ct.v[e1], __ldg(x + min(r0i + 1 + ct.o[e1], nm1)), a1);
+      } else {
+        const double2 p0 = s_tab[cc & 0xff], p1 = s_tab[cc >> 8];
+        a0 = fma(p0.x, __ldg(x + min(r0i + pair_off(p0), nm1)), a0);
+        a1 = fma(p1.x, __ldg(x + min(r0i + 1 + pair_off(p1), nm1)), a1);
+      }
     }
   }
   if constexpr (KS > 1) {
@@ -1281,15 +1301,31 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
 #define PPF_S2(K) PPF_S2E(K, false)
 #define PPF_S2D(K) PPF_S2E(K, true)
 #define PPF_SP(K)                                                                              \
-  launch_pdl(sellp_kernel<K, ACC>, bp, tp, st, A->nslices, A->n_local, A->d_ptr, A->d_code8,   \
-             A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x)
+  launch_pdl(sellp_kernel<K, ACC, false>, bp, tp, st, A->nslices, A->n_local, A->d_ptr,        \
+             A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x, ct)
+#define PPF_SPC(K)                                                                             \
+  launch_pdl(sellp_kernel<K, ACC, true>, bp, tp, st, A->nslices, A->n_local, A->d_ptr,         \
+             A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x, ct)
       if (A->d_code8) {
+        PairTab32 ct{};
+        const bool small = A->ntab <= 32;
+        if (small)
+          for (int i = 0; i < A->ntab; ++i) {
+            ct.v[i] = A->h_tab_val[i];
+            ct.o[i] = A->h_tab_off[i];
+          }
+        const char* ctv = std::getenv("PPF_SELLP_CTAB");   // (read per launch: A/B in one process)
+        const bool use_ct = small && !(ctv && ctv[0] == '0');
         // 8-warp blocks (measured C4 / C3 deg 20: 4-, 8- and 16-warp blocks
         // within 2%)
         const int tp = 256;
         const int64_t spbp = (tp / 32) / KS;
         const int bp = int((A->nslices + spbp - 1) / spbp);
-        PPF_KS(PPF_SP)
+        if (use_ct) {
+          PPF_KS(PPF_SPC)
+        } else {
+          PPF_KS(PPF_SP)
+        }
         post_launch("sellp_kernel");
         return;
       } else if (A->d_d16) {
@@ -1300,6 +1336,7 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
 #undef PPF_S2
 #undef PPF_S2D
 #undef PPF_SP
+#undef PPF_SPC
 #undef PPF_S2E
       post_launch("sell2_kernel");
       return;

@@ -163,6 +163,10 @@ struct ppf_mat {
   const int32_t* d_tab_off = nullptr;
   const double* d_tab_val = nullptr;
   int ntab = 0;
+  // host copy of a small pair table (ntab <= 32): passed to sellp_kernel by
+  // value, so its lookups go through the constant cache, not the L1 data pipe
+  double h_tab_val[32] = {};
+  int h_tab_off[32] = {};
   int csr_group;            // lanes per row for the CSR kernel
   int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks
   int64_t sell_heavy = 0;   // leading slices given a whole block each (see sell_heavy_prefix)
