@@ -142,6 +142,49 @@ def test_pair_codes_bitwise(ctx, shape, ks):
     assert np.all(np.abs(outs["pair8"][0] - ref) <= 1e-14 * absA + 1e-300)
 
 
+@pytest.mark.parametrize("ctab", ["1", "0"])
+@pytest.mark.parametrize("nvals", [3, 10, 40])
+def test_pair_codes_table_sizes(ctx, nvals, ctab, monkeypatch):
+    """Pair tables beyond the 32 entries passed as a kernel parameter are
+    held in shared memory (and PPF_SELLP_CTAB=0 forces that path for small
+    ones): a banded matrix (offsets -3..3, ragged n = 5003) whose values are
+    drawn from `nvals` levels -- 7 * nvals pairs + padding: 22 (parameter
+    table), 71 (shared-memory table), 281 (over the 256-entry table: the
+    deltas) -- against the explicit layout (bitwise) and SciPy."""
+    monkeypatch.setenv("PPF_SELLP_CTAB", ctab)
+    n = 5003
+    rng = np.random.default_rng(nvals)
+    levels = rng.standard_normal(nvals)
+    offs = np.arange(-3, 4)
+    rows, cols = [], []
+    for o in offs:
+        r = np.arange(max(0, -o), min(n, n - o))
+        rows.append(r)
+        cols.append(r + o)
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    order = np.lexsort((cols, rows))
+    rows, cols = rows[order], cols[order]
+    vals = levels[rng.integers(0, nvals, len(rows))]
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    A = CSR(n, rp, cols.astype(np.int64), vals)
+    plan = pp.Plan.from_csr(A, fmt="sell", C_=64)
+    enc, ntab = plan.encoding()
+    assert (enc == "pair8") == (7 * nvals + 1 <= 256), (enc, ntab)
+    if enc == "pair8":
+        assert ntab == 7 * nvals + 1
+    x = rng.standard_normal(n)
+    M = pp.Matrix(ctx, plan)
+    yd = torch.full_like(dev(x), float("nan"))
+    M.spmv(dev(x), yd)
+    Me = pp.Matrix(ctx, pp.Plan.from_csr(A, fmt="sell", C_=64).set_encoding("explicit"))
+    ye = torch.full_like(dev(x), float("nan"))
+    Me.spmv(dev(x), ye)
+    assert np.array_equal(host(yd), host(ye))
+    ref = A.to_scipy() @ x
+    assert np.all(np.abs(host(yd) - ref) <= 1e-14 * (abs(A.to_scipy()) @ np.abs(x)))
+
+
 @pytest.mark.parametrize("ks", [1, 2, 4, 8])
 @pytest.mark.parametrize("C_", [32, 64])
 @pytest.mark.parametrize("which", ["ragged", "ragged_c", "wilson", "lap3"])
