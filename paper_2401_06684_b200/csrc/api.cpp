@@ -462,6 +462,18 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
         }
         return -1;
       };
+      // Lane-major chunks: slice s's codes start at pptr[s] (a multiple of
+      // 512) and come in chunks of 8 columns; in chunk c, the 16 bytes at
+      // 16 l hold column k = 8 c + j of rows 2l, 2l + 1 at bytes 2j, 2j + 1
+      // -- one 16-B load gives a lane all its codes of 8 columns.  pptr[s]
+      // carries the slice width w (< 512) in its low 9 bits.
+      std::vector<int64_t> pptr(B.nslices + 1, 0);
+      for (int64_t s = 0; s < B.nslices; ++s) {
+        const int64_t w = (B.ptr[s + 1] - B.ptr[s]) / C;
+        if (w >= 512) ok = false;
+        pptr[s + 1] = pptr[s] + 512 * ((w + 7) / 8);
+      }
+      if (ok) code.assign(size_t(pptr[B.nslices]), 0);
       for (int64_t s = 0; s < B.nslices && ok; ++s) {
         const int64_t w = (B.ptr[s + 1] - B.ptr[s]) / C;
         for (int64_t k = 0; k < w && ok; ++k) {
@@ -474,11 +486,14 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
               ok = false;
               break;
             }
-            code[idx] = uint8_t(c);
+            code[size_t(pptr[s] + 512 * (k / 8) + 16 * (lane / 2) + 2 * (k % 8) + (lane % 2))] =
+                uint8_t(c);
           }
         }
       }
       if (ok) {
+        for (int64_t s = 0; s < B.nslices; ++s) pptr[s] |= (B.ptr[s + 1] - B.ptr[s]) / C;
+        B.pptr.swap(pptr);
         B.code8.swap(code);
         B.tab_off.swap(toff);
         B.tab_val.swap(tval);
@@ -634,7 +649,8 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
   auto up = [&](size_t off, const void* src, size_t n) {
     if (n) PPF_CUDA(cudaMemcpyAsync(b + off, src, n, cudaMemcpyHostToDevice, st));
   };
-  up(L.ptr, p->diag.ptr.data(), p->diag.ptr.size() * 8);
+  // (pair codes: their own slice pointers, width in the low bits)
+  up(L.ptr, (p->enc == PPF_ENC_PAIR8 ? p->diag.pptr : p->diag.ptr).data(), p->diag.ptr.size() * 8);
   if (p->enc == PPF_ENC_PAIR8) {
     up(L.col, p->diag.code8.data(), p->diag.code8.size());
     up(L.cb, p->diag.tab_off.data(), p->diag.tab_off.size() * 4);

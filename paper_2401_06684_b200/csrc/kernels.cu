@@ -76,6 +76,13 @@ __device__ __forceinline__ int ld_stream(const uint16_t* p) {
   asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
   return int(r);
 }
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
@@ -395,11 +402,18 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 
 // ---------------------------------------------------------------------------
 // SELL-64 fp64 SpMV + fused epilogue on pair codes (PPF_ENC_PAIR8): entry
-// (s, k, t) is the pair (off, val) = table[code8[ptr[s] + 64 k + t]],
-// column = row + off.  Lane i of the slice's warp takes rows 64 s + 2i and
-// 64 s + 2i + 1 (one 16-bit load gives both codes of a column), as in
-// sell2_kernel: the two gathers of a column then fall on the same lines (the
-// second an L1 hit).
+// (s, k, t) is the pair (off, val) = table[code], column = row + off.  Lane
+// i of the slice's warp takes rows 64 s + 2i and 64 s + 2i + 1, as in
+// sell2_kernel (the two gathers of a column fall on the same lines, the
+// second an L1 hit); the codes are stored lane-major in chunks of 8 columns
+// (ppf_internal.h), so one 16-B load gives the lane its codes of 8 columns
+// and all their gathers issue back to back (pair_chunk<NK>, unrolled per
+// chunk width, no per-column branch) -- with __launch_bounds__(256, 8) at 32
+// registers and full occupancy.  Measured on C4 / C3 deg 20 (ms per solve):
+// column-major codes, one 16-bit load per column: 176.4 / 94.8; lane-major
+// chunks with a per-column branch: no batching; pair_chunk at 48 registers
+// (40 warps/SM): 168.6 / 89.5; at 64: 181.4 / 98.7; at 40: 160.2 / 84.3; at
+// 32 (64 warps/SM): 152.5 / 79.8.
 //
 // With 1 byte per entry the matrix is ~18% of the DRAM bytes (C4: 117 of the
 // 654 MB per chain SpMV) and DRAM is no longer the bound: at 155-160 us per
@@ -447,11 +461,37 @@ struct PairTab32 {
   int o[32];
 };
 
+// NK columns of one lane's chunk (codes in q: byte 2j + r = column j, row r):
+// all 2 NK gathers, then the FMAs in column order
+template <int NK, bool CT>
+__device__ __forceinline__ void pair_chunk(const uint4 q, const double* __restrict__ x, int r0i, int nm1,
+                                           const PairTab32& ct, const double2* s_tab, double& a0,
+                                           double& a1) {
+  const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+  double g0[NK], g1[NK];
+  int e0[NK], e1[NK];
+#pragma unroll
+  for (int j = 0; j < NK; ++j) {
+    const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
+    e0[j] = int(wd & 0xffu);
+    e1[j] = int((wd >> 8) & 0xffu);
+    const int o0 = CT ? ct.o[e0[j]] : pair_off(s_tab[e0[j]]);
+    const int o1 = CT ? ct.o[e1[j]] : pair_off(s_tab[e1[j]]);
+    g0[j] = __ldg(x + min(r0i + o0, nm1));
+    g1[j] = __ldg(x + min(r0i + 1 + o1, nm1));
+  }
+#pragma unroll
+  for (int j = 0; j < NK; ++j) {
+    a0 = fma(CT ? ct.v[e0[j]] : s_tab[e0[j]].x, g0[j], a0);
+    a1 = fma(CT ? ct.v[e1[j]] : s_tab[e1[j]].x, g1[j], a1);
+  }
+}
+
 // CT: the table (<= 32 pairs) comes by value as a kernel parameter, so the
 // lookups are constant-cache loads (uniform across the warp where a column's
 // codes agree) instead of shared-memory loads on the L1 data pipe
 template <int KS, bool ACC = false, bool CT = false>
-__global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
+__global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const uint8_t* __restrict__ code8,
                                                     const int32_t* __restrict__ tab_off,
@@ -469,12 +509,14 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
   int64_t base = 0;
   int k0 = 0, k1 = 0;
   if (live) {
-    base = sptr[slice];
-    const int w = int((sptr[slice + 1] - base) >> 6);
+    const int64_t pe = sptr[slice];   // chunk offset | slice width
+    base = pe & ~int64_t(511);
+    const int w = int(pe & 511);
     k0 = part * w / KS;
     k1 = (part + 1) * w / KS;
-    // the slice's codes (64 B per column) into L2 before the PDL wait
-    for (int o = 128 * lane; o < 64 * (k1 - k0); o += 32 * 128) prefetch_l2(code8 + base + 64 * k0 + o);
+    // the slice's code chunks (512 B per 8 columns) into L2 before the PDL wait
+    for (int o = 512 * (k0 / 8) + 128 * lane; o < 512 * ((k1 + 7) / 8); o += 32 * 128)
+      prefetch_l2(code8 + base + o);
   }
   if constexpr (!CT) {
     for (int i = threadIdx.x; i < ntab; i += blockDim.x)
@@ -492,20 +534,39 @@ __global__ void __launch_bounds__(256) sellp_kernel(int64_t nslices, int64_t n,
       if (has_x && e.xe != x) prefetch_l2(e.xe + r0);
     }
   }
-  if (live) {
-    const uint16_t* cp = reinterpret_cast<const uint16_t*>(code8 + base) + lane;
+  if (KS == 1 && live) {
+    // one 16-B load gives the lane its codes of up to 8 columns, then all
+    // their gathers issue back to back (pair_chunk<NK>: no per-column branch)
     const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
-#pragma unroll 4
-    for (int k = k0; k < k1; ++k) {
-      const int cc = ld_stream(cp + 32 * k);
-      if constexpr (CT) {
-        const int e0 = cc & 0xff, e1 = cc >> 8;
-        a0 = fma(ct.v[e0], __ldg(x + min(r0i + ct.o[e0], nm1)), a0);
-        a1 = fma(ct.v[e1], __ldg(x + min(r0i + 1 + ct.o[e1], nm1)), a1);
-      } else {
-        const double2 p0 = s_tab[cc & 0xff], p1 = s_tab[cc >> 8];
-        a0 = fma(p0.x, __ldg(x + min(r0i + pair_off(p0), nm1)), a0);
-        a1 = fma(p1.x, __ldg(x + min(r0i + 1 + pair_off(p1), nm1)), a1);
+    for (int c = 0; 8 * c < k1; ++c) {
+      const uint4 q = ld_stream_u4(code8 + base + 512 * c + 16 * lane);
+      const int nk = k1 - 8 * c < 8 ? k1 - 8 * c : 8;
+      switch (nk) {
+#define PPF_PC(NK) \
+  case NK: pair_chunk<NK, CT>(q, x, r0i, nm1, ct, s_tab, a0, a1); break;
+        PPF_PC(1) PPF_PC(2) PPF_PC(3) PPF_PC(4) PPF_PC(5) PPF_PC(6) PPF_PC(7) PPF_PC(8)
+#undef PPF_PC
+      }
+    }
+  } else if (live) {
+    const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
+    for (int c = k0 / 8; 8 * c < k1; ++c) {
+      const uint4 q = ld_stream_u4(code8 + base + 512 * c + 16 * lane);
+      const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = 8 * c + j;
+        if (k < k0 || k >= k1) continue;
+        const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
+        const int e0 = int(wd & 0xffu), e1 = int((wd >> 8) & 0xffu);
+        if constexpr (CT) {
+          a0 = fma(ct.v[e0], __ldg(x + min(r0i + ct.o[e0], nm1)), a0);
+          a1 = fma(ct.v[e1], __ldg(x + min(r0i + 1 + ct.o[e1], nm1)), a1);
+        } else {
+          const double2 p0 = s_tab[e0], p1 = s_tab[e1];
+          a0 = fma(p0.x, __ldg(x + min(r0i + pair_off(p0), nm1)), a0);
+          a1 = fma(p1.x, __ldg(x + min(r0i + 1 + pair_off(p1), nm1)), a1);
+        }
       }
     }
   }

@@ -107,10 +107,12 @@ struct HostBlock {
   std::vector<int32_t> cb;
   // SELL-64 fp64 (no sorting) with dictionary-coded entries (round 2, "pair
   // codes"): entry (s, k, t) of row r = C s + t is the pair
-  // (tab_off[c], tab_val[c]) with c = code8[ptr[s] + C k + t]: column
+  // (tab_off[c], tab_val[c]) with c = code8[(pptr[s] & ~511) + 512 (k / 8) +
+  // 16 (t / 2) + 2 (k mod 8) + t mod 2] (lane-major chunks of 8 columns): column
   // r + tab_off[c] (clamped to the last row for the padding pair (0, +0.0)),
   // value tab_val[c].  Empty unless the block's entries (padding included)
   // take <= 256 distinct (col - row, value bits) pairs.
+  std::vector<int64_t> pptr;   // pair codes' slice pointers (multiples of 512) | slice width
   std::vector<uint8_t> code8;
   std::vector<int32_t> tab_off;
   std::vector<double> tab_val;
