@@ -413,7 +413,8 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 // column-major codes, one 16-bit load per column: 176.4 / 94.8; lane-major
 // chunks with a per-column branch: no batching; pair_chunk at 48 registers
 // (40 warps/SM): 168.6 / 89.5; at 64: 181.4 / 98.7; at 40: 160.2 / 84.3; at
-// 32 (64 warps/SM): 152.5 / 79.8.
+// 32 (64 warps/SM): 152.5 / 79.8; with the first code chunk loaded before
+// the PDL wait: 155.5 / 84.0 (dropped).
 //
 // With 1 byte per entry the matrix is ~18% of the DRAM bytes (C4: 117 of the
 // 654 MB per chain SpMV) and DRAM is no longer the bound: at 155-160 us per
