@@ -414,7 +414,9 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 // chunks with a per-column branch: no batching; pair_chunk at 48 registers
 // (40 warps/SM): 168.6 / 89.5; at 64: 181.4 / 98.7; at 40: 160.2 / 84.3; at
 // 32 (64 warps/SM): 152.5 / 79.8; with the first code chunk loaded before
-// the PDL wait: 155.5 / 84.0 (dropped).
+// the PDL wait: 155.5 / 84.0 (dropped); with rows i, i + 32 per lane in the
+// chunked layout (half the L1 wavefronts per gather): 152.7 / SpMV unchanged
+// (dropped).
 //
 // With 1 byte per entry the matrix is ~18% of the DRAM bytes (C4: 117 of the
 // 654 MB per chain SpMV) and DRAM is no longer the bound: at 155-160 us per
