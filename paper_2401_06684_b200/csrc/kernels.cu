@@ -459,34 +459,48 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 __device__ __forceinline__ int pair_off(double2 p) { return int(__double_as_longlong(p.y)); }
 
+// one 16-B record per pair: the value, and the column offset in bytes
+// (8 * (col - row)), so a lookup is two constant loads at one scaled index
+struct PairRec {
+  double v;
+  int o8;
+  int pad;
+};
 struct PairTab32 {
-  double v[32];
-  int o[32];
+  PairRec p[32];
 };
 
 // NK columns of one lane's chunk (codes in q: byte 2j + r = column j, row r):
-// all 2 NK gathers, then the FMAs in column order
-template <int NK, bool CT>
+// all 2 NK gathers, then the FMAs in column order.  TAIL (the last slice):
+// columns clamped to n - 1 for the padding pairs of lanes past n; elsewhere
+// the gather address is the row's x address plus the pair's byte offset.
+template <int NK, bool CT, bool TAIL>
 __device__ __forceinline__ void pair_chunk(const uint4 q, const double* __restrict__ x, int r0i, int nm1,
                                            const PairTab32& ct, const double2* s_tab, double& a0,
                                            double& a1) {
   const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
   double g0[NK], g1[NK];
   int e0[NK], e1[NK];
+  const char* xr = reinterpret_cast<const char*>(x + r0i);
 #pragma unroll
   for (int j = 0; j < NK; ++j) {
     const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
     e0[j] = int(wd & 0xffu);
     e1[j] = int((wd >> 8) & 0xffu);
-    const int o0 = CT ? ct.o[e0[j]] : pair_off(s_tab[e0[j]]);
-    const int o1 = CT ? ct.o[e1[j]] : pair_off(s_tab[e1[j]]);
-    g0[j] = __ldg(x + min(r0i + o0, nm1));
-    g1[j] = __ldg(x + min(r0i + 1 + o1, nm1));
+    if constexpr (CT && !TAIL) {
+      g0[j] = __ldg(reinterpret_cast<const double*>(xr + ct.p[e0[j]].o8));
+      g1[j] = __ldg(reinterpret_cast<const double*>(xr + 8 + ct.p[e1[j]].o8));
+    } else {
+      const int o0 = CT ? ct.p[e0[j]].o8 / 8 : pair_off(s_tab[e0[j]]);
+      const int o1 = CT ? ct.p[e1[j]].o8 / 8 : pair_off(s_tab[e1[j]]);
+      g0[j] = __ldg(x + min(r0i + o0, nm1));
+      g1[j] = __ldg(x + min(r0i + 1 + o1, nm1));
+    }
   }
 #pragma unroll
   for (int j = 0; j < NK; ++j) {
-    a0 = fma(CT ? ct.v[e0[j]] : s_tab[e0[j]].x, g0[j], a0);
-    a1 = fma(CT ? ct.v[e1[j]] : s_tab[e1[j]].x, g1[j], a1);
+    a0 = fma(CT ? ct.p[e0[j]].v : s_tab[e0[j]].x, g0[j], a0);
+    a1 = fma(CT ? ct.p[e1[j]].v : s_tab[e1[j]].x, g1[j], a1);
   }
 }
 
@@ -541,12 +555,16 @@ __global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t 
     // one 16-B load gives the lane its codes of up to 8 columns, then all
     // their gathers issue back to back (pair_chunk<NK>: no per-column branch)
     const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
+    const bool tail = slice * 64 + 64 > n;   // warp-uniform
     for (int c = 0; 8 * c < k1; ++c) {
       const uint4 q = ld_stream_u4(code8 + base + 512 * c + 16 * lane);
       const int nk = k1 - 8 * c < 8 ? k1 - 8 * c : 8;
       switch (nk) {
-#define PPF_PC(NK) \
-  case NK: pair_chunk<NK, CT>(q, x, r0i, nm1, ct, s_tab, a0, a1); break;
+#define PPF_PC(NK)                                                             \
+  case NK:                                                                     \
+    if (tail) pair_chunk<NK, CT, true>(q, x, r0i, nm1, ct, s_tab, a0, a1);     \
+    else pair_chunk<NK, CT, false>(q, x, r0i, nm1, ct, s_tab, a0, a1);         \
+    break;
         PPF_PC(1) PPF_PC(2) PPF_PC(3) PPF_PC(4) PPF_PC(5) PPF_PC(6) PPF_PC(7) PPF_PC(8)
 #undef PPF_PC
       }
@@ -563,8 +581,8 @@ __global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t 
         const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
         const int e0 = int(wd & 0xffu), e1 = int((wd >> 8) & 0xffu);
         if constexpr (CT) {
-          a0 = fma(ct.v[e0], __ldg(x + min(r0i + ct.o[e0], nm1)), a0);
-          a1 = fma(ct.v[e1], __ldg(x + min(r0i + 1 + ct.o[e1], nm1)), a1);
+          a0 = fma(ct.p[e0].v, __ldg(x + min(r0i + ct.p[e0].o8 / 8, nm1)), a0);
+          a1 = fma(ct.p[e1].v, __ldg(x + min(r0i + 1 + ct.p[e1].o8 / 8, nm1)), a1);
         } else {
           const double2 p0 = s_tab[e0], p1 = s_tab[e1];
           a0 = fma(p0.x, __ldg(x + min(r0i + pair_off(p0), nm1)), a0);
@@ -1372,11 +1390,14 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
              A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x, ct)
       if (A->d_code8) {
         PairTab32 ct{};
-        const bool small = A->ntab <= 32;
+        // (offsets kept as byte offsets in int32: |col - row| < 2^28)
+        bool small = A->ntab <= 32;
+        for (int i = 0; small && i < A->ntab; ++i)
+          small = A->h_tab_off[i] > -(1 << 28) && A->h_tab_off[i] < (1 << 28);
         if (small)
           for (int i = 0; i < A->ntab; ++i) {
-            ct.v[i] = A->h_tab_val[i];
-            ct.o[i] = A->h_tab_off[i];
+            ct.p[i].v = A->h_tab_val[i];
+            ct.p[i].o8 = 8 * A->h_tab_off[i];
           }
         const char* ctv = std::getenv("PPF_SELLP_CTAB");   // (read per launch: A/B in one process)
         const bool use_ct = small && !(ctv && ctv[0] == '0');
