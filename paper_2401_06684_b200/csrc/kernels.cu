@@ -413,7 +413,9 @@ __global__ void __launch_bounds__(256) sell2_kernel(int64_t nslices, int64_t n,
 // column-major codes, one 16-bit load per column: 176.4 / 94.8; lane-major
 // chunks with a per-column branch: no batching; pair_chunk at 48 registers
 // (40 warps/SM): 168.6 / 89.5; at 64: 181.4 / 98.7; at 40: 160.2 / 84.3; at
-// 32 (64 warps/SM): 152.5 / 79.8; with the first code chunk loaded before
+// 32 (64 warps/SM): 152.5 / 79.8; pair records (value, byte offset) and no
+// column clamp outside the last slice: 144.0 / 77.1.  With the first code
+// chunk loaded before
 // the PDL wait: 155.5 / 84.0 (dropped); with rows i, i + 32 per lane in the
 // chunked layout (half the L1 wavefronts per gather): 152.7 / SpMV unchanged
 // (dropped).
