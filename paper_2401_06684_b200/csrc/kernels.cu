@@ -639,203 +639,6 @@ __global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t 
 }
 
 // ---------------------------------------------------------------------------
-// Two consecutive chain SpMVs in one persistent launch (pair codes, KS = 1):
-//   step 1: out1 = epi1(A x1),   step 2: out2 = epi2(A out1)
-// -- two Clenshaw steps b_i, b_{i-1} -- swept as a wavefront through
-// L2.  Work items are blocks of P2_ROWS rows in either step, handed out in a
-// fixed order by an atomic counter: step-1 items in row order, and step 2 of
-// block b right after step 1 of block b + K - 1, where K - 1 >= H, H = the
-// operator's half bandwidth in blocks (max |col - row| of the pair table).  A
-// step-2 item waits (acquire) for the completion flags of step-1 blocks
-// b - H .. b + H, set (release) by the CTA that finished them.  Every item a
-// CTA waits on was handed out earlier to a running CTA that never waits on a
-// later one, so the order is deadlock-free with any number of resident CTAs.
-// Step 2 then reads b_i, b_{i+1} and u while they are still in L2 (the
-// K-block window), so a pair streams five vectors from DRAM instead of eight.
-//
-// Loads of vectors written inside this launch (out1 in step 2; z1, the buffer
-// step 2 overwrites with out2) are plain weak ld.global after the acquire, not
-// the non-coherent path; the codes, x1 and u are read-only here.  Each row's
-// multiply-adds are sellp_kernel's in its order: results are bitwise those of
-// two sellp_kernel launches.  The sync words (item counter, exit counter,
-// epoch) and one flag per block live in the run workspace (zeroed once); the
-// last CTA to exit resets the counters and advances the epoch, so a captured
-// graph can replay the launch.
-// ---------------------------------------------------------------------------
-constexpr int P2_SLICES = 16;                 // slices (of 64 rows) per work item
-constexpr int P2_ROWS = 64 * P2_SLICES;
-
-__device__ __forceinline__ double ld_weak(const double* p) {
-  double r;
-  asm volatile("ld.global.f64 %0, [%1];" : "=d"(r) : "l"(p) : "memory");
-  return r;
-}
-__device__ __forceinline__ double2 ld_weak2(const double* p) {
-  double2 r;
-  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p) : "memory");
-  return r;
-}
-
-// pair_chunk with the gathers through the non-coherent (NC) or the weak path
-template <int NK, bool NC, bool TAIL>
-__device__ __forceinline__ void pair_chunk2(const uint4 q, const double* x, int r0i, int nm1,
-                                            const PairTab32& ct, double& a0, double& a1) {
-  const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
-  double g0[NK], g1[NK];
-  int e0[NK], e1[NK];
-  const char* xr = reinterpret_cast<const char*>(x + r0i);
-#pragma unroll
-  for (int j = 0; j < NK; ++j) {
-    const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
-    e0[j] = int(wd & 0xffu);
-    e1[j] = int((wd >> 8) & 0xffu);
-    const double* p0 = TAIL ? x + min(r0i + ct.p[e0[j]].o8 / 8, nm1)
-                            : reinterpret_cast<const double*>(xr + ct.p[e0[j]].o8);
-    const double* p1 = TAIL ? x + min(r0i + 1 + ct.p[e1[j]].o8 / 8, nm1)
-                            : reinterpret_cast<const double*>(xr + 8 + ct.p[e1[j]].o8);
-    if constexpr (NC) {
-      g0[j] = ld_gather(p0);
-      g1[j] = ld_gather(p1);
-    } else {
-      g0[j] = ld_weak(p0);
-      g1[j] = ld_weak(p1);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < NK; ++j) {
-    a0 = fma(ct.p[e0[j]].v, g0[j], a0);
-    a1 = fma(ct.p[e1[j]].v, g1[j], a1);
-  }
-}
-
-// one slice (64 rows; lane: rows 2 lane, 2 lane + 1) of one step
-template <bool NC>
-__device__ __forceinline__ void sellp_slice(int64_t slice, int64_t n, const int64_t* __restrict__ sptr,
-                                            const uint8_t* __restrict__ code8, const PairTab32& ct,
-                                            const double* x, double* out, const EpiT<double>& e,
-                                            bool has_x, int lane) {
-  const int64_t pe = sptr[slice];
-  const int64_t base = pe & ~int64_t(511);
-  const int w = int(pe & 511);
-  const int r0i = int(slice * 64 + 2 * lane), nm1 = int(n - 1);
-  const bool tail = slice * 64 + 64 > n;   // warp-uniform
-  double a0 = 0.0, a1 = 0.0;
-  for (int c = 0; 8 * c < w; ++c) {
-    const uint4 q = ld_stream_u4(code8 + base + 512 * c + 16 * lane);
-    const int nk = w - 8 * c < 8 ? w - 8 * c : 8;
-    switch (nk) {
-#define PPF_PC2(NK)                                                    \
-  case NK:                                                             \
-    if (tail) pair_chunk2<NK, NC, true>(q, x, r0i, nm1, ct, a0, a1);   \
-    else pair_chunk2<NK, NC, false>(q, x, r0i, nm1, ct, a0, a1);       \
-    break;
-      PPF_PC2(1) PPF_PC2(2) PPF_PC2(3) PPF_PC2(4) PPF_PC2(5) PPF_PC2(6) PPF_PC2(7) PPF_PC2(8)
-#undef PPF_PC2
-    }
-  }
-  const int64_t r0 = slice * 64 + 2 * lane;
-  if (r0 + 1 < n) {
-    double2 r;
-    r.x = e.s_ax * a0;
-    r.y = e.s_ax * a1;
-    if (has_x) {
-      const double2 xv = ld_weak2(e.xe + r0);
-      r.x = fma(e.s_x, xv.x, r.x);
-      r.y = fma(e.s_x, xv.y, r.y);
-    }
-    if (e.z) {
-      const double2 zv = ld_weak2(e.z + r0);
-      r.x = fma(e.s_z, zv.x, r.x);
-      r.y = fma(e.s_z, zv.y, r.y);
-    }
-    if (e.u) {
-      const double2 uv = ld_weak2(e.u + r0);
-      r.x = fma(e.s_u, uv.x, r.x);
-      r.y = fma(e.s_u, uv.y, r.y);
-    }
-    *reinterpret_cast<double2*>(out + r0) = r;
-  } else if (r0 < n) {
-    // epilogue()'s order: s_ax Ax, + s_x xe, + s_z z, + s_u u
-    double r = e.s_ax * a0;
-    if (has_x) r = fma(e.s_x, ld_weak(e.xe + r0), r);
-    if (e.z) r = fma(e.s_z, ld_weak(e.z + r0), r);
-    if (e.u) r = fma(e.s_u, ld_weak(e.u + r0), r);
-    out[r0] = r;
-  }
-}
-
-__global__ void __launch_bounds__(256, 8) sellp_pair_kernel(
-    int64_t nslices, int64_t n, const int64_t* __restrict__ sptr, const uint8_t* __restrict__ code8,
-    const double* x1, double* out1, EpiT<double> e1, bool has_x1, double* out2, EpiT<double> e2,
-    bool has_x2, unsigned* sync_words, int nblk, int halo, int lead,
-    const __grid_constant__ PairTab32 ct) {
-  // sync_words: [0] item counter, [1] exit counter, [2] epoch - 1, then one flag per block
-  __shared__ int s_item;
-  unsigned* flag = sync_words + 4;
-  pdl_release();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  pdl_wait();
-  const unsigned epoch = *reinterpret_cast<volatile unsigned*>(sync_words + 2) + 1u;
-  const int K = lead < nblk ? lead : nblk;   // step-1 items ahead of the first step-2 item
-  const int R = nblk - K;
-  const int total = 2 * nblk;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = int(atomicAdd(sync_words, 1u));
-    __syncthreads();
-    const int it = s_item;
-    __syncthreads();
-    if (it >= total) break;
-    int step, blk;
-    if (it < K) {
-      step = 1;
-      blk = it;
-    } else if (it - K < 2 * R) {
-      const int j = it - K;
-      step = (j & 1) ? 1 : 2;
-      blk = (j & 1) ? K + (j >> 1) : (j >> 1);
-    } else {
-      step = 2;
-      blk = R + (it - K - 2 * R);
-    }
-    if (step == 2) {
-      const int lo = blk - halo < 0 ? 0 : blk - halo;
-      const int hi = blk + halo >= nblk ? nblk - 1 : blk + halo;
-      for (int b = lo + int(threadIdx.x); b <= hi; b += blockDim.x) {
-        unsigned v;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag + b) : "memory");
-        } while (v != epoch);
-      }
-      __threadfence();
-      __syncthreads();
-    }
-#pragma unroll 1
-    for (int s = 0; s < P2_SLICES / 8; ++s) {
-      const int64_t slice = int64_t(blk) * P2_SLICES + warp * (P2_SLICES / 8) + s;
-      if (slice >= nslices) break;
-      if (step == 1)
-        sellp_slice<true>(slice, n, sptr, code8, ct, x1, out1, e1, has_x1, lane);
-      else
-        sellp_slice<false>(slice, n, sptr, code8, ct, out1, out2, e2, has_x2, lane);
-    }
-    if (step == 1) {
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag + blk), "r"(epoch) : "memory");
-      }
-    }
-  }
-  if (threadIdx.x == 0 && atomicAdd(sync_words + 1, 1u) == gridDim.x - 1) {
-    // every CTA has left the loop: reset for the next (stream-ordered) launch
-    sync_words[0] = 0;
-    sync_words[1] = 0;
-    sync_words[2] = epoch;
-    __threadfence();
-  }
-}
-
-// ---------------------------------------------------------------------------
 // CSR SpMV + fused epilogue, G lanes per row.
 // ---------------------------------------------------------------------------
 template <typename T, int G, bool ACC = false>
@@ -1709,53 +1512,6 @@ void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_
     spmv_t<double>(A, x, out, e, st);
   else
     spmv_t<cplx>(A, x, out, e, st);
-}
-
-// Sync words for launch_spmv_pair (P2Sync + one flag per block of P2_ROWS rows)
-size_t spmv_pair_sync_bytes(int64_t n) { return 16 + 4 * size_t((n + P2_ROWS - 1) / P2_ROWS); }
-
-bool spmv_pair_ok(const ppf_mat* A) {
-  const char* env = std::getenv("PPF_PAIR2");   // (read per chain: A/B in one process)
-  if (!(env && env[0] == '1') || !A->d_code8 || A->dtype != PPF_R64 || A->C != 64 || A->sell_ks != 1 || A->d_perm ||
-      A->nranks != 1 || A->ntab > 32 || A->n_local < 2 * P2_ROWS)
-    return false;
-  for (int i = 0; i < A->ntab; ++i)
-    if (A->h_tab_off[i] <= -(1 << 28) || A->h_tab_off[i] >= (1 << 28)) return false;
-  return true;
-}
-
-// out1 = epi1(A x1), then out2 = epi2(A out1), in one launch (sellp_pair_kernel);
-// sync: spmv_pair_sync_bytes(n) bytes, zeroed before the first launch
-void launch_spmv_pair(ppf_mat* A, const void* x1, void* out1, const Epi& e1, void* out2, const Epi& e2,
-                      void* sync, cudaStream_t st) {
-  PairTab32 ct{};
-  int maxoff = 0;
-  for (int i = 0; i < A->ntab; ++i) {
-    ct.p[i].v = A->h_tab_val[i];
-    ct.p[i].o8 = 8 * A->h_tab_off[i];
-    maxoff = std::max(maxoff, std::abs(A->h_tab_off[i]));
-  }
-  const int nblk = int((A->n_local + P2_ROWS - 1) / P2_ROWS);
-  const int halo = (maxoff + P2_ROWS - 1) / P2_ROWS;
-  static int occ = 0;   // resident CTAs per SM (launch bounds: 8)
-  if (!occ) {
-    cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sellp_pair_kernel, 256, 0),
-               "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
-    if (occ < 1) occ = 1;
-  }
-  const int grid = std::min(2 * nblk, occ * A->ctx->num_sms);
-  // step-1 blocks handed out ahead of step 2: the half bandwidth plus a slack
-  // of about half the resident CTAs, so that a step-2 item rarely waits
-  const char* senv = std::getenv("PPF_PAIR2_SLACK");   // (tests and tuning)
-  const int slack_env = senv ? std::atoi(senv) : -1;
-  const int slack = slack_env >= 0 ? slack_env : grid / 2;
-  const int lead = halo + 1 + slack;
-  const EpiT<double> t1 = to_epi<double>(e1, x1), t2 = to_epi<double>(e2, out1);
-  const bool hx1 = e1.s_x[0] != 0.0, hx2 = e2.s_x[0] != 0.0;
-  launch_pdl(sellp_pair_kernel, grid, 256, st, A->nslices, A->n_local, A->d_ptr, A->d_code8,
-             static_cast<const double*>(x1), static_cast<double*>(out1), t1, hx1,
-             static_cast<double*>(out2), t2, hx2, static_cast<unsigned*>(sync), nblk, halo, lead, ct);
-  post_launch("sellp_pair_kernel");
 }
 
 void launch_acc(ppf_mat* A, const void* x, const void* out, const Epi& e, cudaStream_t st) {

@@ -303,11 +303,6 @@ void launch_spmv(ppf_mat* A, const void* x, void* out, const Epi& e, cudaStream_
 void launch_halo_pack(ppf_mat* A, const void* x, cudaStream_t st);
 // the second output of an Epi with acc set, from a completed `out` (x: the SpMV input)
 void launch_acc(ppf_mat* A, const void* x, const void* out, const Epi& e, cudaStream_t st);
-// two chained SpMVs in one launch (pair codes; kernels.cu sellp_pair_kernel)
-size_t spmv_pair_sync_bytes(int64_t n);
-bool spmv_pair_ok(const ppf_mat* A);
-void launch_spmv_pair(ppf_mat* A, const void* x1, void* out1, const Epi& e1, void* out2, const Epi& e2,
-                      void* sync, cudaStream_t st);
 // recv: the receive buffer to read (null: A->d_recv)
 void launch_halo_apply(ppf_mat* A, void* out, const double* s_ax, cudaStream_t st,
                        const void* recv = nullptr, const unsigned* recv_sel = nullptr);

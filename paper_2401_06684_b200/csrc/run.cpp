@@ -43,7 +43,7 @@ struct WsLayout {
   int ldh;           // leading dimension of H
   int vcols;         // columns of V
   size_t V, Yb, U, Y, T0, T1, T2, XA, TSQ, W2, H, hbuf, gbuf, ybuf, ybuf2, scal, partials,
-      counter, raw, sync2, total;
+      counter, raw, total;
   int max_blocks;
   int max_vals;
 };
@@ -96,8 +96,6 @@ WsLayout ws_layout(int64_t n, ppf_dtype dt, int m_max, int num_sms, int shape = 
   o += 256;
   L.raw = o;
   o += al256(size_t(L.max_vals) * 8);
-  L.sync2 = o;   // launch_spmv_pair's counters and block flags
-  o += al256(spmv_pair_sync_bytes(n));
   L.total = o;
   return L;
 }
@@ -324,7 +322,6 @@ struct Runner {
     grid_vec = std::min(L.max_blocks, 4 * c->num_sms);
     grid_cgs = std::min(L.max_blocks, c->num_sms);  // persistent CGS kernel: one CTA per SM
     PPF_CUDA(cudaMemsetAsync(w + L.counter, 0, 256, st));
-    PPF_CUDA(cudaMemsetAsync(w + L.sync2, 0, spmv_pair_sync_bytes(n), st));
     PPF_CUDA(cudaMemsetAsync(w + L.H, 0, size_t(L.ldh) * (m_max + 1) * sc, st));
     // pinned host staging: H (and beta0), then two coefficient-vector slots;
     // grown on demand (the context keeps the largest)
@@ -448,39 +445,6 @@ struct Runner {
     }
   }
 
-  // A chain of SpMVs, each reading the previous one's output (Clenshaw):
-  // consecutive calls go two at a time through launch_spmv_pair (one launch
-  // sweeping both as a wavefront through L2, bitwise the same results) where
-  // the operator allows it (pair codes, one rank); else one launch each.
-  struct ChainCall {
-    const void* x;
-    void* out;
-    Epi e;
-  };
-  void chain(const std::vector<ChainCall>& cs) {
-    const bool pairs = !rec && power == 1 && spmv_pair_ok(A);
-    size_t i = 0;
-    while (i < cs.size()) {
-      const ChainCall& a = cs[i];
-      if (pairs && i + 1 < cs.size() && cs[i + 1].x == a.out && !a.e.acc && !cs[i + 1].e.acc &&
-          !a.e.xe && !cs[i + 1].e.xe) {
-        const ChainCall& b = cs[i + 1];
-        // algorithmic bytes of the pair: the codes once (step 2 finds them in
-        // L2), x1, z1, u1 read and out1, out2 written once; step 2's x (= out1)
-        // and any of its z, u already read by step 1 come from L2
-        double vecs = 3.0 + (a.e.z ? 1 : 0) + (a.e.u ? 1 : 0);
-        if (b.e.z && b.e.z != a.x && b.e.z != a.e.z && b.e.z != a.e.u) vecs += 1;
-        if (b.e.u && b.e.u != a.x && b.e.u != a.e.z && b.e.u != a.e.u) vecs += 1;
-        const double bytes = double(A->nnz) + double(sc) * double(n) * vecs;
-        timed(0, bytes, [&] { launch_spmv_pair(A, a.x, a.out, a.e, b.out, b.e, vec(L.sync2), st); });
-        i += 2;
-      } else {
-        spmv(a.x, a.out, a.e);
-        i += 1;
-      }
-    }
-  }
-
   // out = q(A) in.  T0..T2 rotation buffers; in/out distinct from them.
   void apply_q(const void* in, void* out) {
     void* T[3] = {vec(L.T0), vec(L.T1), vec(L.T2)};
@@ -496,28 +460,26 @@ struct Runner {
         spmv(in, out, epi(alpha * c[1], beta * c[1] + c[0], 0.0, nullptr, 0.0, nullptr));
         return;
       }
-      std::vector<ChainCall> cs;
       // b_{d-1} = 2 Ahat (c_d u) + c_{d-1} u
-      cs.push_back({in, T[0], epi(2.0 * alpha * c[d], 2.0 * beta * c[d] + c[d - 1], 0.0, nullptr, 0.0,
-                                  nullptr)});
+      spmv(in, T[0], epi(2.0 * alpha * c[d], 2.0 * beta * c[d] + c[d - 1], 0.0, nullptr, 0.0,
+                         nullptr));
       // index of buffers holding b_{i+1} (cur) and b_{i+2} (prev); b_d = c_d u is implicit
       int cur = 0, prev = -1;
       for (int i = d - 2; i >= 1; --i) {
         int nxt = 0;
         while (nxt == cur || nxt == prev) ++nxt;
         if (prev < 0)  // b_{i+2} = b_d = c_d u
-          cs.push_back({T[cur], T[nxt], epi(2.0 * alpha, 2.0 * beta, 0.0, nullptr, c[i] - c[d], in)});
+          spmv(T[cur], T[nxt], epi(2.0 * alpha, 2.0 * beta, 0.0, nullptr, c[i] - c[d], in));
         else
-          cs.push_back({T[cur], T[nxt], epi(2.0 * alpha, 2.0 * beta, -1.0, T[prev], c[i], in)});
+          spmv(T[cur], T[nxt], epi(2.0 * alpha, 2.0 * beta, -1.0, T[prev], c[i], in));
         prev = cur;
         cur = nxt;
       }
       // out = Ahat b_1 - b_2 + c_0 u
       if (prev < 0)
-        cs.push_back({T[cur], out, epi(alpha, beta, 0.0, nullptr, c[0] - c[d], in)});
+        spmv(T[cur], out, epi(alpha, beta, 0.0, nullptr, c[0] - c[d], in));
       else
-        cs.push_back({T[cur], out, epi(alpha, beta, -1.0, T[prev], c[0], in)});
-      chain(cs);
+        spmv(T[cur], out, epi(alpha, beta, -1.0, T[prev], c[0], in));
     } else if (q->newton_eval == 2) {
       // real conjugate-pair form (real_pair_form): P_0 = v, P_{j+1} =
       // (A - a_j) P_j [+ b_j^2 P_{j-1}], out = sum c_j P_j carried as the
