@@ -651,8 +651,17 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
   };
   // (pair codes: their own slice pointers, width in the low bits)
   up(L.ptr, (p->enc == PPF_ENC_PAIR8 ? p->diag.pptr : p->diag.ptr).data(), p->diag.ptr.size() * 8);
+  // (pair codes of a table of <= 16 pairs go up pre-multiplied by 16, see
+  // ppf_mat::code_scaled; PPF_SELLP_SCALED=0 keeps them as indices)
+  const char* scv = std::getenv("PPF_SELLP_SCALED");
+  const bool scaled = p->enc == PPF_ENC_PAIR8 && p->diag.tab_off.size() <= 16 && !(scv && scv[0] == '0');
+  std::vector<uint8_t> code16;
+  if (scaled) {
+    code16.resize(p->diag.code8.size());
+    for (size_t i = 0; i < code16.size(); ++i) code16[i] = uint8_t(p->diag.code8[i] << 4);
+  }
   if (p->enc == PPF_ENC_PAIR8) {
-    up(L.col, p->diag.code8.data(), p->diag.code8.size());
+    up(L.col, scaled ? code16.data() : p->diag.code8.data(), p->diag.code8.size());
     up(L.cb, p->diag.tab_off.data(), p->diag.tab_off.size() * 4);
     up(L.val, p->diag.tab_val.data(), p->diag.tab_val.size() * 8);
   } else {
@@ -704,6 +713,7 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     m->d_tab_off = reinterpret_cast<const int32_t*>(b + L.cb);
     m->d_tab_val = reinterpret_cast<const double*>(b + L.val);
     m->ntab = int(p->diag.tab_off.size());
+    m->code_scaled = scaled;
     for (int i = 0; i < m->ntab && i < 32; ++i) {
       m->h_tab_val[i] = p->diag.tab_val[size_t(i)];
       m->h_tab_off[i] = p->diag.tab_off[size_t(i)];

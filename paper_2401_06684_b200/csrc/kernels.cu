@@ -472,11 +472,37 @@ struct PairTab32 {
   PairRec p[32];
 };
 
+// a pair's record from its code: an index, or (SC, ppf_mat::code_scaled) the
+// record's byte offset (16 x index), so the lookup needs no scaling
+template <bool SC>
+__device__ __forceinline__ const PairRec& crec(const PairTab32& ct, int e) {
+  if constexpr (SC) return *reinterpret_cast<const PairRec*>(reinterpret_cast<const char*>(ct.p) + e);
+  else return ct.p[e];
+}
+template <bool SC>
+__device__ __forceinline__ double2 srec(const double2* s_tab, int e) {
+  if constexpr (SC) return *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(s_tab) + e);
+  else return s_tab[e];
+}
+// codes of column j (0..7 in the chunk) for the lane's rows 0 and 1: bytes
+// 2j, 2j + 1 of the chunk
+template <bool SC>
+__device__ __forceinline__ void pair_codes(const uint32_t* qw, int j, int& e0, int& e1) {
+  if constexpr (SC) {   // one PRMT each (byte into a zeroed word)
+    e0 = int(__byte_perm(qw[j >> 1], 0u, (j & 1) ? 0x4442u : 0x4440u));
+    e1 = int(__byte_perm(qw[j >> 1], 0u, (j & 1) ? 0x4443u : 0x4441u));
+  } else {
+    const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
+    e0 = int(wd & 0xffu);
+    e1 = int((wd >> 8) & 0xffu);
+  }
+}
+
 // NK columns of one lane's chunk (codes in q: byte 2j + r = column j, row r):
 // all 2 NK gathers, then the FMAs in column order.  TAIL (the last slice):
 // columns clamped to n - 1 for the padding pairs of lanes past n; elsewhere
 // the gather address is the row's x address plus the pair's byte offset.
-template <int NK, bool CT, bool TAIL>
+template <int NK, bool CT, bool TAIL, bool SC>
 __device__ __forceinline__ void pair_chunk(const uint4 q, const double* __restrict__ x, int r0i, int nm1,
                                            const PairTab32& ct, const double2* s_tab, double& a0,
                                            double& a1) {
@@ -486,30 +512,28 @@ __device__ __forceinline__ void pair_chunk(const uint4 q, const double* __restri
   const char* xr = reinterpret_cast<const char*>(x + r0i);
 #pragma unroll
   for (int j = 0; j < NK; ++j) {
-    const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
-    e0[j] = int(wd & 0xffu);
-    e1[j] = int((wd >> 8) & 0xffu);
+    pair_codes<SC>(qw, j, e0[j], e1[j]);
     if constexpr (CT && !TAIL) {
-      g0[j] = __ldg(reinterpret_cast<const double*>(xr + ct.p[e0[j]].o8));
-      g1[j] = __ldg(reinterpret_cast<const double*>(xr + 8 + ct.p[e1[j]].o8));
+      g0[j] = __ldg(reinterpret_cast<const double*>(xr + crec<SC>(ct, e0[j]).o8));
+      g1[j] = __ldg(reinterpret_cast<const double*>(xr + 8 + crec<SC>(ct, e1[j]).o8));
     } else {
-      const int o0 = CT ? ct.p[e0[j]].o8 / 8 : pair_off(s_tab[e0[j]]);
-      const int o1 = CT ? ct.p[e1[j]].o8 / 8 : pair_off(s_tab[e1[j]]);
+      const int o0 = CT ? crec<SC>(ct, e0[j]).o8 / 8 : pair_off(srec<SC>(s_tab, e0[j]));
+      const int o1 = CT ? crec<SC>(ct, e1[j]).o8 / 8 : pair_off(srec<SC>(s_tab, e1[j]));
       g0[j] = __ldg(x + min(r0i + o0, nm1));
       g1[j] = __ldg(x + min(r0i + 1 + o1, nm1));
     }
   }
 #pragma unroll
   for (int j = 0; j < NK; ++j) {
-    a0 = fma(CT ? ct.p[e0[j]].v : s_tab[e0[j]].x, g0[j], a0);
-    a1 = fma(CT ? ct.p[e1[j]].v : s_tab[e1[j]].x, g1[j], a1);
+    a0 = fma(CT ? crec<SC>(ct, e0[j]).v : srec<SC>(s_tab, e0[j]).x, g0[j], a0);
+    a1 = fma(CT ? crec<SC>(ct, e1[j]).v : srec<SC>(s_tab, e1[j]).x, g1[j], a1);
   }
 }
 
 // CT: the table (<= 32 pairs) comes by value as a kernel parameter, so the
 // lookups are constant-cache loads (uniform across the warp where a column's
 // codes agree) instead of shared-memory loads on the L1 data pipe
-template <int KS, bool ACC = false, bool CT = false>
+template <int KS, bool ACC = false, bool CT = false, bool SC = false>
 __global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t n,
                                                     const int64_t* __restrict__ sptr,
                                                     const uint8_t* __restrict__ code8,
@@ -564,8 +588,8 @@ __global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t 
       switch (nk) {
 #define PPF_PC(NK)                                                             \
   case NK:                                                                     \
-    if (tail) pair_chunk<NK, CT, true>(q, x, r0i, nm1, ct, s_tab, a0, a1);     \
-    else pair_chunk<NK, CT, false>(q, x, r0i, nm1, ct, s_tab, a0, a1);         \
+    if (tail) pair_chunk<NK, CT, true, SC>(q, x, r0i, nm1, ct, s_tab, a0, a1); \
+    else pair_chunk<NK, CT, false, SC>(q, x, r0i, nm1, ct, s_tab, a0, a1);     \
     break;
         PPF_PC(1) PPF_PC(2) PPF_PC(3) PPF_PC(4) PPF_PC(5) PPF_PC(6) PPF_PC(7) PPF_PC(8)
 #undef PPF_PC
@@ -580,13 +604,14 @@ __global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t 
       for (int j = 0; j < 8; ++j) {
         const int k = 8 * c + j;
         if (k < k0 || k >= k1) continue;
-        const uint32_t wd = qw[j >> 1] >> (16 * (j & 1));
-        const int e0 = int(wd & 0xffu), e1 = int((wd >> 8) & 0xffu);
+        int e0, e1;
+        pair_codes<SC>(qw, j, e0, e1);
         if constexpr (CT) {
-          a0 = fma(ct.p[e0].v, __ldg(x + min(r0i + ct.p[e0].o8 / 8, nm1)), a0);
-          a1 = fma(ct.p[e1].v, __ldg(x + min(r0i + 1 + ct.p[e1].o8 / 8, nm1)), a1);
+          const PairRec &r0 = crec<SC>(ct, e0), &r1 = crec<SC>(ct, e1);
+          a0 = fma(r0.v, __ldg(x + min(r0i + r0.o8 / 8, nm1)), a0);
+          a1 = fma(r1.v, __ldg(x + min(r0i + 1 + r1.o8 / 8, nm1)), a1);
         } else {
-          const double2 p0 = s_tab[e0], p1 = s_tab[e1];
+          const double2 p0 = srec<SC>(s_tab, e0), p1 = srec<SC>(s_tab, e1);
           a0 = fma(p0.x, __ldg(x + min(r0i + pair_off(p0), nm1)), a0);
           a1 = fma(p1.x, __ldg(x + min(r0i + 1 + pair_off(p1), nm1)), a1);
         }
@@ -1384,12 +1409,15 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
              reinterpret_cast<const double*>(val), xt, ot, et, has_x, A->d_d16, A->d_cb)
 #define PPF_S2(K) PPF_S2E(K, false)
 #define PPF_S2D(K) PPF_S2E(K, true)
-#define PPF_SP(K)                                                                              \
-  launch_pdl(sellp_kernel<K, ACC, false>, bp, tp, st, A->nslices, A->n_local, A->d_ptr,        \
+#define PPF_SPX(K, CTB, SCB)                                                                   \
+  launch_pdl(sellp_kernel<K, ACC, CTB, SCB>, bp, tp, st, A->nslices, A->n_local, A->d_ptr,     \
              A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x, ct)
-#define PPF_SPC(K)                                                                             \
-  launch_pdl(sellp_kernel<K, ACC, true>, bp, tp, st, A->nslices, A->n_local, A->d_ptr,         \
-             A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x, ct)
+#define PPF_SP(K)                           \
+  if (A->code_scaled) PPF_SPX(K, false, true); \
+  else PPF_SPX(K, false, false)
+#define PPF_SPC(K)                          \
+  if (A->code_scaled) PPF_SPX(K, true, true); \
+  else PPF_SPX(K, true, false)
       if (A->d_code8) {
         PairTab32 ct{};
         // (offsets kept as byte offsets in int32: |col - row| < 2^28)
@@ -1424,6 +1452,7 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
 #undef PPF_S2D
 #undef PPF_SP
 #undef PPF_SPC
+#undef PPF_SPX
 #undef PPF_S2E
       post_launch("sell2_kernel");
       return;

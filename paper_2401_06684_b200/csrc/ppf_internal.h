@@ -169,6 +169,9 @@ struct ppf_mat {
   // value, so its lookups go through the constant cache, not the L1 data pipe
   double h_tab_val[32] = {};
   int h_tab_off[32] = {};
+  // codes uploaded pre-multiplied by 16 (tables of <= 16 pairs): each code byte
+  // is then the byte offset of its 16-B record, one PRMT from the code word
+  bool code_scaled = false;
   int csr_group;            // lanes per row for the CSR kernel
   int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks
   int64_t sell_heavy = 0;   // leading slices given a whole block each (see sell_heavy_prefix)
