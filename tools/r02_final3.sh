@@ -1,7 +1,7 @@
 # Round-2 session-3 verification batch (current pair-record code): build, smoke,
 # the full GPU suite, the default bench line, the C4 launch list and one ncu
 # --set full capture of the pair-code SpMV.  Usage on the GPU box: bash tools/r02_final3.sh
-O=gpurun_out/r02s3
+O=gpurun_out/${OUT:-r02s3}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build_rc=$?
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('SMOKE OK')" > $O/smoke.log 2>&1; echo smoke_rc=$?
