@@ -142,16 +142,19 @@ def test_pair_codes_bitwise(ctx, shape, ks):
     assert np.all(np.abs(outs["pair8"][0] - ref) <= 1e-14 * absA + 1e-300)
 
 
+@pytest.mark.parametrize("scaled", ["1", "0"])
 @pytest.mark.parametrize("ctab", ["1", "0"])
-@pytest.mark.parametrize("nvals", [3, 10, 40])
-def test_pair_codes_table_sizes(ctx, nvals, ctab, monkeypatch):
+@pytest.mark.parametrize("nvals", [2, 3, 10, 40])
+def test_pair_codes_table_sizes(ctx, nvals, ctab, scaled, monkeypatch):
     """Pair tables beyond the 32 entries passed as a kernel parameter are
     held in shared memory (and PPF_SELLP_CTAB=0 forces that path for small
     ones): a banded matrix (offsets -3..3, ragged n = 5003) whose values are
-    drawn from `nvals` levels -- 7 * nvals pairs + padding: 22 (parameter
+    drawn from `nvals` levels -- 7 * nvals pairs + padding: 15 (codes
+    uploaded as record byte offsets unless PPF_SELLP_SCALED=0), 22 (parameter
     table), 71 (shared-memory table), 281 (over the 256-entry table: the
     deltas) -- against the explicit layout (bitwise) and SciPy."""
     monkeypatch.setenv("PPF_SELLP_CTAB", ctab)
+    monkeypatch.setenv("PPF_SELLP_SCALED", scaled)
     n = 5003
     rng = np.random.default_rng(nvals)
     levels = rng.standard_normal(nvals)
