@@ -302,7 +302,7 @@ def run_reference(args):
     workload, metric and config as the GPU arm, each step ONE full oracle run
     (oracle_run).  A full run takes minutes at the BASELINE sizes (C4: ~3-4
     min), so the arm runs as many steps as fit in PPF_REF_BUDGET_S seconds
-    (default 600; at least one), with no warm-up (host code has nothing to
+    (default 300; at least one), with no warm-up (host code has nothing to
     warm), and reports the steps it ran.  Under torchrun only rank 0 works."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -315,7 +315,7 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "the oracle arm covers the configs' own method only (no variant flags)"}))
         return
-    budget = float(os.environ.get("PPF_REF_BUDGET_S", "600"))
+    budget = float(os.environ.get("PPF_REF_BUDGET_S", "300"))
     times, t_all = [], time.perf_counter()
     m = mvms = threads = None
     while len(times) < args.steps:
