@@ -199,6 +199,19 @@ ppf_status ppf_plan_index_bits(const ppf_plan* plan, int* bits);
  * reports the layout in force: 8 (pair codes), 16 or 32. */
 ppf_status ppf_plan_encoding(const ppf_plan* plan, int* enc, int* ntab);
 ppf_status ppf_plan_set_encoding(ppf_plan* plan, int enc);
+/* ppf_plan_slice_schedule: the order in which the pair-code SpMV (P:131-146's
+ * mat-vec on PPF_ENC_PAIR8) hands SELL slices to thread blocks: warp w of block
+ * b takes slice out[8 b + w] (-1: none).  Blocks are tiles of slices whose rows
+ * gather from one another (the pair table's two smallest |column - row| >= 64,
+ * a stencil's +-N and +-N^2 neighbours), so their x gathers share L1 lines;
+ * every slice appears exactly once.  Scheduling only: results are bitwise
+ * those of the in-order launch.  *count = number of entries (a multiple of 8;
+ * 0 = slices in order, 8 per block: no pair codes, no far offsets, fewer than
+ * 64 slices, or PPF_SELLP_TILE=0 at plan time; PPF_SELLP_TILE=TYxTZ with
+ * TY * TZ = 8 picks the tile).  `out` (host, may be NULL) receives
+ * min(cap, *count) entries. */
+ppf_status ppf_plan_slice_schedule(const ppf_plan* plan, int32_t* out, int64_t cap,
+                                   int64_t* count);
 ppf_status ppf_plan_halo_count(const ppf_plan* plan, int peer, int64_t* count);
 ppf_status ppf_plan_halo_recv(const ppf_plan* plan, int peer, int64_t* global_idx);
 ppf_status ppf_plan_set_halo_send(ppf_plan* plan, int peer, int64_t count,

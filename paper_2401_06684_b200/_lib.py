@@ -68,6 +68,7 @@ SIGNATURES = {
     "ppf_plan_halo_count": (C.c_int, [vp, C.c_int, i64p]),
     "ppf_plan_index_bits": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "ppf_plan_encoding": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "ppf_plan_slice_schedule": (C.c_int, [vp, C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_int64)]),
     "ppf_plan_set_encoding": (C.c_int, [vp, C.c_int]),
     "ppf_plan_halo_recv": (C.c_int, [vp, C.c_int, i64p]),
     "ppf_plan_set_halo_send": (C.c_int, [vp, C.c_int, C.c_int64, i64p]),

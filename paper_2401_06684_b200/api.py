@@ -174,6 +174,17 @@ class Plan:
         check(_lib().ppf_plan_encoding(self.h, C.byref(e), C.byref(t)))
         return self.ENCODINGS[e.value], t.value
 
+    def slice_schedule(self) -> np.ndarray:
+        """ppf_plan_slice_schedule: slice of warp w of block b at [8 b + w] (-1: none);
+        empty = slices in order."""
+        cnt = C.c_int64()
+        check(_lib().ppf_plan_slice_schedule(self.h, None, 0, C.byref(cnt)))
+        out = np.empty(cnt.value, dtype=np.int32)
+        if cnt.value:
+            check(_lib().ppf_plan_slice_schedule(
+                self.h, out.ctypes.data_as(C.POINTER(C.c_int32)), cnt.value, C.byref(cnt)))
+        return out
+
     def set_encoding(self, enc: str) -> "Plan":
         """ppf_plan_set_encoding: select a wider layout than the one chosen."""
         check(_lib().ppf_plan_set_encoding(self.h, self.ENCODINGS.index(enc)))

@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -11,6 +12,12 @@
 #include <memory>
 
 #include "ppf_internal.h"
+
+// default tile of the pair-code slice schedule (0 x 0: slices in order)
+#ifndef PPF_SELLP_TILE_TY
+#define PPF_SELLP_TILE_TY 0
+#define PPF_SELLP_TILE_TZ 0
+#endif
 
 namespace ppf {
 
@@ -208,6 +215,71 @@ void ppf_ctx_destroy(ppf_ctx* c) {
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   delete c;
+}
+
+// ---------------------------------------------------------------------------
+// Slice schedule of the pair-code SpMV (HostBlock::sched).  The pair table's
+// offsets say which rows gather from each other: with a1 < a2 the two smallest
+// |col - row| >= C (a 3-D stencil's +-N and +-N^2), slices G1 = a1 / C and
+// G2 = a2 / C apart are y- and z-neighbours.  A block of 8 warps takes a
+// ty x tz tile of such slices (same residue r modulo G1), so most of the +-a1 /
+// +-a2 gathers of its rows fall on lines another warp of the block also reads
+// (8 consecutive slices of C4 -- two grid lines -- pull 32 quarter-lines of x
+// through L1 for their 8; a 4 x 2 tile pulls 20).  Blocks run r fastest, so
+// neighbouring blocks still stream neighbouring slices.  PPF_SELLP_TILE =
+// "0" (none) | "TYxTZ" (TY * TZ = 8).  Scheduling only.
+// ---------------------------------------------------------------------------
+static void build_slice_schedule(HostBlock& B, int C) {
+  B.sched.clear();
+  int ty = PPF_SELLP_TILE_TY, tz = PPF_SELLP_TILE_TZ;
+  if (const char* ev = std::getenv("PPF_SELLP_TILE")) {
+    if (ev[0] == '0') return;
+    int a = 0, b = 0;
+    if (std::sscanf(ev, "%dx%d", &a, &b) == 2 && a > 0 && b > 0 && a * b == 8) {
+      ty = a;
+      tz = b;
+    }
+  }
+  if (ty <= 0) return;
+  std::vector<int64_t> far;
+  for (int32_t o : B.tab_off) {
+    const int64_t a = o < 0 ? -int64_t(o) : int64_t(o);
+    if (a >= C) far.push_back(a);
+  }
+  std::sort(far.begin(), far.end());
+  far.erase(std::unique(far.begin(), far.end()), far.end());
+  const int64_t ns = B.nslices;
+  if (far.empty() || ns < 64) return;
+  const int64_t G1 = std::max<int64_t>(1, (far[0] + C / 2) / C);
+  int64_t G2 = ns;   // one plane: a 2-D stencil, tiles of 8 along y
+  for (size_t i = 1; i < far.size(); ++i) {
+    const int64_t g = (far[i] + C / 2) / C;
+    if (g >= 2 * G1 * ty) {
+      G2 = std::min(g, ns);
+      break;
+    }
+  }
+  if (G2 >= ns) {
+    ty = 8;
+    tz = 1;
+  }
+  const int64_t nz = (ns + G2 - 1) / G2, ny = (G2 + G1 - 1) / G1;
+  B.sched.reserve(size_t(ns + ns / 8));
+  for (int64_t zt = 0; zt * tz < nz; ++zt)
+    for (int64_t yt = 0; yt * ty < ny; ++yt)
+      for (int64_t r = 0; r < G1; ++r) {
+        int32_t blk[8];
+        bool any = false;
+        for (int wz = 0; wz < tz; ++wz)
+          for (int wy = 0; wy < ty; ++wy) {
+            const int64_t z = zt * tz + wz, y = yt * ty + wy, in = y * G1 + r;
+            const int64_t sl = z * G2 + in;
+            const bool ok = z < nz && y < ny && in < G2 && sl < ns;
+            blk[wz * ty + wy] = ok ? int32_t(sl) : -1;
+            any |= ok;
+          }
+        if (any) B.sched.insert(B.sched.end(), blk, blk + 8);
+      }
 }
 
 // ---------------------------------------------------------------------------
@@ -498,11 +570,24 @@ ppf_status ppf_plan_create(ppf_dtype dtype, int64_t n_global, int nranks, int ra
         B.tab_off.swap(toff);
         B.tab_val.swap(tval);
         p->enc = PPF_ENC_PAIR8;
+        build_slice_schedule(B, C);
       }
     }
   }
   p->sends_set = (nranks == 1);
   *out = guard.release();
+  PPF_API_END
+}
+
+ppf_status ppf_plan_slice_schedule(const ppf_plan* p, int32_t* out, int64_t cap, int64_t* count) {
+  PPF_API_BEGIN
+  PPF_REQUIRE(p && count, "NULL argument");
+  PPF_REQUIRE(cap >= 0, "negative capacity");
+  const std::vector<int32_t> none;
+  const std::vector<int32_t>& sc = p->enc == PPF_ENC_PAIR8 ? p->diag.sched : none;
+  *count = int64_t(sc.size());
+  if (out)
+    for (int64_t i = 0; i < cap && i < *count; ++i) out[i] = sc[size_t(i)];
   PPF_API_END
 }
 
@@ -562,7 +647,7 @@ ppf_status ppf_plan_set_halo_send(ppf_plan* p, int peer, int64_t count, const in
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t ptr, col, cb, val, perm, hrows, hptr, hcol, hval, recv, send, sidx, total;
+  size_t ptr, col, cb, val, sched, perm, hrows, hptr, hcol, hval, recv, send, sidx, total;
 };
 
 static Layout layout_of(const ppf_plan* p) {
@@ -579,6 +664,8 @@ static Layout layout_of(const ppf_plan* p) {
     o += al256(p->diag.tab_off.size() * 4);
     L.val = o;
     o += al256(p->diag.tab_val.size() * 8);
+    L.sched = o;
+    o += al256(p->diag.sched.size() * 4);
   } else {
     if (p->enc == PPF_ENC_EXPLICIT) {
       o += al256(p->diag.col.size() * 4);
@@ -664,6 +751,7 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     up(L.col, scaled ? code16.data() : p->diag.code8.data(), p->diag.code8.size());
     up(L.cb, p->diag.tab_off.data(), p->diag.tab_off.size() * 4);
     up(L.val, p->diag.tab_val.data(), p->diag.tab_val.size() * 8);
+    up(L.sched, p->diag.sched.data(), p->diag.sched.size() * 4);
   } else {
     if (p->enc == PPF_ENC_EXPLICIT) {
       up(L.col, p->diag.col.data(), p->diag.col.size() * 4);
@@ -714,6 +802,10 @@ ppf_status ppf_mat_create(ppf_ctx* ctx, const ppf_plan* p, void* buf, size_t byt
     m->d_tab_val = reinterpret_cast<const double*>(b + L.val);
     m->ntab = int(p->diag.tab_off.size());
     m->code_scaled = scaled;
+    if (!p->diag.sched.empty()) {
+      m->d_sched = reinterpret_cast<const int32_t*>(b + L.sched);
+      m->sched_blocks = int(p->diag.sched.size() / 8);
+    }
     for (int i = 0; i < m->ntab && i < 32; ++i) {
       m->h_tab_val[i] = p->diag.tab_val[size_t(i)];
       m->h_tab_off[i] = p->diag.tab_off[size_t(i)];

@@ -541,13 +541,17 @@ __global__ void __launch_bounds__(256, 8) sellp_kernel(int64_t nslices, int64_t 
                                                     const double* __restrict__ tab_val, int ntab,
                                                     const double* __restrict__ x,
                                                     double* __restrict__ out, EpiT<double> e,
-                                                    bool has_x, const __grid_constant__ PairTab32 ct) {
+                                                    bool has_x, const __grid_constant__ PairTab32 ct,
+                                                    const int32_t* __restrict__ sched) {
   __shared__ double2 s_tab[CT ? 1 : 256];
   pdl_release();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t slice = int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
+  // (KS = 1 with a slice schedule: the block's warps take a tile of slices
+  // that gather from each other's rows, api.cpp build_slice_schedule)
+  const int64_t slice = (KS == 1 && sched) ? int64_t(__ldg(sched + blockIdx.x * 8 + warp))
+                                           : int64_t(blockIdx.x) * (blockDim.x >> 5) / KS + warp / KS;
   const int part = warp % KS;
-  const bool live = slice < nslices;
+  const bool live = slice >= 0 && slice < nslices;
   double a0 = 0.0, a1 = 0.0;
   int64_t base = 0;
   int k0 = 0, k1 = 0;
@@ -1411,7 +1415,7 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
 #define PPF_S2D(K) PPF_S2E(K, true)
 #define PPF_SPX(K, CTB, SCB)                                                                   \
   launch_pdl(sellp_kernel<K, ACC, CTB, SCB>, bp, tp, st, A->nslices, A->n_local, A->d_ptr,     \
-             A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x, ct)
+             A->d_code8, A->d_tab_off, A->d_tab_val, A->ntab, xt, ot, et, has_x, ct, sch)
 #define PPF_SP(K)                           \
   if (A->code_scaled) PPF_SPX(K, false, true); \
   else PPF_SPX(K, false, false)
@@ -1435,7 +1439,8 @@ static void launch_sell(ppf_mat* A, const T* xt, T* ot, const T* val, const EpiT
         // within 2%)
         const int tp = 256;
         const int64_t spbp = (tp / 32) / KS;
-        const int bp = int((A->nslices + spbp - 1) / spbp);
+        const int32_t* sch = KS == 1 ? A->d_sched : nullptr;
+        const int bp = sch ? A->sched_blocks : int((A->nslices + spbp - 1) / spbp);
         if (use_ct) {
           PPF_KS(PPF_SPC)
         } else {

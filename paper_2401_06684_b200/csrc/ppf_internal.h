@@ -116,6 +116,12 @@ struct HostBlock {
   std::vector<uint8_t> code8;
   std::vector<int32_t> tab_off;
   std::vector<double> tab_val;
+  // slice schedule of the pair-code SpMV (optional): warp w of block b takes
+  // slice sched[8 b + w] (-1: none).  Blocks are (y, z) tiles of slices whose
+  // rows are each other's far neighbours (the pair table's two smallest
+  // offsets >= C), so their x gathers meet in the SM's L1; empty = slices in
+  // order, 8 per block.  Scheduling only: results are bitwise the same.
+  std::vector<int32_t> sched;
 };
 
 struct HostHalo {
@@ -172,6 +178,8 @@ struct ppf_mat {
   // codes uploaded pre-multiplied by 16 (tables of <= 16 pairs): each code byte
   // is then the byte offset of its 16-B record, one PRMT from the code word
   bool code_scaled = false;
+  const int32_t* d_sched = nullptr;  // slice schedule (see HostBlock::sched), 8 per block
+  int sched_blocks = 0;
   int csr_group;            // lanes per row for the CSR kernel
   int sell_ks;              // warps per SELL slice (1, 2, 4, 8), see auto_sell_ks
   int64_t sell_heavy = 0;   // leading slices given a whole block each (see sell_heavy_prefix)

@@ -142,6 +142,37 @@ def test_pair_codes_bitwise(ctx, shape, ks):
     assert np.all(np.abs(outs["pair8"][0] - ref) <= 1e-14 * absA + 1e-300)
 
 
+@pytest.mark.parametrize("tile", ["4x2", "8x1", "2x4"])
+@pytest.mark.parametrize("shape", [(64, 3, (10.0, 10.0, 10.0)), (47, 3, (10.0, 5.0, 2.5)), (90, 2, None),
+                                   (21, 3, None)])
+def test_pair_codes_slice_schedule_bitwise(ctx, shape, tile, monkeypatch):
+    """The slice schedule (ppf_plan_slice_schedule: blocks take tiles of slices
+    that gather from one another) only reorders which warp computes which
+    slice: SpMV and the fused Clenshaw chain are bitwise those of the in-order
+    launch and of the explicit layout, for aligned and ragged grids, 2-D and
+    3-D, and every tile shape."""
+    N, dim, beta = shape
+    A = ops.laplacian(N, dim) if beta is None else ops.convdiff(N, 3, beta)
+    rng = np.random.default_rng(N + dim)
+    x = rng.standard_normal(A.n)
+    outs = {}
+    for name, env in (("tiled", tile), ("inorder", "0")):
+        monkeypatch.setenv("PPF_SELLP_TILE", env)
+        plan = pp.Plan.from_csr(A, fmt="sell", C_=64)
+        assert plan.encoding()[0] == "pair8"
+        assert (len(plan.slice_schedule()) > 0) == (name == "tiled")
+        M = pp.Matrix(ctx, plan)
+        yd = torch.full_like(dev(x), float("nan"))
+        M.spmv(dev(x), yd)
+        q = pp.Poly.chebyshev(0.5, 20.0, 7)
+        outs[name] = (host(yd), host(q.apply(ctx, M, dev(x))))
+    assert np.array_equal(outs["tiled"][0], outs["inorder"][0])
+    assert np.array_equal(outs["tiled"][1], outs["inorder"][1])
+    ref = A.to_scipy() @ x
+    absA = abs(A.to_scipy()) @ np.abs(x)
+    assert np.all(np.abs(outs["tiled"][0] - ref) <= 1e-14 * absA + 1e-300)
+
+
 @pytest.mark.parametrize("scaled", ["1", "0"])
 @pytest.mark.parametrize("ctab", ["1", "0"])
 @pytest.mark.parametrize("nvals", [2, 3, 10, 40])

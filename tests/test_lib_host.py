@@ -477,3 +477,43 @@ def test_plan_pair_codes_choice(monkeypatch):
             assert enc[1] == k
     monkeypatch.setenv("PPF_PAIR8", "0")
     assert Plan.from_csr(ops.laplacian(30, 3), fmt="sell", C_=64).encoding()[0] == "delta16"
+
+
+def test_pair_code_slice_schedule(monkeypatch):
+    """ppf_plan_slice_schedule: with PPF_SELLP_TILE=TYxTZ every slice appears
+    exactly once, 8 entries per block, and the live warps of a block are slices
+    G1 = N / 64 (y-neighbours) and G2 = N^2 / 64 (z-neighbours) apart; a 2-D
+    stencil (one far offset) gets tiles of 8 along y; ragged sizes (N not a
+    multiple of 64) still cover every slice once; PPF_SELLP_TILE=0, a wider
+    layout or a small block give the in-order launch (empty schedule)."""
+    monkeypatch.setenv("PPF_SELLP_TILE", "4x2")
+    N = 64
+    A = ops.convdiff(N, 3, (10.0, 10.0, 10.0))
+    p = Plan.from_csr(A, fmt="sell", C_=64)
+    s = p.slice_schedule()
+    ns = N**3 // 64
+    assert len(s) % 8 == 0 and len(s) == ns           # N = 64: no dead warps
+    assert np.array_equal(np.sort(s), np.arange(ns))
+    blk = s.reshape(-1, 8)
+    G1, G2 = N // 64, N * N // 64
+    assert np.array_equal(blk[:, 1] - blk[:, 0], np.full(len(blk), G1))
+    assert np.array_equal(blk[:, 4] - blk[:, 0], np.full(len(blk), G2))
+    p.set_encoding("delta16")
+    assert len(p.slice_schedule()) == 0
+    for tile in ("8x1", "2x4", "1x8"):
+        monkeypatch.setenv("PPF_SELLP_TILE", tile)
+        s = Plan.from_csr(A, fmt="sell", C_=64).slice_schedule()
+        assert np.array_equal(np.sort(s[s >= 0]), np.arange(ns)), tile
+    monkeypatch.setenv("PPF_SELLP_TILE", "4x2")
+    for B in (ops.convdiff(40, 3, (10.0, 10.0, 10.0)), ops.laplacian(30, 3), ops.laplacian(100, 2)):
+        s = Plan.from_csr(B, fmt="sell", C_=64).slice_schedule()
+        nsb = (B.n + 63) // 64
+        assert len(s) % 8 == 0 and len(s) >= nsb
+        assert np.array_equal(np.sort(s[s >= 0]), np.arange(nsb))
+        assert (s >= -1).all() and (s.reshape(-1, 8) >= 0).any(axis=1).all()   # no empty block
+    s2 = Plan.from_csr(ops.laplacian(100, 2), fmt="sell", C_=64).slice_schedule().reshape(-1, 8)
+    full = (s2 >= 0).all(axis=1)
+    assert full.any() and (np.diff(s2[full], axis=1) == round(100 / 64)).all()   # 8 along y
+    assert len(Plan.from_csr(ops.laplacian(32, 2), fmt="sell", C_=64).slice_schedule()) == 0  # 16 slices
+    monkeypatch.setenv("PPF_SELLP_TILE", "0")
+    assert len(Plan.from_csr(A, fmt="sell", C_=64).slice_schedule()) == 0
