@@ -227,7 +227,11 @@ void ppf_ctx_destroy(ppf_ctx* c) {
 // (8 consecutive slices of C4 -- two grid lines -- pull 32 quarter-lines of x
 // through L1 for their 8; a 4 x 2 tile pulls 20).  Blocks run r fastest, so
 // neighbouring blocks still stream neighbouring slices.  PPF_SELLP_TILE =
-// "0" (none) | "TYxTZ" (TY * TZ = 8).  Scheduling only.
+// "0" (none) | "TYxTZ" (TY * TZ = 8).  Scheduling only.  Measured (one B200,
+// SpMV ms per solve, C4 / C3 deg 20): in order 124.8 / 74.5, 4x2 128.4 / 77.5,
+// 8x1 129.5 / 79.0, 2x4 129.6 / 77.6 -- the tiles lose the single ascending
+// front of the in-order launch and the kernel is not bound by L1 misses, so
+// the default (PPF_SELLP_TILE_TY = 0) is no schedule.
 // ---------------------------------------------------------------------------
 static void build_slice_schedule(HostBlock& B, int C) {
   B.sched.clear();
